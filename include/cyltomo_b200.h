@@ -1,0 +1,211 @@
+/*
+ * cyltomo_b200.h -- C-ABI of the B200-native cone-beam projector / SART path.
+ *
+ * Drop-in seam: the reference's kernel boundary is the set of numba kernels
+ * in cyltomo/_kernels.py, called with plain arrays and scalars by
+ * cyltomo/projector.py and cyltomo/grid.py.  Every entry point below replaces
+ * one of them (file:line cited per function) or fuses a reference numpy step
+ * (cyltomo/recon.py) into a kernel epilogue.
+ *
+ * Conventions
+ *  - All array arguments are DEVICE pointers owned by the caller, float32
+ *    unless stated (the reference is float64 on the host; the B200 path keeps
+ *    fp32 data and does per-ray setup in fp64 -- see DESIGN.md "Numerics").
+ *  - Cylindrical volumes: mu[n_h][n_theta][n_r], r fastest
+ *    (cyltomo/grid.py:91-93).  Cartesian volumes: mu[n_z][n_y][n_x].
+ *  - Projection stacks / correction images: [views][det_rows][det_cols].
+ *  - Struct arguments passed by pointer are HOST pointers, read during the
+ *    call only.  `views`/`dets` tables are DEVICE arrays (upload once per
+ *    geometry; that keeps every call capturable in a CUDA graph).
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ *    asynchronous; no call synchronises the device.
+ *  - Return value: CT_OK or a negative CT_ERR_*; CT_ERR_CUDA means a launch
+ *    failed -- ct_last_error() gives the CUDA error string.  No exceptions
+ *    cross the ABI.
+ *  - FP entry points OVERWRITE their outputs; BP entry points accumulate or
+ *    overwrite as documented (the reference's backproject_* accumulate).
+ *  - Results are deterministic: no atomics on data, fixed reduction order.
+ */
+#ifndef CYLTOMO_B200_H
+#define CYLTOMO_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CT_ABI_VERSION 1
+
+#define CT_OK 0
+#define CT_ERR_ARG (-1)   /* invalid argument (null pointer, bad size) */
+#define CT_ERR_CUDA (-2)  /* kernel launch / runtime failure */
+
+typedef void *ct_stream_t; /* cudaStream_t */
+
+/* Object-aligned cylindrical grid (cyltomo/grid.py:62-110).  rot is the
+ * row-major object->world rotation R, t the translation (X' = R X + t). */
+typedef struct ct_cyl_grid {
+    int32_t n_h, n_theta, n_r, _pad;
+    double radius, height;
+    double rot[9];
+    double t[3];
+} ct_cyl_grid;
+
+/* World-aligned Cartesian grid (cyltomo/grid.py:139-187). */
+typedef struct ct_cart_grid {
+    int32_t n_z, n_y, n_x, _pad;
+    double voxel_size;
+    double origin[3];
+} ct_cart_grid;
+
+/* Per-view ray basis for the forward projector: source, pixel-(0,0) centre,
+ * per-column and per-row steps.  For cylindrical grids these are already in
+ * the grid-aligned frame (cyltomo/projector.py:83-88); for Cartesian grids
+ * they are world-frame (cyltomo/geometry.py:257-273). */
+typedef struct ct_ray_view {
+    double src[3], origin[3], du[3], dv[3];
+} ct_ray_view;
+
+/* Per-view detector parameters for the back-projector
+ * (cyltomo/projector.py:151-163): principal point, pitch, distances and the
+ * cos/sin of the stage angle. */
+typedef struct ct_det_view {
+    double u0, v0, pitch, sdd, sod, cphi, sphi, _pad;
+} ct_det_view;
+
+/* Ray sampling (cyltomo/projector.py:28-56): step in mm (already resolved),
+ * supersample >= 1, nearest != 0 for nearest-neighbour interpolation. */
+typedef struct ct_sampling {
+    double step;
+    int32_t supersample;
+    int32_t nearest;
+} ct_sampling;
+
+/* Fused SART update (cyltomo/recon.py:105-119):
+ *   touched = den > 0 [&& weights != 0]
+ *   mu[touched] = max(mu + relaxation * w * num / den, 0 if nonneg)
+ * weights may be NULL (unweighted). */
+typedef struct ct_update {
+    float relaxation;
+    int32_t nonneg;
+    const float *weights;
+    float *mu;
+} ct_update;
+
+/* Detector / batch description shared by the batched calls:
+ * view_ids[b] (device, int32) is the global view index of batch slot b; it
+ * selects the entry of `views`/`dets`, of `p_meas` ([P][rows][cols]) and of
+ * `row_thr`.  view_ids may be NULL, meaning slot b == view b. */
+typedef struct ct_batch {
+    int32_t n_batch;
+    int32_t det_rows, det_cols;
+    int32_t _pad;
+    const int32_t *view_ids;
+} ct_batch;
+
+/* ---- library ------------------------------------------------------------ */
+int ct_abi_version(void);
+const char *ct_last_error(void);
+/* Compiled-for architecture string, e.g. "sm_100a". */
+const char *ct_arch(void);
+
+/* ---- forward projection (cyltomo/_kernels.py:238-293 forward_cyl,
+ *      :296-343 forward_cart) ---------------------------------------------- */
+
+/* forward_cyl over a batch of views: out_p / out_w are [n_batch][rows][cols]
+ * (OVERWRITTEN).  out_w = in-support sample count * step / ss^2 (the SART row
+ * sums, cyltomo/projector.py:100-103); out_w may be NULL. */
+int ct_fp_cyl(const float *mu, const ct_cyl_grid *grid, const ct_ray_view *views,
+              const ct_batch *batch, const ct_sampling *sampling,
+              float *out_p, float *out_w, ct_stream_t stream);
+
+int ct_fp_cart(const float *mu, const ct_cart_grid *grid, const ct_ray_view *views,
+               const ct_batch *batch, const ct_sampling *sampling,
+               float *out_p, float *out_w, ct_stream_t stream);
+
+/* FP with the SART correction epilogue (cyltomo/recon.py:96-102):
+ *   corr[b] = (w > row_thr[v]) ? (p_meas[v] - sim) / w : 0,   v = view_ids[b]
+ * row_thr (device, float64, [P]) = ROW_SUM_SKIP_FRACTION * max_row per view
+ * (ct_rowsum_max_*).  corr is [n_batch][rows][cols]. */
+int ct_fp_cyl_correction(const float *mu, const ct_cyl_grid *grid, const ct_ray_view *views,
+                         const ct_batch *batch, const ct_sampling *sampling,
+                         const float *p_meas, const double *row_thr, float *corr,
+                         ct_stream_t stream);
+int ct_fp_cart_correction(const float *mu, const ct_cart_grid *grid, const ct_ray_view *views,
+                          const ct_batch *batch, const ct_sampling *sampling,
+                          const float *p_meas, const double *row_thr, float *corr,
+                          ct_stream_t stream);
+
+/* FP with the residual epilogue (cyltomo/recon.py:148-153): adds
+ * sum_b sum_pix (p_meas[v] - sim)^2 (fp64, fixed reduction order) into
+ * *accum (device double).  `scratch` must hold ct_residual_scratch_len()
+ * doubles. */
+int64_t ct_residual_scratch_len(const ct_batch *batch);
+int ct_fp_cyl_residual(const float *mu, const ct_cyl_grid *grid, const ct_ray_view *views,
+                       const ct_batch *batch, const ct_sampling *sampling,
+                       const float *p_meas, double *scratch, double *accum,
+                       ct_stream_t stream);
+int ct_fp_cart_residual(const float *mu, const ct_cart_grid *grid, const ct_ray_view *views,
+                        const ct_batch *batch, const ct_sampling *sampling,
+                        const float *p_meas, double *scratch, double *accum,
+                        ct_stream_t stream);
+
+/* Geometry-only row-sum maximum per view (the max_row of
+ * cyltomo/recon.py:96-98), computed without marching: max_row[b] (device,
+ * float64, [n_batch]) = max over pixels of out_w.  Exact (sample counts are
+ * computed with the reference's fp64 interval arithmetic). */
+int ct_rowsum_max_cyl(const ct_cyl_grid *grid, const ct_ray_view *views,
+                      const ct_batch *batch, const ct_sampling *sampling,
+                      double *max_row, ct_stream_t stream);
+int ct_rowsum_max_cart(const ct_cart_grid *grid, const ct_ray_view *views,
+                       const ct_batch *batch, const ct_sampling *sampling,
+                       double *max_row, ct_stream_t stream);
+
+/* ---- back-projection (cyltomo/_kernels.py:380-417 backproject_cyl,
+ *      :420-443 backproject_cart) ----------------------------------------- */
+
+/* Sum over the batch of backproject_*(corr[b], view_ids[b]).  accumulate != 0
+ * adds into num/den (the reference's semantics); 0 overwrites.  den may be
+ * NULL.  trig (device, float64, [2*n_theta]) holds cos(theta_j), sin(theta_j)
+ * of the voxel centres (see ct_cyl_trig). */
+int ct_bp_cyl(const float *corr, const ct_det_view *dets, const ct_batch *batch,
+              const ct_cyl_grid *grid, const double *trig, float *num, float *den,
+              int accumulate, ct_stream_t stream);
+int ct_bp_cart(const float *corr, const ct_det_view *dets, const ct_batch *batch,
+               const ct_cart_grid *grid, float *num, float *den, int accumulate,
+               ct_stream_t stream);
+
+/* BP of the batch followed by the fused SART / OS-SART update of
+ * cyltomo/recon.py:105-119 with num/den = the batch sums (kept in registers). */
+int ct_bp_cyl_update(const float *corr, const ct_det_view *dets, const ct_batch *batch,
+                     const ct_cyl_grid *grid, const double *trig, const ct_update *upd,
+                     ct_stream_t stream);
+int ct_bp_cart_update(const float *corr, const ct_det_view *dets, const ct_batch *batch,
+                      const ct_cart_grid *grid, const ct_update *upd, ct_stream_t stream);
+
+/* Fill trig[0:n] = cos((j+.5)dtheta), trig[n:2n] = sin(...) (fp64). */
+int ct_cyl_trig(const ct_cyl_grid *grid, double *trig, ct_stream_t stream);
+
+/* Stand-alone update from reduced num/den over voxels [offset, offset+count)
+ * (the multi-GPU path: BP partials -> NCCL reduce-scatter -> this). */
+int ct_sart_update(const float *num, const float *den, int64_t offset, int64_t count,
+                   const ct_update *upd, ct_stream_t stream);
+
+/* ---- point sampling (cyltomo/_kernels.py:154-163, grid.py:261-319) ------- */
+int ct_sample_cyl(const float *mu, const ct_cyl_grid *grid, const double *rs,
+                  const double *ths, const double *hs, int64_t n, int nearest,
+                  float *out, ct_stream_t stream);
+int ct_sample_cart(const float *mu, const ct_cart_grid *grid, const double *xs,
+                   const double *ys, const double *zs, int64_t n, int nearest,
+                   float *out, ct_stream_t stream);
+/* resample_cyl_to_cyl (cyltomo/grid.py:310-319): evaluate src at every voxel
+ * centre of dst (both in object coordinates; poses ignored). */
+int ct_resample_cyl_to_cyl(const float *src_mu, const ct_cyl_grid *src,
+                           const ct_cyl_grid *dst, int nearest, float *dst_mu,
+                           ct_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CYLTOMO_B200_H */

@@ -1,0 +1,1086 @@
+// cyltomo_b200.cu -- sm_100a kernels + C-ABI for the cone-beam FP / BP / SART
+// hot path (see include/cyltomo_b200.h for the contract, DESIGN.md for the
+// data layout and rooflines).
+//
+// Reference semantics restated (not translated) from
+//   /root/reference/pkg/src/cyltomo/_kernels.py  (forward_cyl :238-293,
+//   forward_cart :296-343, backproject_cyl :380-417, backproject_cart
+//   :420-443, interp_* :48-151, intervals :170-231)
+//   /root/reference/pkg/src/cyltomo/recon.py     (correction / update :88-120,
+//   residual :148-153)
+//
+// Numerics:
+//  * per-ray setup -- sub-ray direction, support interval, sample count
+//    n = ceil((t1-t0)/step) and the in-support test of the last sample -- is
+//    done in fp64 with explicitly rounded ops (no FMA contraction), i.e. the
+//    same IEEE operation sequence as the reference, so sample counts and the
+//    SART row sums w are bit-identical to the fp64 oracle;
+//  * the march itself is fp32, relative to the first sample position, with
+//    the support convexity argument: samples 0..n-2 lie inside the support
+//    by >= step/2 along the ray, only sample n-1 can fall outside;
+//  * BP computes (u,v) in fp32 and recomputes them in fp64 (reference
+//    arithmetic) only when a footprint lies within 1e-3 px of the detector
+//    frame edge, where the `den > 0` decision is discontinuous.
+#include "cyltomo_b200.h"
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+namespace {
+
+constexpr double kTwoPi = 2.0 * 3.141592653589793;
+constexpr float kTwoPiF = 6.28318530717958647692f;
+
+thread_local char g_err[512] = "";
+
+int set_err(int code, const char* msg) {
+  snprintf(g_err, sizeof g_err, "%s", msg);
+  return code;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    snprintf(g_err, sizeof g_err, "%s: %s", what, cudaGetErrorString(e));
+    return CT_ERR_CUDA;
+  }
+  return CT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// exact fp64 helpers: the reference evaluates a*b+c as two rounded ops
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double dsqrt(double a) { return __dsqrt_rn(a); }
+
+// Unit direction of the sub-ray through detector point (cu, cv)
+// (_kernels.py:263-272): ((o + cu*du) + cv*dv) - src, normalised.
+__device__ __forceinline__ void subray_dir(const ct_ray_view& v, double cu, double cv,
+                                           double d[3]) {
+  double dx = dsub(dadd(dadd(v.origin[0], dmul(cu, v.du[0])), dmul(cv, v.dv[0])), v.src[0]);
+  double dy = dsub(dadd(dadd(v.origin[1], dmul(cu, v.du[1])), dmul(cv, v.dv[1])), v.src[1]);
+  double dz = dsub(dadd(dadd(v.origin[2], dmul(cu, v.du[2])), dmul(cv, v.dv[2])), v.src[2]);
+  double norm = dsqrt(dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz)));
+  d[0] = ddiv(dx, norm);
+  d[1] = ddiv(dy, norm);
+  d[2] = ddiv(dz, norm);
+}
+
+// ---------------------------------------------------------------------------
+// grid policies: support interval (fp64), last-sample test (fp64) and the
+// fp32 trilinear sample
+// ---------------------------------------------------------------------------
+struct CylGeo {
+  const float* __restrict__ mu;
+  int nh, nt, nr;
+  double radius, half_h;
+  // fp32 sampling constants
+  float inv_dr, inv_dth, inv_dh, h_off, nr_m1, nh_m1;
+
+  __host__ void init(const float* m, const ct_cyl_grid& g) {
+    mu = m;
+    nh = g.n_h; nt = g.n_theta; nr = g.n_r;
+    radius = g.radius;
+    half_h = 0.5 * g.height;
+    inv_dr = (float)(g.n_r / g.radius);
+    inv_dth = (float)(g.n_theta / kTwoPi);
+    inv_dh = (float)(g.n_h / g.height);
+    h_off = (float)(0.5 * g.n_h - 0.5);
+    nr_m1 = (float)(g.n_r - 1);
+    nh_m1 = (float)(g.n_h - 1);
+  }
+
+  // _kernels.py:170-204 (same operation order)
+  __device__ __forceinline__ bool interval(const double s[3], const double d[3], double& t0,
+                                           double& t1) const {
+    double tr0, tr1, tz0, tz1;
+    double a = dadd(dmul(d[0], d[0]), dmul(d[1], d[1]));
+    if (a < 1e-18) {
+      if (dadd(dmul(s[0], s[0]), dmul(s[1], s[1])) > dmul(radius, radius)) return false;
+      tr0 = -1e30; tr1 = 1e30;
+    } else {
+      double b = dadd(dmul(s[0], d[0]), dmul(s[1], d[1]));
+      double c = dsub(dadd(dmul(s[0], s[0]), dmul(s[1], s[1])), dmul(radius, radius));
+      double disc = dsub(dmul(b, b), dmul(a, c));
+      if (disc <= 0.0) return false;
+      double sq = dsqrt(disc);
+      tr0 = ddiv(dsub(-b, sq), a);
+      tr1 = ddiv(dadd(-b, sq), a);
+    }
+    if (fabs(d[2]) < 1e-18) {
+      if (fabs(s[2]) > half_h) return false;
+      tz0 = -1e30; tz1 = 1e30;
+    } else {
+      tz0 = ddiv(dsub(-half_h, s[2]), d[2]);
+      tz1 = ddiv(dsub(half_h, s[2]), d[2]);
+      if (tz0 > tz1) { double tmp = tz0; tz0 = tz1; tz1 = tmp; }
+    }
+    t0 = fmax(fmax(tr0, tz0), 0.0);
+    t1 = fmin(tr1, tz1);
+    return true;
+  }
+
+  // in-support test of a sample at parameter t (_kernels.py:280-286)
+  __device__ __forceinline__ bool inside(const double s[3], const double d[3], double t) const {
+    double x = dadd(s[0], dmul(t, d[0]));
+    double y = dadd(s[1], dmul(t, d[1]));
+    double z = dadd(s[2], dmul(t, d[2]));
+    double r = dsqrt(dadd(dmul(x, x), dmul(y, y)));
+    return !(r > radius || z < -half_h || z > half_h);
+  }
+  // the interpolator's own zero-outside test (_kernels.py:56-57) is the same
+  // expression as `inside` for cylinders
+  __device__ __forceinline__ bool interp_nonzero(const double*, const double*, double) const {
+    return true;
+  }
+
+  template <bool NEAREST>
+  __device__ __forceinline__ float sample(float x, float y, float z) const {
+    float r = sqrtf(fmaf(x, x, y * y));
+    float ft = atan2f(y, x) * inv_dth - 0.5f;
+    if (ft < -0.5f) ft += (float)nt;  // theta += 2*pi (_kernels.py:287-289)
+    float fr = fminf(fmaxf(fmaf(r, inv_dr, -0.5f), 0.0f), nr_m1);
+    float fh = fminf(fmaxf(fmaf(z, inv_dh, h_off), 0.0f), nh_m1);
+    if (NEAREST) {
+      int ir = (int)rintf(fr), ih = (int)rintf(fh), it = (int)rintf(ft);
+      if (it < 0) it += nt;
+      if (it >= nt) it -= nt;
+      return __ldg(mu + ((size_t)ih * nt + it) * nr + ir);
+    }
+    int i0 = (int)fr;  // fr >= 0
+    float wr = fr - (float)i0;
+    int i1 = min(i0 + 1, nr - 1);
+    int k0 = (int)fh;
+    float wh = fh - (float)k0;
+    int k1 = min(k0 + 1, nh - 1);
+    float jf = floorf(ft);
+    float wt = ft - jf;
+    int j0 = (int)jf;
+    if (j0 < 0) j0 += nt;
+    if (j0 >= nt) j0 -= nt;
+    int j1 = (j0 + 1 == nt) ? 0 : j0 + 1;
+    const float* p00 = mu + ((size_t)k0 * nt + j0) * nr;
+    const float* p01 = mu + ((size_t)k0 * nt + j1) * nr;
+    const float* p10 = mu + ((size_t)k1 * nt + j0) * nr;
+    const float* p11 = mu + ((size_t)k1 * nt + j1) * nr;
+    float a0 = __ldg(p00 + i0), a1 = __ldg(p00 + i1);
+    float b0 = __ldg(p01 + i0), b1 = __ldg(p01 + i1);
+    float c0 = __ldg(p10 + i0), c1 = __ldg(p10 + i1);
+    float e0 = __ldg(p11 + i0), e1 = __ldg(p11 + i1);
+    float c00 = fmaf(a1 - a0, wr, a0);
+    float c01 = fmaf(b1 - b0, wr, b0);
+    float c10 = fmaf(c1 - c0, wr, c0);
+    float c11 = fmaf(e1 - e0, wr, e0);
+    float q0 = fmaf(c01 - c00, wt, c00);
+    float q1 = fmaf(c11 - c10, wt, c10);
+    return fmaf(q1 - q0, wh, q0);
+  }
+};
+
+struct CartGeo {
+  const float* __restrict__ mu;
+  int nz, ny, nx;
+  double vs, lo[3], hi[3];
+  float inv_vs, off[3], nx_m1, ny_m1, nz_m1;
+
+  __host__ void init(const float* m, const ct_cart_grid& g) {
+    mu = m;
+    nz = g.n_z; ny = g.n_y; nx = g.n_x;
+    vs = g.voxel_size;
+    for (int a = 0; a < 3; ++a) lo[a] = g.origin[a];
+    hi[0] = g.origin[0] + g.n_x * g.voxel_size;
+    hi[1] = g.origin[1] + g.n_y * g.voxel_size;
+    hi[2] = g.origin[2] + g.n_z * g.voxel_size;
+    inv_vs = (float)(1.0 / g.voxel_size);
+    for (int a = 0; a < 3; ++a) off[a] = (float)(-g.origin[a] / g.voxel_size - 0.5);
+    nx_m1 = (float)(nx - 1); ny_m1 = (float)(ny - 1); nz_m1 = (float)(nz - 1);
+  }
+
+  // _kernels.py:207-231
+  __device__ __forceinline__ bool interval(const double s[3], const double d[3], double& t0,
+                                           double& t1) const {
+    t0 = 0.0;
+    t1 = 1e30;
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      if (fabs(d[ax]) < 1e-18) {
+        if (s[ax] < lo[ax] || s[ax] > hi[ax]) return false;
+      } else {
+        double ta = ddiv(dsub(lo[ax], s[ax]), d[ax]);
+        double tb = ddiv(dsub(hi[ax], s[ax]), d[ax]);
+        if (ta > tb) { double tmp = ta; ta = tb; tb = tmp; }
+        if (ta > t0) t0 = ta;
+        if (tb < t1) t1 = tb;
+      }
+    }
+    return true;
+  }
+
+  __device__ __forceinline__ bool inside(const double s[3], const double d[3], double t) const {
+    double x = dadd(s[0], dmul(t, d[0]));
+    double y = dadd(s[1], dmul(t, d[1]));
+    double z = dadd(s[2], dmul(t, d[2]));
+    return !(x < lo[0] || x > hi[0] || y < lo[1] || y > hi[1] || z < lo[2] || z > hi[2]);
+  }
+  // interp_cart's own outside test (_kernels.py:117-118): a counted sample can
+  // still interpolate to 0 if index recovery lands outside [-.5, n-.5]
+  __device__ __forceinline__ bool interp_nonzero(const double* s, const double* d,
+                                                 double t) const {
+    double p[3];
+    for (int a = 0; a < 3; ++a) p[a] = dadd(s[a], dmul(t, d[a]));
+    double f[3];
+    for (int a = 0; a < 3; ++a) {
+      f[a] = dsub(ddiv(dsub(p[a], lo[a]), vs), 0.5);
+      double r = rint(f[a]);
+      if (fabs(f[a] - r) < 1e-9) f[a] = r;
+    }
+    return !(f[0] < -0.5 || f[0] > nx - 0.5 || f[1] < -0.5 || f[1] > ny - 0.5 ||
+             f[2] < -0.5 || f[2] > nz - 0.5);
+  }
+
+  template <bool NEAREST>
+  __device__ __forceinline__ float sample(float x, float y, float z) const {
+    float fx = fminf(fmaxf(fmaf(x, inv_vs, off[0]), 0.0f), nx_m1);
+    float fy = fminf(fmaxf(fmaf(y, inv_vs, off[1]), 0.0f), ny_m1);
+    float fz = fminf(fmaxf(fmaf(z, inv_vs, off[2]), 0.0f), nz_m1);
+    if (NEAREST) {
+      return __ldg(mu + ((size_t)(int)rintf(fz) * ny + (int)rintf(fy)) * nx + (int)rintf(fx));
+    }
+    int i0 = (int)fx, j0 = (int)fy, k0 = (int)fz;
+    float wx = fx - (float)i0, wy = fy - (float)j0, wz = fz - (float)k0;
+    int i1 = min(i0 + 1, nx - 1), j1 = min(j0 + 1, ny - 1), k1 = min(k0 + 1, nz - 1);
+    const float* p00 = mu + ((size_t)k0 * ny + j0) * nx;
+    const float* p01 = mu + ((size_t)k0 * ny + j1) * nx;
+    const float* p10 = mu + ((size_t)k1 * ny + j0) * nx;
+    const float* p11 = mu + ((size_t)k1 * ny + j1) * nx;
+    float a0 = __ldg(p00 + i0), a1 = __ldg(p00 + i1);
+    float b0 = __ldg(p01 + i0), b1 = __ldg(p01 + i1);
+    float c0 = __ldg(p10 + i0), c1 = __ldg(p10 + i1);
+    float e0 = __ldg(p11 + i0), e1 = __ldg(p11 + i1);
+    float c00 = fmaf(a1 - a0, wx, a0);
+    float c01 = fmaf(b1 - b0, wx, b0);
+    float c10 = fmaf(c1 - c0, wx, c0);
+    float c11 = fmaf(e1 - e0, wx, e0);
+    float q0 = fmaf(c01 - c00, wy, c00);
+    float q1 = fmaf(c11 - c10, wy, c10);
+    return fmaf(q1 - q0, wz, q0);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// forward projection
+// ---------------------------------------------------------------------------
+enum FpEpi { EPI_PROJECT = 0, EPI_CORR = 1, EPI_RESID = 2, EPI_ROWMAX = 3 };
+
+constexpr int FP_TILE_W = 16, FP_TILE_H = 8, FP_THREADS = 128;
+
+template <class Geo>
+struct FpArgs {
+  Geo geo;
+  const ct_ray_view* __restrict__ views;
+  const int32_t* __restrict__ view_ids;
+  int rows, cols, ss;
+  double step;
+  const float* __restrict__ p_meas;
+  const double* __restrict__ row_thr;
+  float* __restrict__ out0;
+  float* __restrict__ out1;
+  double* __restrict__ red;  // residual partials / per-view max_row
+};
+
+// One sub-ray: returns the in-support sample count; adds the fp32 sum of
+// interpolated values into acc (skipped for COUNT_ONLY).
+template <class Geo, bool NEAREST, bool COUNT_ONLY>
+__device__ __forceinline__ int march(const Geo& geo, const ct_ray_view& v, double cu, double cv,
+                                     double step, float& acc) {
+  double d[3];
+  subray_dir(v, cu, cv, d);
+  double t0, t1;
+  if (!geo.interval(v.src, d, t0, t1)) return 0;
+  if (t1 <= t0) return 0;
+  const int n = (int)ceil(ddiv(dsub(t1, t0), step));
+  const double t_last = dadd(t0, dmul((double)(n - 1) + 0.5, step));
+  const bool last_in = geo.inside(v.src, d, t_last);
+  if (COUNT_ONLY) return n - 1 + (last_in ? 1 : 0);
+  // fp32 march relative to the first sample position
+  const double ts = dadd(t0, dmul(0.5, step));
+  const float ex = (float)(v.src[0] + ts * d[0]);
+  const float ey = (float)(v.src[1] + ts * d[1]);
+  const float ez = (float)(v.src[2] + ts * d[2]);
+  const float ix = (float)(step * d[0]);
+  const float iy = (float)(step * d[1]);
+  const float iz = (float)(step * d[2]);
+  const int n_int = n - 1;
+  float sum = 0.0f;
+  int k = 0;
+  for (; k + 4 <= n_int; k += 4) {
+    const float k0 = (float)k;
+    float s0 = geo.template sample<NEAREST>(fmaf(k0, ix, ex), fmaf(k0, iy, ey), fmaf(k0, iz, ez));
+    float s1 = geo.template sample<NEAREST>(fmaf(k0 + 1.f, ix, ex), fmaf(k0 + 1.f, iy, ey),
+                                            fmaf(k0 + 1.f, iz, ez));
+    float s2 = geo.template sample<NEAREST>(fmaf(k0 + 2.f, ix, ex), fmaf(k0 + 2.f, iy, ey),
+                                            fmaf(k0 + 2.f, iz, ez));
+    float s3 = geo.template sample<NEAREST>(fmaf(k0 + 3.f, ix, ex), fmaf(k0 + 3.f, iy, ey),
+                                            fmaf(k0 + 3.f, iz, ez));
+    sum += (s0 + s1) + (s2 + s3);
+  }
+  for (; k < n_int; ++k) {
+    const float kf = (float)k;
+    sum += geo.template sample<NEAREST>(fmaf(kf, ix, ex), fmaf(kf, iy, ey), fmaf(kf, iz, ez));
+  }
+  if (last_in && geo.interp_nonzero(v.src, d, t_last)) {
+    const float kf = (float)n_int;
+    sum += geo.template sample<NEAREST>(fmaf(kf, ix, ex), fmaf(kf, iy, ey), fmaf(kf, iz, ez));
+  }
+  acc += sum;
+  return n_int + (last_in ? 1 : 0);
+}
+
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+__device__ __forceinline__ double warp_max(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+
+template <class Geo, int EPI, bool NEAREST>
+__global__ void __launch_bounds__(FP_THREADS) fp_kernel(const FpArgs<Geo> a) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // each warp covers an 8x4 pixel patch; the block a 16x8 tile
+  const int col = blockIdx.x * FP_TILE_W + (warp & 1) * 8 + (lane & 7);
+  const int row = blockIdx.z * FP_TILE_H + (warp >> 1) * 4 + (lane >> 3);
+  const int b = blockIdx.y;
+  const int vid = a.view_ids ? a.view_ids[b] : b;
+  const bool active = row < a.rows && col < a.cols;
+  const size_t npix = (size_t)a.rows * a.cols;
+  const size_t pix = (size_t)row * a.cols + col;
+
+  float acc = 0.0f;
+  int count = 0;
+  if (active) {
+    const ct_ray_view& v = a.views[vid];
+    const int ss = a.ss;
+    for (int sv = 0; sv < ss; ++sv) {
+      const double off_v = dsub(ddiv((double)sv + 0.5, (double)ss), 0.5);
+      for (int su = 0; su < ss; ++su) {
+        const double off_u = dsub(ddiv((double)su + 0.5, (double)ss), 0.5);
+        count += march<Geo, NEAREST, EPI == EPI_ROWMAX>(
+            a.geo, v, dadd((double)col, off_u), dadd((double)row, off_v), a.step, acc);
+      }
+    }
+  }
+  const double inv_ss2 = ddiv(1.0, (double)(a.ss * a.ss));
+  // out_w = wacc * step * inv_ss2, out_p = acc * step * inv_ss2 (_kernels.py:292-293)
+  const double w64 = dmul(dmul((double)count, a.step), inv_ss2);
+  const double p64 = (double)acc * a.step * inv_ss2;
+
+  if (EPI == EPI_PROJECT) {
+    if (active) {
+      a.out0[(size_t)b * npix + pix] = (float)p64;
+      if (a.out1) a.out1[(size_t)b * npix + pix] = (float)w64;
+    }
+  } else if (EPI == EPI_CORR) {
+    if (active) {
+      float c = 0.0f;
+      if (w64 > a.row_thr[vid]) {
+        const float pm = a.p_meas[(size_t)vid * npix + pix];
+        c = (pm - (float)p64) / (float)w64;
+      }
+      a.out0[(size_t)b * npix + pix] = c;
+    }
+  } else {
+    double x = 0.0;
+    if (active) {
+      if (EPI == EPI_RESID) {
+        const double r = (double)a.p_meas[(size_t)vid * npix + pix] - p64;
+        x = r * r;
+      } else {
+        x = w64;
+      }
+    }
+    __shared__ double sred[FP_THREADS / 32];
+    x = (EPI == EPI_RESID) ? warp_sum(x) : warp_max(x);
+    if (lane == 0) sred[warp] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = sred[0];
+      for (int w = 1; w < FP_THREADS / 32; ++w)
+        t = (EPI == EPI_RESID) ? t + sred[w] : fmax(t, sred[w]);
+      if (EPI == EPI_RESID) {
+        const size_t blk = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        a.red[blk] = t;
+      } else {
+        // non-negative doubles order like their bit patterns
+        atomicMax(reinterpret_cast<unsigned long long*>(a.red + b),
+                  (unsigned long long)__double_as_longlong(t));
+      }
+    }
+  }
+}
+
+// Deterministic second stage: fixed-order sum of the per-block partials.
+__global__ void __launch_bounds__(1024) sum_partials_kernel(const double* __restrict__ part,
+                                                            int64_t n, double* accum) {
+  __shared__ double s[32];
+  double x = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) x += part[i];
+  x = warp_sum(x);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
+    *accum += t;
+  }
+}
+
+dim3 fp_grid(const ct_batch& b) {
+  return dim3((b.det_cols + FP_TILE_W - 1) / FP_TILE_W, b.n_batch,
+              (b.det_rows + FP_TILE_H - 1) / FP_TILE_H);
+}
+
+int check_batch(const ct_batch* b, const void* views, const ct_sampling* s) {
+  if (!b || !views || !s) return set_err(CT_ERR_ARG, "null batch/views/sampling");
+  if (b->n_batch < 1 || b->n_batch > 65535 || b->det_rows < 1 || b->det_cols < 1 ||
+      (b->det_rows + FP_TILE_H - 1) / FP_TILE_H > 65535)
+    return set_err(CT_ERR_ARG, "bad batch dimensions");
+  if (!(s->step > 0.0) || s->supersample < 1) return set_err(CT_ERR_ARG, "bad sampling");
+  return CT_OK;
+}
+
+int check_cyl(const ct_cyl_grid* g) {
+  if (!g || g->n_h < 1 || g->n_theta < 1 || g->n_r < 1 || !(g->radius > 0) || !(g->height > 0))
+    return set_err(CT_ERR_ARG, "bad cylindrical grid");
+  if ((int64_t)g->n_h * g->n_theta * g->n_r >= (int64_t)1 << 31)
+    return set_err(CT_ERR_ARG, "grid has >= 2^31 voxels");
+  return CT_OK;
+}
+int check_cart(const ct_cart_grid* g) {
+  if (!g || g->n_z < 1 || g->n_y < 1 || g->n_x < 1 || !(g->voxel_size > 0))
+    return set_err(CT_ERR_ARG, "bad Cartesian grid");
+  if ((int64_t)g->n_z * g->n_y * g->n_x >= (int64_t)1 << 31)
+    return set_err(CT_ERR_ARG, "grid has >= 2^31 voxels");
+  return CT_OK;
+}
+
+template <class Geo, int EPI>
+int launch_fp(const Geo& geo, const ct_ray_view* views, const ct_batch& b, const ct_sampling& s,
+              const float* p_meas, const double* thr, float* o0, float* o1, double* red,
+              cudaStream_t st) {
+  FpArgs<Geo> a;
+  a.geo = geo;
+  a.views = views;
+  a.view_ids = b.view_ids;
+  a.rows = b.det_rows;
+  a.cols = b.det_cols;
+  a.ss = s.supersample;
+  a.step = s.step;
+  a.p_meas = p_meas;
+  a.row_thr = thr;
+  a.out0 = o0;
+  a.out1 = o1;
+  a.red = red;
+  if (s.nearest)
+    fp_kernel<Geo, EPI, true><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
+  else
+    fp_kernel<Geo, EPI, false><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
+  return check_launch("fp_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// back-projection
+// ---------------------------------------------------------------------------
+enum BpMode { BP_ACC = 0, BP_WRITE = 1, BP_UPDATE = 2 };
+
+constexpr int BP_THREADS = 256;
+constexpr int BP_CHUNK = 64;   // views staged in shared memory per pass
+constexpr float BP_EDGE_EPS = 1e-3f;  // px band around the frame edge refined in fp64
+
+struct BpViewF {
+  float cphi, sphi, sod, sdd_p;  // sdd / pitch
+  float u0, v0, depth_floor, _pad;
+};
+
+struct CylVox {
+  int nh, nt, nr;
+  double dr, dth, dh, half_h;
+  double rot[9], t[3];
+  const double* __restrict__ trig;  // cos[nt], sin[nt]
+  __host__ void init(const ct_cyl_grid& g, const double* tr) {
+    nh = g.n_h; nt = g.n_theta; nr = g.n_r;
+    dr = g.radius / g.n_r;
+    dth = kTwoPi / g.n_theta;
+    dh = g.height / g.n_h;
+    half_h = 0.5 * g.height;
+    for (int i = 0; i < 9; ++i) rot[i] = g.rot[i];
+    for (int i = 0; i < 3; ++i) t[i] = g.t[i];
+    trig = tr;
+  }
+  __host__ __device__ int64_t count() const { return (int64_t)nh * nt * nr; }
+  // voxel centre, object -> world (_kernels.py:396-406), reference op order
+  __device__ __forceinline__ void world(int m, double w[3]) const {
+    const int ir = m % nr;
+    const int j = (m / nr) % nt;
+    const int k = m / (nr * nt);
+    const double r = dmul((double)ir + 0.5, dr);
+    const double h = dsub(dmul((double)k + 0.5, dh), half_h);
+    const double xo = dmul(r, trig[j]);
+    const double yo = dmul(r, trig[nt + j]);
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      w[i] = dadd(dadd(dadd(dmul(rot[3 * i], xo), dmul(rot[3 * i + 1], yo)),
+                       dmul(rot[3 * i + 2], h)), t[i]);
+  }
+};
+
+struct CartVox {
+  int nz, ny, nx;
+  double vs, o[3];
+  __host__ void init(const ct_cart_grid& g) {
+    nz = g.n_z; ny = g.n_y; nx = g.n_x;
+    vs = g.voxel_size;
+    for (int i = 0; i < 3; ++i) o[i] = g.origin[i];
+  }
+  __host__ __device__ int64_t count() const { return (int64_t)nz * ny * nx; }
+  // _kernels.py:431-437
+  __device__ __forceinline__ void world(int m, double w[3]) const {
+    const int i = m % nx;
+    const int j = (m / nx) % ny;
+    const int k = m / (nx * ny);
+    w[0] = dadd(o[0], dmul((double)i + 0.5, vs));
+    w[1] = dadd(o[1], dmul((double)j + 0.5, vs));
+    w[2] = dadd(o[2], dmul((double)k + 0.5, vs));
+  }
+};
+
+template <class Vox>
+struct BpArgs {
+  Vox vox;
+  const float* __restrict__ corr;
+  const ct_det_view* __restrict__ dets;
+  const int32_t* __restrict__ view_ids;
+  int n_batch, rows, cols;
+  float* num;
+  float* den;
+  ct_update upd;
+};
+
+// fp64 re-evaluation of one voxel-view with the reference's arithmetic
+// (_kernels.py:407-417 + _bilinear_gather :350-377); only taken for
+// footprints within BP_EDGE_EPS of the frame edge or near the source plane.
+__device__ __noinline__ void bp_refine(const ct_det_view& dv, const double w[3],
+                                       const float* __restrict__ img, int rows, int cols,
+                                       float& num, float& den) {
+  const double xi = dsub(dmul(dv.cphi, w[0]), dmul(dv.sphi, w[1]));
+  const double yi = dadd(dmul(dv.sphi, w[0]), dmul(dv.cphi, w[1]));
+  const double depth = dadd(dv.sod, yi);
+  if (depth <= dmul(1e-6, dv.sod)) return;
+  const double scale = ddiv(dv.sdd, dmul(depth, dv.pitch));
+  const double u = dadd(dv.u0, dmul(xi, scale));
+  const double v = dadd(dv.v0, dmul(w[2], scale));
+  const double fiu = floor(u), fiv = floor(v);
+  const double fu = dsub(u, fiu), fv = dsub(v, fiv);
+  if (!(fiu >= -2.0 && fiu <= (double)cols) || !(fiv >= -2.0 && fiv <= (double)rows)) return;
+  const int iu = (int)fiu, iv = (int)fiv;
+  for (int dvv = 0; dvv < 2; ++dvv) {
+    const int rr = iv + dvv;
+    if (rr < 0 || rr >= rows) continue;
+    const double wv = dvv == 1 ? fv : dsub(1.0, fv);
+    for (int duu = 0; duu < 2; ++duu) {
+      const int cc = iu + duu;
+      if (cc < 0 || cc >= cols) continue;
+      const double wu = duu == 1 ? fu : dsub(1.0, fu);
+      const double wt = dmul(wu, wv);
+      num += (float)wt * img[(size_t)rr * cols + cc];
+      den += (float)wt;
+    }
+  }
+}
+
+template <class Vox, int MODE>
+__global__ void __launch_bounds__(BP_THREADS) bp_kernel(const BpArgs<Vox> a) {
+  __shared__ BpViewF sv[BP_CHUNK];
+  const int64_t nvox = a.vox.count();
+  const int m = blockIdx.x * BP_THREADS + threadIdx.x;
+  const bool active = m < nvox;
+  double w64[3] = {0.0, 0.0, 0.0};
+  if (active) a.vox.world(m, w64);
+  const float xw = (float)w64[0], yw = (float)w64[1], zw = (float)w64[2];
+  const float W = (float)a.cols, H = (float)a.rows;
+  const size_t npix = (size_t)a.rows * a.cols;
+  float num = 0.0f, den = 0.0f;
+
+  for (int c0 = 0; c0 < a.n_batch; c0 += BP_CHUNK) {
+    const int nc = min(BP_CHUNK, a.n_batch - c0);
+    __syncthreads();
+    if (threadIdx.x < nc) {
+      const int vid = a.view_ids ? a.view_ids[c0 + threadIdx.x] : c0 + threadIdx.x;
+      const ct_det_view& d = a.dets[vid];
+      BpViewF f;
+      f.cphi = (float)d.cphi; f.sphi = (float)d.sphi; f.sod = (float)d.sod;
+      f.sdd_p = (float)(d.sdd / d.pitch);
+      f.u0 = (float)d.u0; f.v0 = (float)d.v0;
+      f.depth_floor = (float)(1e-6 * d.sod);
+      f._pad = 0.0f;
+      sv[threadIdx.x] = f;
+    }
+    __syncthreads();
+    if (!active) continue;
+    for (int i = 0; i < nc; ++i) {
+      const BpViewF f = sv[i];
+      const float* img = a.corr + (size_t)(c0 + i) * npix;
+      const float xi = fmaf(f.cphi, xw, -f.sphi * yw);
+      const float yi = fmaf(f.sphi, xw, f.cphi * yw);
+      const float depth = f.sod + yi;
+      const float scale = f.sdd_p / depth;
+      const float u = fmaf(xi, scale, f.u0);
+      const float v = fmaf(zw, scale, f.v0);
+      const bool edge = fabsf(u + 1.0f) < BP_EDGE_EPS || fabsf(u - W) < BP_EDGE_EPS ||
+                        fabsf(v + 1.0f) < BP_EDGE_EPS || fabsf(v - H) < BP_EDGE_EPS ||
+                        depth <= 2.0f * f.depth_floor;
+      if (edge) {
+        const int vid = a.view_ids ? a.view_ids[c0 + i] : c0 + i;
+        bp_refine(a.dets[vid], w64, img, a.rows, a.cols, num, den);
+        continue;
+      }
+      if (!(u > -1.0f && u < W && v > -1.0f && v < H)) continue;
+      const float fiu = floorf(u), fiv = floorf(v);
+      const int iu = (int)fiu, iv = (int)fiv;
+      const float fu = u - fiu, fv = v - fiv;
+      const bool cu0 = iu >= 0, cu1 = iu + 1 < a.cols;
+      const bool rv0 = iv >= 0, rv1 = iv + 1 < a.rows;
+      const float* r0 = img + (size_t)iv * a.cols + iu;
+      const float* r1 = r0 + a.cols;
+      const float t00 = (rv0 && cu0) ? __ldg(r0) : 0.0f;
+      const float t01 = (rv0 && cu1) ? __ldg(r0 + 1) : 0.0f;
+      const float t10 = (rv1 && cu0) ? __ldg(r1) : 0.0f;
+      const float t11 = (rv1 && cu1) ? __ldg(r1 + 1) : 0.0f;
+      const float wu0 = 1.0f - fu, wv0 = 1.0f - fv;
+      num += wv0 * (wu0 * t00 + fu * t01) + fv * (wu0 * t10 + fu * t11);
+      den += ((cu0 ? wu0 : 0.0f) + (cu1 ? fu : 0.0f)) * ((rv0 ? wv0 : 0.0f) + (rv1 ? fv : 0.0f));
+    }
+  }
+  if (!active) return;
+  if (MODE == BP_ACC) {
+    a.num[m] += num;
+    if (a.den) a.den[m] += den;
+  } else if (MODE == BP_WRITE) {
+    a.num[m] = num;
+    if (a.den) a.den[m] = den;
+  } else {
+    // cyltomo/recon.py:105-119: touched = den > 0 [& w != 0];
+    // mu = max(mu + (relaxation * w) * num / den, 0)
+    if (den > 0.0f) {
+      float lw = a.upd.relaxation;
+      if (a.upd.weights) {
+        const float wm = a.upd.weights[m];
+        if (wm == 0.0f) return;
+        lw = lw * wm;
+      }
+      const float delta = (lw * num) / den;
+      float mu = a.upd.mu[m] + delta;
+      if (a.upd.nonneg) mu = fmaxf(mu, 0.0f);
+      a.upd.mu[m] = mu;
+    }
+  }
+}
+
+template <class Vox, int MODE>
+int launch_bp(const Vox& vox, const float* corr, const ct_det_view* dets, const ct_batch& b,
+              float* num, float* den, const ct_update* upd, cudaStream_t st) {
+  BpArgs<Vox> a;
+  a.vox = vox;
+  a.corr = corr;
+  a.dets = dets;
+  a.view_ids = b.view_ids;
+  a.n_batch = b.n_batch;
+  a.rows = b.det_rows;
+  a.cols = b.det_cols;
+  a.num = num;
+  a.den = den;
+  if (upd) a.upd = *upd; else memset(&a.upd, 0, sizeof a.upd);
+  const int64_t nvox = vox.count();
+  const unsigned blocks = (unsigned)((nvox + BP_THREADS - 1) / BP_THREADS);
+  bp_kernel<Vox, MODE><<<blocks, BP_THREADS, 0, st>>>(a);
+  return check_launch("bp_kernel");
+}
+
+__global__ void update_kernel(const float* __restrict__ num, const float* __restrict__ den,
+                              int64_t offset, int64_t count, ct_update u) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const int64_t m = offset + i;
+  const float d = den[i];
+  if (!(d > 0.0f)) return;
+  float lw = u.relaxation;
+  if (u.weights) {
+    const float wm = u.weights[m];
+    if (wm == 0.0f) return;
+    lw = lw * wm;
+  }
+  float mu = u.mu[m] + (lw * num[i]) / d;
+  if (u.nonneg) mu = fmaxf(mu, 0.0f);
+  u.mu[m] = mu;
+}
+
+__global__ void trig_kernel(int nt, double* trig) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nt) return;
+  const double th = ((double)j + 0.5) * (kTwoPi / nt);
+  trig[j] = cos(th);
+  trig[nt + j] = sin(th);
+}
+
+// ---------------------------------------------------------------------------
+// point sampling (fp64 index arithmetic with the reference's snap, fp32 data)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double snap_idx(double f) {
+  const double r = rint(f);
+  return fabs(f - r) < 1e-9 ? r : f;
+}
+
+// _kernels.py:48-107
+__device__ float interp_cyl64(const float* __restrict__ mu, int nh, int nt, int nr,
+                              double radius, double height, double r, double th, double h,
+                              bool nearest) {
+  const double half_h = 0.5 * height;
+  if (r > radius || h < -half_h || h > half_h) return 0.0f;
+  const double dr = radius / nr, dth = kTwoPi / nt, dh = height / nh;
+  double fr = fmin(fmax(snap_idx(r / dr - 0.5), 0.0), (double)nr - 1.0);
+  double fh = fmin(fmax(snap_idx((h + half_h) / dh - 0.5), 0.0), (double)nh - 1.0);
+  double ft = snap_idx(th / dth - 0.5);
+  if (nearest) {
+    const int ir = (int)rint(fr), ih = (int)rint(fh);
+    long long it = (long long)rint(ft) % nt;
+    if (it < 0) it += nt;
+    return mu[((size_t)ih * nt + it) * nr + ir];
+  }
+  const int i0 = (int)floor(fr);
+  const double wr = fr - i0;
+  const int i1 = min(i0 + 1, nr - 1);
+  const int k0 = (int)floor(fh);
+  const double wh = fh - k0;
+  const int k1 = min(k0 + 1, nh - 1);
+  const double jf = floor(ft);
+  const double wt = ft - jf;
+  long long j0 = (long long)jf % nt;
+  if (j0 < 0) j0 += nt;
+  const long long j1 = j0 + 1 == nt ? 0 : j0 + 1;
+  auto M = [&](int k, long long j, int i) { return (double)mu[((size_t)k * nt + j) * nr + i]; };
+  const double c00 = M(k0, j0, i0) * (1.0 - wr) + M(k0, j0, i1) * wr;
+  const double c01 = M(k0, j1, i0) * (1.0 - wr) + M(k0, j1, i1) * wr;
+  const double c10 = M(k1, j0, i0) * (1.0 - wr) + M(k1, j0, i1) * wr;
+  const double c11 = M(k1, j1, i0) * (1.0 - wr) + M(k1, j1, i1) * wr;
+  const double c0 = c00 * (1.0 - wt) + c01 * wt;
+  const double c1 = c10 * (1.0 - wt) + c11 * wt;
+  return (float)(c0 * (1.0 - wh) + c1 * wh);
+}
+
+// _kernels.py:110-151
+__device__ float interp_cart64(const float* __restrict__ mu, int nz, int ny, int nx, double vs,
+                               const double o[3], double x, double y, double z, bool nearest) {
+  double fx = snap_idx((x - o[0]) / vs - 0.5);
+  double fy = snap_idx((y - o[1]) / vs - 0.5);
+  double fz = snap_idx((z - o[2]) / vs - 0.5);
+  if (fx < -0.5 || fx > nx - 0.5 || fy < -0.5 || fy > ny - 0.5 || fz < -0.5 || fz > nz - 0.5)
+    return 0.0f;
+  fx = fmin(fmax(fx, 0.0), nx - 1.0);
+  fy = fmin(fmax(fy, 0.0), ny - 1.0);
+  fz = fmin(fmax(fz, 0.0), nz - 1.0);
+  if (nearest)
+    return mu[((size_t)(int)rint(fz) * ny + (int)rint(fy)) * nx + (int)rint(fx)];
+  const int i0 = (int)floor(fx), j0 = (int)floor(fy), k0 = (int)floor(fz);
+  const double wx = fx - i0, wy = fy - j0, wz = fz - k0;
+  const int i1 = min(i0 + 1, nx - 1), j1 = min(j0 + 1, ny - 1), k1 = min(k0 + 1, nz - 1);
+  auto M = [&](int k, int j, int i) { return (double)mu[((size_t)k * ny + j) * nx + i]; };
+  const double c00 = M(k0, j0, i0) * (1.0 - wx) + M(k0, j0, i1) * wx;
+  const double c01 = M(k0, j1, i0) * (1.0 - wx) + M(k0, j1, i1) * wx;
+  const double c10 = M(k1, j0, i0) * (1.0 - wx) + M(k1, j0, i1) * wx;
+  const double c11 = M(k1, j1, i0) * (1.0 - wx) + M(k1, j1, i1) * wx;
+  const double c0 = c00 * (1.0 - wy) + c01 * wy;
+  const double c1 = c10 * (1.0 - wy) + c11 * wy;
+  return (float)(c0 * (1.0 - wz) + c1 * wz);
+}
+
+__global__ void sample_cyl_kernel(const float* __restrict__ mu, ct_cyl_grid g,
+                                  const double* __restrict__ rs, const double* __restrict__ ths,
+                                  const double* __restrict__ hs, int64_t n, int nearest,
+                                  float* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[i] = interp_cyl64(mu, g.n_h, g.n_theta, g.n_r, g.radius, g.height, rs[i], ths[i], hs[i],
+                        nearest != 0);
+}
+
+__global__ void sample_cart_kernel(const float* __restrict__ mu, ct_cart_grid g,
+                                   const double* __restrict__ xs, const double* __restrict__ ys,
+                                   const double* __restrict__ zs, int64_t n, int nearest,
+                                   float* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[i] = interp_cart64(mu, g.n_z, g.n_y, g.n_x, g.voxel_size, g.origin, xs[i], ys[i], zs[i],
+                         nearest != 0);
+}
+
+// grid.py:310-319 -- target voxel centres (h_centers/theta_centers/r_centers)
+__global__ void resample_cyl_kernel(const float* __restrict__ src_mu, ct_cyl_grid s,
+                                    ct_cyl_grid d, int nearest, float* out) {
+  const int64_t n = (int64_t)d.n_h * d.n_theta * d.n_r;
+  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n) return;
+  const int ir = (int)(m % d.n_r);
+  const int j = (int)((m / d.n_r) % d.n_theta);
+  const int k = (int)(m / ((int64_t)d.n_r * d.n_theta));
+  const double r = (ir + 0.5) * (d.radius / d.n_r);
+  const double th = (j + 0.5) * (kTwoPi / d.n_theta);
+  const double h = (k + 0.5) * (d.height / d.n_h) - 0.5 * d.height;
+  out[m] = interp_cyl64(src_mu, s.n_h, s.n_theta, s.n_r, s.radius, s.height, r, th, h,
+                        nearest != 0);
+}
+
+unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+int ct_abi_version(void) { return CT_ABI_VERSION; }
+const char* ct_last_error(void) { return g_err; }
+const char* ct_arch(void) { return "sm_100a"; }
+
+#define CT_STREAM(s) (static_cast<cudaStream_t>(s))
+
+int ct_fp_cyl(const float* mu, const ct_cyl_grid* grid, const ct_ray_view* views,
+              const ct_batch* batch, const ct_sampling* s, float* out_p, float* out_w,
+              ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cyl(grid))) return rc;
+  if (!mu || !out_p) return set_err(CT_ERR_ARG, "null mu/out_p");
+  CylGeo geo;
+  geo.init(mu, *grid);
+  return launch_fp<CylGeo, EPI_PROJECT>(geo, views, *batch, *s, nullptr, nullptr, out_p, out_w,
+                                        nullptr, CT_STREAM(stream));
+}
+
+int ct_fp_cart(const float* mu, const ct_cart_grid* grid, const ct_ray_view* views,
+               const ct_batch* batch, const ct_sampling* s, float* out_p, float* out_w,
+               ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cart(grid))) return rc;
+  if (!mu || !out_p) return set_err(CT_ERR_ARG, "null mu/out_p");
+  CartGeo geo;
+  geo.init(mu, *grid);
+  return launch_fp<CartGeo, EPI_PROJECT>(geo, views, *batch, *s, nullptr, nullptr, out_p, out_w,
+                                         nullptr, CT_STREAM(stream));
+}
+
+int ct_fp_cyl_correction(const float* mu, const ct_cyl_grid* grid, const ct_ray_view* views,
+                         const ct_batch* batch, const ct_sampling* s, const float* p_meas,
+                         const double* row_thr, float* corr, ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cyl(grid))) return rc;
+  if (!mu || !p_meas || !row_thr || !corr) return set_err(CT_ERR_ARG, "null pointer");
+  CylGeo geo;
+  geo.init(mu, *grid);
+  return launch_fp<CylGeo, EPI_CORR>(geo, views, *batch, *s, p_meas, row_thr, corr, nullptr,
+                                     nullptr, CT_STREAM(stream));
+}
+
+int ct_fp_cart_correction(const float* mu, const ct_cart_grid* grid, const ct_ray_view* views,
+                          const ct_batch* batch, const ct_sampling* s, const float* p_meas,
+                          const double* row_thr, float* corr, ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cart(grid))) return rc;
+  if (!mu || !p_meas || !row_thr || !corr) return set_err(CT_ERR_ARG, "null pointer");
+  CartGeo geo;
+  geo.init(mu, *grid);
+  return launch_fp<CartGeo, EPI_CORR>(geo, views, *batch, *s, p_meas, row_thr, corr, nullptr,
+                                      nullptr, CT_STREAM(stream));
+}
+
+int64_t ct_residual_scratch_len(const ct_batch* batch) {
+  if (!batch) return 0;
+  dim3 g = fp_grid(*batch);
+  return (int64_t)g.x * g.y * g.z;
+}
+
+static int finish_residual(const ct_batch* batch, double* scratch, double* accum,
+                           cudaStream_t st) {
+  sum_partials_kernel<<<1, 1024, 0, st>>>(scratch, ct_residual_scratch_len(batch), accum);
+  return check_launch("sum_partials_kernel");
+}
+
+int ct_fp_cyl_residual(const float* mu, const ct_cyl_grid* grid, const ct_ray_view* views,
+                       const ct_batch* batch, const ct_sampling* s, const float* p_meas,
+                       double* scratch, double* accum, ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cyl(grid))) return rc;
+  if (!mu || !p_meas || !scratch || !accum) return set_err(CT_ERR_ARG, "null pointer");
+  CylGeo geo;
+  geo.init(mu, *grid);
+  rc = launch_fp<CylGeo, EPI_RESID>(geo, views, *batch, *s, p_meas, nullptr, nullptr, nullptr,
+                                    scratch, CT_STREAM(stream));
+  return rc ? rc : finish_residual(batch, scratch, accum, CT_STREAM(stream));
+}
+
+int ct_fp_cart_residual(const float* mu, const ct_cart_grid* grid, const ct_ray_view* views,
+                        const ct_batch* batch, const ct_sampling* s, const float* p_meas,
+                        double* scratch, double* accum, ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cart(grid))) return rc;
+  if (!mu || !p_meas || !scratch || !accum) return set_err(CT_ERR_ARG, "null pointer");
+  CartGeo geo;
+  geo.init(mu, *grid);
+  rc = launch_fp<CartGeo, EPI_RESID>(geo, views, *batch, *s, p_meas, nullptr, nullptr, nullptr,
+                                     scratch, CT_STREAM(stream));
+  return rc ? rc : finish_residual(batch, scratch, accum, CT_STREAM(stream));
+}
+
+int ct_rowsum_max_cyl(const ct_cyl_grid* grid, const ct_ray_view* views, const ct_batch* batch,
+                      const ct_sampling* s, double* max_row, ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cyl(grid))) return rc;
+  if (!max_row) return set_err(CT_ERR_ARG, "null max_row");
+  if (cudaMemsetAsync(max_row, 0, sizeof(double) * batch->n_batch, CT_STREAM(stream)))
+    return check_launch("memset");
+  CylGeo geo;
+  geo.init(nullptr, *grid);
+  return launch_fp<CylGeo, EPI_ROWMAX>(geo, views, *batch, *s, nullptr, nullptr, nullptr,
+                                       nullptr, max_row, CT_STREAM(stream));
+}
+
+int ct_rowsum_max_cart(const ct_cart_grid* grid, const ct_ray_view* views,
+                       const ct_batch* batch, const ct_sampling* s, double* max_row,
+                       ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cart(grid))) return rc;
+  if (!max_row) return set_err(CT_ERR_ARG, "null max_row");
+  if (cudaMemsetAsync(max_row, 0, sizeof(double) * batch->n_batch, CT_STREAM(stream)))
+    return check_launch("memset");
+  CartGeo geo;
+  geo.init(nullptr, *grid);
+  return launch_fp<CartGeo, EPI_ROWMAX>(geo, views, *batch, *s, nullptr, nullptr, nullptr,
+                                        nullptr, max_row, CT_STREAM(stream));
+}
+
+static int check_bp(const float* corr, const ct_det_view* dets, const ct_batch* b) {
+  if (!corr || !dets || !b) return set_err(CT_ERR_ARG, "null corr/dets/batch");
+  if (b->n_batch < 1 || b->det_rows < 1 || b->det_cols < 1)
+    return set_err(CT_ERR_ARG, "bad batch dimensions");
+  return CT_OK;
+}
+
+int ct_bp_cyl(const float* corr, const ct_det_view* dets, const ct_batch* batch,
+              const ct_cyl_grid* grid, const double* trig, float* num, float* den,
+              int accumulate, ct_stream_t stream) {
+  int rc = check_bp(corr, dets, batch);
+  if (rc || (rc = check_cyl(grid))) return rc;
+  if (!trig || !num) return set_err(CT_ERR_ARG, "null trig/num");
+  CylVox vox;
+  vox.init(*grid, trig);
+  if (accumulate)
+    return launch_bp<CylVox, BP_ACC>(vox, corr, dets, *batch, num, den, nullptr, CT_STREAM(stream));
+  return launch_bp<CylVox, BP_WRITE>(vox, corr, dets, *batch, num, den, nullptr, CT_STREAM(stream));
+}
+
+int ct_bp_cart(const float* corr, const ct_det_view* dets, const ct_batch* batch,
+               const ct_cart_grid* grid, float* num, float* den, int accumulate,
+               ct_stream_t stream) {
+  int rc = check_bp(corr, dets, batch);
+  if (rc || (rc = check_cart(grid))) return rc;
+  if (!num) return set_err(CT_ERR_ARG, "null num");
+  CartVox vox;
+  vox.init(*grid);
+  if (accumulate)
+    return launch_bp<CartVox, BP_ACC>(vox, corr, dets, *batch, num, den, nullptr, CT_STREAM(stream));
+  return launch_bp<CartVox, BP_WRITE>(vox, corr, dets, *batch, num, den, nullptr, CT_STREAM(stream));
+}
+
+int ct_bp_cyl_update(const float* corr, const ct_det_view* dets, const ct_batch* batch,
+                     const ct_cyl_grid* grid, const double* trig, const ct_update* upd,
+                     ct_stream_t stream) {
+  int rc = check_bp(corr, dets, batch);
+  if (rc || (rc = check_cyl(grid))) return rc;
+  if (!trig || !upd || !upd->mu) return set_err(CT_ERR_ARG, "null trig/update/mu");
+  CylVox vox;
+  vox.init(*grid, trig);
+  return launch_bp<CylVox, BP_UPDATE>(vox, corr, dets, *batch, nullptr, nullptr, upd,
+                                      CT_STREAM(stream));
+}
+
+int ct_bp_cart_update(const float* corr, const ct_det_view* dets, const ct_batch* batch,
+                      const ct_cart_grid* grid, const ct_update* upd, ct_stream_t stream) {
+  int rc = check_bp(corr, dets, batch);
+  if (rc || (rc = check_cart(grid))) return rc;
+  if (!upd || !upd->mu) return set_err(CT_ERR_ARG, "null update/mu");
+  CartVox vox;
+  vox.init(*grid);
+  return launch_bp<CartVox, BP_UPDATE>(vox, corr, dets, *batch, nullptr, nullptr, upd,
+                                       CT_STREAM(stream));
+}
+
+int ct_cyl_trig(const ct_cyl_grid* grid, double* trig, ct_stream_t stream) {
+  int rc = check_cyl(grid);
+  if (rc) return rc;
+  if (!trig) return set_err(CT_ERR_ARG, "null trig");
+  trig_kernel<<<blocks_for(grid->n_theta, 256), 256, 0, CT_STREAM(stream)>>>(grid->n_theta, trig);
+  return check_launch("trig_kernel");
+}
+
+int ct_sart_update(const float* num, const float* den, int64_t offset, int64_t count,
+                   const ct_update* upd, ct_stream_t stream) {
+  if (!num || !den || !upd || !upd->mu || offset < 0 || count < 0)
+    return set_err(CT_ERR_ARG, "bad update arguments");
+  if (count == 0) return CT_OK;
+  update_kernel<<<blocks_for(count, 256), 256, 0, CT_STREAM(stream)>>>(num, den, offset, count,
+                                                                       *upd);
+  return check_launch("update_kernel");
+}
+
+int ct_sample_cyl(const float* mu, const ct_cyl_grid* grid, const double* rs, const double* ths,
+                  const double* hs, int64_t n, int nearest, float* out, ct_stream_t stream) {
+  int rc = check_cyl(grid);
+  if (rc) return rc;
+  if (!mu || !rs || !ths || !hs || !out || n < 0) return set_err(CT_ERR_ARG, "bad sample args");
+  if (n == 0) return CT_OK;
+  sample_cyl_kernel<<<blocks_for(n, 256), 256, 0, CT_STREAM(stream)>>>(mu, *grid, rs, ths, hs, n,
+                                                                       nearest, out);
+  return check_launch("sample_cyl_kernel");
+}
+
+int ct_sample_cart(const float* mu, const ct_cart_grid* grid, const double* xs, const double* ys,
+                   const double* zs, int64_t n, int nearest, float* out, ct_stream_t stream) {
+  int rc = check_cart(grid);
+  if (rc) return rc;
+  if (!mu || !xs || !ys || !zs || !out || n < 0) return set_err(CT_ERR_ARG, "bad sample args");
+  if (n == 0) return CT_OK;
+  sample_cart_kernel<<<blocks_for(n, 256), 256, 0, CT_STREAM(stream)>>>(mu, *grid, xs, ys, zs, n,
+                                                                        nearest, out);
+  return check_launch("sample_cart_kernel");
+}
+
+int ct_resample_cyl_to_cyl(const float* src_mu, const ct_cyl_grid* src, const ct_cyl_grid* dst,
+                           int nearest, float* dst_mu, ct_stream_t stream) {
+  int rc = check_cyl(src);
+  if (rc || (rc = check_cyl(dst))) return rc;
+  if (!src_mu || !dst_mu) return set_err(CT_ERR_ARG, "null volume");
+  const int64_t n = (int64_t)dst->n_h * dst->n_theta * dst->n_r;
+  resample_cyl_kernel<<<blocks_for(n, 256), 256, 0, CT_STREAM(stream)>>>(src_mu, *src, *dst,
+                                                                         nearest, dst_mu);
+  return check_launch("resample_cyl_kernel");
+}
+
+}  // extern "C"

@@ -1,0 +1,351 @@
+"""SART / OS-SART reconstruction on the B200 (drop-in for ``cyltomo/recon.py``).
+
+One SART view update (``cyltomo/recon.py:88-120``) is two kernels:
+
+1. ``ct_fp_*_correction`` -- forward projection of the view(s) whose
+   epilogue writes the correction image c = (p - sim) / w on valid pixels
+   (w > 1e-6 * max_row, ``recon.py:96-102``);
+2. ``ct_bp_*_update`` -- voxel-driven back-projection whose epilogue applies
+   mu += relaxation * w_m * num / den on touched voxels (den > 0, w_m != 0),
+   clamped at 0 when nonnegativity is on (``recon.py:105-119``).
+
+``n_subsets`` (new) turns this into OS-SART: subset s is
+the positions k of the projection order with k % S == s; every view of a
+subset is projected on the same mu, their corrections are back-projected
+and summed (num, den) in registers, and the update is applied once.
+S = P (or None) is exactly the reference's per-view SART.
+
+The row-sum maxima are pure geometry, so they are computed once per run
+without marching (``ct_rowsum_max_*``); an empty view therefore raises
+``EmptyView`` before any update is applied -- observably the same as the
+reference, whose partially updated volume is discarded with the exception.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _device as D
+from . import _native as N
+from .errors import ConfigError, EmptyRoi, EmptyView
+from .geometry import ScanGeometry
+from .grid import CartGrid, CartVolume, CylGrid, CylVolume, is_device_array
+from .projector import LINE_INTEGRAL, ProjectionSet, RaySamplingConfig
+
+ROW_SUM_SKIP_FRACTION = 1e-6  # cyltomo/recon.py:29
+
+
+@dataclass
+class SartConfig:
+    """Knobs of a (OS-)SART run (``cyltomo/recon.py:32-61``).
+
+    Reference fields keep their meaning.  Additions: ``n_subsets`` (None =
+    per-view SART; S < P = OS-SART with interleaved subsets) and
+    ``compute_residuals`` (the reference always evaluates ||p - A mu|| after
+    every pass, one extra full forward projection per pass).
+    """
+
+    relaxation: float = 1.0
+    n_iterations: int = 1
+    projection_order: str = "acquisition"
+    order_seed: int = 0
+    nonnegativity: bool = True
+    initial: object = None
+    weights: object = None
+    resample_initial: bool = False
+    sampling: RaySamplingConfig = field(default_factory=RaySamplingConfig)
+    n_subsets: int | None = None
+    compute_residuals: bool = True
+
+    def __post_init__(self):
+        if not 0.0 < self.relaxation <= 2.0:
+            raise ConfigError("relaxation must lie in (0, 2]")
+        if self.n_iterations < 1:
+            raise ConfigError("n_iterations must be >= 1")
+        if self.projection_order not in ("acquisition", "fixed_permutation"):
+            raise ConfigError(f"unknown projection order {self.projection_order!r}")
+        if self.n_subsets is not None and int(self.n_subsets) < 1:
+            raise ConfigError("n_subsets must be >= 1")
+
+
+@dataclass
+class ReconReport:
+    """Per-pass residual norms ||p - A mu||_2, wall time and config echo."""
+
+    residuals: list
+    wall_time: float
+    config: dict
+
+
+def _config_echo(cfg: SartConfig) -> dict:
+    return {
+        "relaxation": cfg.relaxation,
+        "n_iterations": cfg.n_iterations,
+        "projection_order": cfg.projection_order,
+        "order_seed": cfg.order_seed,
+        "nonnegativity": cfg.nonnegativity,
+        "initial": None if cfg.initial is None else f"volume{tuple(cfg.initial.mu.shape)}",
+        "weights": None if cfg.weights is None else f"map{tuple(np.shape(cfg.weights))}",
+        "step_mm": cfg.sampling.step,
+        "supersample": cfg.sampling.supersample,
+        "n_subsets": cfg.n_subsets,
+    }
+
+
+def projection_order(cfg: SartConfig, n_proj: int) -> np.ndarray:
+    """Acquisition order or the seeded fixed permutation (``recon.py:166-169``)."""
+    if cfg.projection_order == "fixed_permutation":
+        return np.random.default_rng(cfg.order_seed).permutation(n_proj)
+    return np.arange(n_proj)
+
+
+def make_subsets(order: np.ndarray, n_subsets: int | None) -> list:
+    """Interleaved OS-SART subsets: positions k of `order` with k % S == s."""
+    n = len(order)
+    s = n if n_subsets is None else min(int(n_subsets), n)
+    return [np.asarray(order[i::s], dtype=np.int64) for i in range(s)]
+
+
+class SartEngine:
+    """Device-resident tables and launchers for one (grid, geometry, sampling).
+
+    ``views`` restricts the tables to a subset of the geometry's views (slot b
+    of the tables is view views[b]); all launchers take device int32 slot
+    lists.
+    """
+
+    def __init__(self, grid, geom: ScanGeometry, sampling: RaySamplingConfig, views=None):
+        if not isinstance(grid, (CylGrid, CartGrid)):
+            raise TypeError(f"cannot reconstruct on {type(grid).__name__}")
+        self.device = D.require_cuda()
+        self.grid, self.geom = grid, geom
+        self.cyl = isinstance(grid, CylGrid)
+        self.views = np.arange(geom.n_proj) if views is None else np.asarray(views)
+        self.gc = D.grid_c(grid)
+        self.rows, self.cols = geom.det_rows, geom.det_cols
+        self.samp = D.sampling_c(sampling.step_for(grid), sampling.supersample,
+                                 sampling.interpolation == "nearest")
+        self.fp_views = D.upload_f64(D.ray_view_table(grid, geom, self.views))
+        self.bp_dets = D.upload_f64(D.det_view_table(geom, self.views))
+        self.trig = D.upload_f64(D.trig_table(grid)) if self.cyl else None
+        self.row_thr = None
+        self._scratch = {}
+
+    # -- geometry-only setup -------------------------------------------------
+    def row_max(self) -> np.ndarray:
+        """max_row of every table slot (exact; no march)."""
+        torch = D.torch_mod()
+        n = len(self.views)
+        out = torch.zeros(n, dtype=torch.float64, device=self.device)
+        b = D.batch_c(n, self.rows, self.cols)
+        fn = "ct_rowsum_max_cyl" if self.cyl else "ct_rowsum_max_cart"
+        N.call(fn, C.byref(self.gc), D.ptr(self.fp_views), C.byref(b), C.byref(self.samp),
+               D.ptr(out), D.stream_handle())
+        return D.to_host(out)
+
+    def prepare_thresholds(self, order_slots=None) -> np.ndarray:
+        """Row maxima -> skip thresholds; EmptyView for the first empty view."""
+        max_row = self.row_max()
+        check = range(len(self.views)) if order_slots is None else order_slots
+        for slot in check:
+            if max_row[slot] <= 0.0:
+                raise EmptyView(f"view {int(self.views[slot])} misses the volume entirely")
+        self.row_thr = D.upload_f64(ROW_SUM_SKIP_FRACTION * max_row)
+        return max_row
+
+    # -- launchers -------------------------------------------------------------
+    def correction(self, mu, p_meas, slots, n: int, corr) -> None:
+        b = D.batch_c(n, self.rows, self.cols, slots)
+        fn = "ct_fp_cyl_correction" if self.cyl else "ct_fp_cart_correction"
+        N.call(fn, D.ptr(mu), C.byref(self.gc), D.ptr(self.fp_views), C.byref(b),
+               C.byref(self.samp), D.ptr(p_meas), D.ptr(self.row_thr), D.ptr(corr),
+               D.stream_handle())
+
+    def bp_update(self, corr, slots, n: int, upd: N.UpdateC) -> None:
+        b = D.batch_c(n, self.rows, self.cols, slots)
+        if self.cyl:
+            N.call("ct_bp_cyl_update", D.ptr(corr), D.ptr(self.bp_dets), C.byref(b),
+                   C.byref(self.gc), D.ptr(self.trig), C.byref(upd), D.stream_handle())
+        else:
+            N.call("ct_bp_cart_update", D.ptr(corr), D.ptr(self.bp_dets), C.byref(b),
+                   C.byref(self.gc), C.byref(upd), D.stream_handle())
+
+    def bp_partial(self, corr, slots, n: int, num, den) -> None:
+        """num/den = sum over the batch of the BP (overwrites)."""
+        b = D.batch_c(n, self.rows, self.cols, slots)
+        if self.cyl:
+            N.call("ct_bp_cyl", D.ptr(corr), D.ptr(self.bp_dets), C.byref(b), C.byref(self.gc),
+                   D.ptr(self.trig), D.ptr(num), D.ptr(den), 0, D.stream_handle())
+        else:
+            N.call("ct_bp_cart", D.ptr(corr), D.ptr(self.bp_dets), C.byref(b),
+                   C.byref(self.gc), D.ptr(num), D.ptr(den), 0, D.stream_handle())
+
+    def residual(self, mu, p_meas, slots, n: int, accum) -> None:
+        """accum (device f64 scalar view) += sum (p - A mu)^2 over the batch."""
+        torch = D.torch_mod()
+        b = D.batch_c(n, self.rows, self.cols, slots)
+        length = int(N.load_library().ct_residual_scratch_len(C.byref(b)))
+        key = (n, length)
+        if key not in self._scratch:
+            self._scratch[key] = torch.empty(length, dtype=torch.float64, device=self.device)
+        fn = "ct_fp_cyl_residual" if self.cyl else "ct_fp_cart_residual"
+        N.call(fn, D.ptr(mu), C.byref(self.gc), D.ptr(self.fp_views), C.byref(b),
+               C.byref(self.samp), D.ptr(p_meas), D.ptr(self._scratch[key]), D.ptr(accum),
+               D.stream_handle())
+
+
+def make_update(mu, weights, cfg: SartConfig) -> N.UpdateC:
+    u = N.UpdateC()
+    u.relaxation = float(cfg.relaxation)
+    u.nonneg = 1 if cfg.nonnegativity else 0
+    u.weights = None if weights is None else weights.data_ptr()
+    u.mu = mu.data_ptr()
+    return u
+
+
+def _device_weights(cfg: SartConfig, shape, device):
+    if cfg.weights is None:
+        return None
+    if tuple(np.shape(cfg.weights)) != tuple(shape):
+        raise ConfigError("weight map shape does not match the volume")
+    return D.to_device(cfg.weights, device=device)
+
+
+def _volume_cls(grid):
+    return CylVolume if isinstance(grid, CylGrid) else CartVolume
+
+
+def sart_update_view(vol, ps: ProjectionSet, i: int, cfg: SartConfig):
+    """Apply the SART correction of view i to the volume, in place
+    (``cyltomo/recon.py:88-120``).  Raises EmptyView when no ray of the view
+    intersects the volume."""
+    if ps.kind != LINE_INTEGRAL:
+        raise ConfigError("SART needs line-integral projections")
+    torch = D.torch_mod()
+    i = int(i)
+    eng = SartEngine(vol.grid, ps.geom, cfg.sampling, views=[i])
+    eng.prepare_thresholds()
+    dev = eng.device
+    mu = D.to_device(vol.mu, device=dev)
+    weights = _device_weights(cfg, mu.shape, dev)
+    p_meas = D.to_device(ps.images[i:i + 1], device=dev)
+    corr = torch.empty((1, eng.rows, eng.cols), dtype=torch.float32, device=dev)
+    slots = D.upload_i32([0])
+    eng.correction(mu, p_meas, slots, 1, corr)
+    eng.bp_update(corr, slots, 1, make_update(mu, weights, cfg))
+    if is_device_array(vol.mu):
+        if vol.mu.data_ptr() != mu.data_ptr():
+            vol.mu.copy_(mu)
+    else:
+        vol.mu[...] = D.to_host(mu)
+    return vol
+
+
+def _initial_mu(grid, cfg: SartConfig, device):
+    """Zeros, a copy of the template, or its resampling (``recon.py:123-145``)."""
+    torch = D.torch_mod()
+    init = cfg.initial
+    if init is None:
+        return torch.zeros(grid.shape, dtype=torch.float32, device=device)
+    if isinstance(grid, CylGrid):
+        if not isinstance(init, CylVolume):
+            raise ConfigError("initial volume must be cylindrical for a CylGrid run")
+        same = (init.grid.shape == grid.shape and init.grid.radius == grid.radius
+                and init.grid.height == grid.height)
+        if same:
+            return D.to_device(init.mu, device=device).clone()
+        if not cfg.resample_initial:
+            raise ConfigError("initial volume shape does not match the grid; "
+                              "set resample_initial to resample the template")
+        from ._device import resample_cyl_to_cyl
+        res = resample_cyl_to_cyl(CylVolume(init.grid, D.to_device(init.mu, device=device)),
+                                  grid)
+        return res.mu
+    if not isinstance(init, CartVolume) or init.grid.shape != grid.shape:
+        raise ConfigError("initial volume must match the Cartesian grid")
+    return D.to_device(init.mu, device=device).clone()
+
+
+class SartRun:
+    """A prepared (OS-)SART reconstruction: tables, thresholds, buffers.
+
+    ``sart_run`` is ``SartRun(...).run()``; the bench and the distributed
+    driver use the object directly to time passes and reuse buffers.
+    """
+
+    def __init__(self, ps: ProjectionSet, grid, cfg: SartConfig):
+        if ps.kind != LINE_INTEGRAL:
+            raise ConfigError("SART needs line-integral projections")
+        torch = D.torch_mod()
+        self.ps, self.grid, self.cfg = ps, grid, cfg
+        self.eng = SartEngine(grid, ps.geom, cfg.sampling)
+        dev = self.eng.device
+        self.mu = _initial_mu(grid, cfg, dev)
+        self.order = projection_order(cfg, ps.geom.n_proj)
+        self.subsets = make_subsets(self.order, cfg.n_subsets)
+        self.eng.prepare_thresholds(order_slots=self.order)
+        self.weights = _device_weights(cfg, grid.shape, dev)
+        self.p_meas = D.to_device(ps.images, device=dev)
+        self.subset_slots = [D.upload_i32(s) for s in self.subsets]
+        self.all_slots = D.upload_i32(np.arange(ps.geom.n_proj))
+        nmax = max(len(s) for s in self.subsets)
+        self.corr = torch.empty((nmax, self.eng.rows, self.eng.cols), dtype=torch.float32,
+                                device=dev)
+        self.upd = make_update(self.mu, self.weights, cfg)
+        self.resid = torch.zeros(cfg.n_iterations, dtype=torch.float64, device=dev)
+        self.passes_done = 0
+
+    def run_pass(self, residual: bool | None = None) -> None:
+        """One pass over all subsets (+ the residual FP if enabled)."""
+        e = self.eng
+        for s, slots in zip(self.subsets, self.subset_slots):
+            e.correction(self.mu, self.p_meas, slots, len(s), self.corr)
+            e.bp_update(self.corr, slots, len(s), self.upd)
+        want = self.cfg.compute_residuals if residual is None else residual
+        if want:
+            k = min(self.passes_done, self.resid.numel() - 1)
+            e.residual(self.mu, self.p_meas, self.all_slots, self.ps.geom.n_proj,
+                       self.resid[k:k + 1])
+        self.passes_done += 1
+
+    def run(self):
+        torch = D.torch_mod()
+        t0 = time.perf_counter()
+        for _ in range(self.cfg.n_iterations):
+            self.run_pass()
+        torch.cuda.synchronize(self.eng.device)
+        wall = time.perf_counter() - t0
+        residuals = ([math.sqrt(float(x)) for x in D.to_host(self.resid)]
+                     if self.cfg.compute_residuals else [])
+        mu = self.mu if self.ps.on_device else D.to_host(self.mu)
+        vol = _volume_cls(self.grid)(self.grid, mu)
+        return vol, ReconReport(residuals=residuals, wall_time=wall,
+                                config=_config_echo(self.cfg))
+
+
+def sart_run(ps: ProjectionSet, grid, cfg: SartConfig | None = None):
+    """Run (OS-)SART on an object-aligned grid; returns (volume, ReconReport)
+    (``cyltomo/recon.py:156-182``).  The grid carries the pose, so a template
+    initial volume in object coordinates aligns automatically."""
+    cfg = cfg or SartConfig()
+    return SartRun(ps, grid, cfg).run()
+
+
+def presence_metric(vol, roi) -> float:
+    """Mean attenuation over a region (``cyltomo/recon.py:185-200``)."""
+    mu = D.to_host(vol.mu) if is_device_array(vol.mu) else np.asarray(vol.mu)
+    if hasattr(roi, "mask"):
+        mask = roi.mask(vol.grid)
+    else:
+        mask = np.asarray(roi, dtype=bool)
+        if mask.shape != mu.shape:
+            raise EmptyRoi("roi mask shape does not match the volume")
+    n = int(mask.sum())
+    if n == 0:
+        raise EmptyRoi("region contains no voxels")
+    return float(mu[mask].astype(np.float64).mean())

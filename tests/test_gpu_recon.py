@@ -1,0 +1,288 @@
+"""GPU parity of the fused SART / OS-SART path.
+
+Ports every case of the reference's tests/test_recon.py to the B200 API
+(bit-exact invariants stay bit-exact), and checks reconstructions against the
+unmodified reference's outputs (golden) and the oracle: within 1e-3 relative
+L2 after N iterations (north_star).
+"""
+
+import warnings
+
+import numpy as np
+import pytest
+
+import paper_2005_11976_b200 as P
+from paper_2005_11976_b200 import (CartGrid, CartVolume, ComponentSpec, CylGrid, CylVolume,
+                                   Pose, ProjectionSet, RaySamplingConfig, SartConfig,
+                                   ScanGeometry, forward_project_all, make_assembly_phantom,
+                                   make_circular_trajectory, sart_run, sart_update_view)
+from paper_2005_11976_b200.errors import ConfigError, EmptyView
+
+pytestmark = pytest.mark.gpu
+
+RECON_TOL = 1e-3   # north_star: reconstructions within 1e-3 relative L2
+FINE = RaySamplingConfig(step=0.01)
+
+
+def rel_l2(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def tiny_system():
+    """3x3x1 Cartesian system with its explicit-matrix LS oracle (test_recon.py:14-32)."""
+    rng = np.random.default_rng(7)
+    grid = CartGrid.centered(3, 3, 1, 1.0)
+    geom = ScanGeometry(15.0, 10.0, 9, 3, 0.7, (4.0, 1.0),
+                        make_circular_trajectory(8, np.radians(200.0)))
+    a_mat = np.zeros((geom.n_proj * geom.det_rows * geom.det_cols, 9))
+    for l in range(9):
+        e = np.zeros(9)
+        e[l] = 1.0
+        ps_e = forward_project_all(CartVolume(grid, e.reshape(grid.shape)), geom, FINE)
+        a_mat[:, l] = ps_e.images.astype(np.float64).ravel()
+    mu_true = rng.uniform(0.2, 1.0, size=9)
+    ps = forward_project_all(CartVolume(grid, mu_true.reshape(grid.shape)), geom, FINE)
+    mu_star, *_ = np.linalg.lstsq(a_mat, ps.images.astype(np.float64).ravel(), rcond=None)
+    return grid, geom, ps, mu_star
+
+
+@pytest.fixture
+def small_cyl_setup(desk_geometry):
+    grid = CylGrid(6, 12, 8, radius=6.0, height=20.0)
+    body = ComponentSpec("body", mu=0.03)
+    insert = ComponentSpec("insert", mu=0.2, r_range=(0.0, 2.0), h_range=(-4.0, 4.0))
+    with pytest.warns(UserWarning):
+        vol = make_assembly_phantom([body, insert], grid)
+    return grid, vol, forward_project_all(vol, desk_geometry)
+
+
+class TestScalarUpdate:
+    def _setup(self):
+        grid = CylGrid(1, 1, 1, radius=0.5, height=4.0)
+        geom = ScanGeometry(15.0, 10.0, 1, 1, 1.0, (0.0, 0.0), [0.0])
+        return grid, geom, ProjectionSet(geom, np.full((1, 1, 1), 2.0))
+
+    @pytest.mark.parametrize("relax,w,expected", [(1.0, None, 2.0), (1.0, 0.5, 1.0),
+                                                  (0.25, None, 0.5)])
+    def test_scalar_updates(self, relax, w, expected):
+        grid, geom, ps = self._setup()
+        vol = CylVolume.zeros(grid)
+        weights = None if w is None else np.full(grid.shape, w)
+        cfg = SartConfig(relaxation=relax, weights=weights, sampling=RaySamplingConfig(step=0.1))
+        sart_update_view(vol, ps, 0, cfg)
+        assert vol.mu[0, 0, 0] == pytest.approx(expected, rel=1e-6)
+
+
+class TestFixedPointAndInvariants:
+    def test_consistent_data_is_fixed_point(self, small_cyl_setup):
+        grid, vol, ps = small_cyl_setup
+        work = CylVolume(grid, vol.mu.copy())
+        cfg = SartConfig(n_iterations=3)
+        for _ in range(3):
+            for i in range(ps.geom.n_proj):
+                sart_update_view(work, ps, i, cfg)
+        assert np.array_equal(work.mu, vol.mu)
+
+    def test_fixed_point_through_sart_run(self, small_cyl_setup):
+        grid, vol, ps = small_cyl_setup
+        out, _ = sart_run(ps, grid, SartConfig(n_iterations=2, initial=vol))
+        assert np.array_equal(out.mu, vol.mu)
+        out, _ = sart_run(ps, grid, SartConfig(n_iterations=2, initial=vol, n_subsets=3))
+        assert np.array_equal(out.mu, vol.mu)
+
+    def test_weight_zero_voxels_bit_identical(self, small_cyl_setup, rng):
+        grid, vol, ps = small_cyl_setup
+        weights = rng.random(grid.shape)
+        weights[weights < 0.3] = 0.0
+        frozen = weights == 0.0
+        init = CylVolume(grid, rng.random(grid.shape) * 0.01)
+        before = init.mu.copy()
+        out, _ = sart_run(ps, grid, SartConfig(n_iterations=2, weights=weights, initial=init))
+        assert np.array_equal(out.mu[frozen], before[frozen])
+        assert not np.array_equal(out.mu[~frozen], before[~frozen])
+
+    def test_all_ones_weights_equal_unweighted(self, small_cyl_setup):
+        grid, vol, ps = small_cyl_setup
+        plain, _ = sart_run(ps, grid, SartConfig(n_iterations=2))
+        weighted, _ = sart_run(ps, grid, SartConfig(n_iterations=2, weights=np.ones(grid.shape)))
+        assert np.array_equal(plain.mu, weighted.mu)
+
+    def test_nonnegativity_flag(self, small_cyl_setup, rng):
+        grid, vol, ps = small_cyl_setup
+        noisy = ProjectionSet(ps.geom, ps.images + rng.normal(0, 0.1, ps.images.shape))
+        clamped, _ = sart_run(noisy, grid, SartConfig(n_iterations=2))
+        assert clamped.mu.min() >= 0.0
+        free, _ = sart_run(noisy, grid, SartConfig(n_iterations=2, nonnegativity=False))
+        assert free.mu.min() < 0.0
+
+
+class TestOracleConvergence:
+    def test_converges_to_least_squares_solution(self, tiny_system):
+        grid, geom, ps, mu_star = tiny_system
+        vol, report = sart_run(ps, grid, SartConfig(relaxation=1.0, n_iterations=40,
+                                                    sampling=FINE))
+        assert np.abs(vol.mu.ravel() - mu_star).max() < 1e-3
+        assert len(report.residuals) == 40
+
+    def test_monotone_residual_first_passes(self, tiny_system):
+        grid, geom, ps, mu_star = tiny_system
+        _, report = sart_run(ps, grid, SartConfig(relaxation=0.8, n_iterations=10,
+                                                  sampling=FINE))
+        res = report.residuals
+        for a, b in zip(res, res[1:]):
+            assert b <= a * (1 + 1e-5) + 1e-7   # fp32 data: round-off floor ~1e-7
+
+    def test_initial_template_lowers_first_pass_residual(self, small_cyl_setup):
+        grid, vol, ps = small_cyl_setup
+        _, plain = sart_run(ps, grid, SartConfig(n_iterations=1))
+        _, primed = sart_run(ps, grid, SartConfig(n_iterations=1,
+                                                  initial=CylVolume(grid, vol.mu.copy())))
+        assert primed.residuals[0] < plain.residuals[0]
+
+
+class TestRunConfiguration:
+    def test_initial_shape_mismatch_needs_resampling(self, small_cyl_setup):
+        grid, vol, ps = small_cyl_setup
+        template = CylVolume.full(CylGrid(3, 6, 4, grid.radius, grid.height), 0.03)
+        with pytest.raises(ConfigError):
+            sart_run(ps, grid, SartConfig(initial=template))
+        out, _ = sart_run(ps, grid, SartConfig(initial=template, resample_initial=True))
+        assert out.mu.shape == grid.shape
+
+    def test_requires_line_integrals(self, small_cyl_setup):
+        grid, vol, ps = small_cyl_setup
+        intens = ProjectionSet(ps.geom, np.exp(-ps.images), kind="intensity")
+        with pytest.raises(ConfigError):
+            sart_update_view(CylVolume.zeros(grid), intens, 0, SartConfig())
+
+    def test_fixed_permutation_deterministic(self, small_cyl_setup):
+        grid, vol, ps = small_cyl_setup
+        cfg = dict(n_iterations=1, projection_order="fixed_permutation", order_seed=3)
+        a, _ = sart_run(ps, grid, SartConfig(**cfg))
+        b, _ = sart_run(ps, grid, SartConfig(**cfg))
+        assert np.array_equal(a.mu, b.mu)
+
+    def test_empty_view_raises(self):
+        geom = ScanGeometry(15.0, 10.0, 3, 3, 0.1, (1.0, 1.0), [0.0])
+        grid = CylGrid(2, 4, 4, radius=0.5, height=1.0, pose=Pose(t=[50.0, 0.0, 0.0]))
+        ps = ProjectionSet(geom, np.zeros((1, 3, 3)))
+        with pytest.raises(EmptyView):
+            sart_update_view(CylVolume.zeros(grid), ps, 0, SartConfig())
+        with pytest.raises(EmptyView):
+            sart_run(ps, grid, SartConfig())
+
+    def test_weight_shape_validated(self, small_cyl_setup):
+        grid, vol, ps = small_cyl_setup
+        with pytest.raises(ConfigError):
+            sart_run(ps, grid, SartConfig(weights=np.ones((2, 2, 2))))
+
+
+# ---------------------------------------------------------------------------
+# parity against the unmodified reference (golden) and the oracle
+# ---------------------------------------------------------------------------
+def _desk():
+    return ScanGeometry(791.0, 679.0, 65, 33, 0.748, (32.0, 16.0),
+                        make_circular_trajectory(8, np.radians(200.0)))
+
+
+@pytest.mark.parametrize("name", ["plain", "weighted", "free", "perm"])
+def test_golden_sart_runs(golden_sart, name):
+    geom = _desk()
+    grid = CylGrid(6, 12, 8, radius=6.0, height=20.0)
+    ps = ProjectionSet(geom, golden_sart["sart_noisy"])
+    kw = dict(n_iterations=2)
+    if name == "plain":
+        kw["relaxation"] = 0.7
+    if name == "weighted":
+        kw.update(weights=golden_sart["sart_weights"],
+                  initial=CylVolume(grid, golden_sart["sart_init"]))
+    if name == "free":
+        kw["nonnegativity"] = False
+    if name == "perm":
+        kw.update(projection_order="fixed_permutation", order_seed=3)
+    out, rep = sart_run(ps, grid, SartConfig(**kw))
+    assert rel_l2(out.mu, golden_sart[f"sart_{name}_mu"]) < RECON_TOL
+    assert np.allclose(rep.residuals, golden_sart[f"sart_{name}_res"], rtol=1e-3)
+
+
+def test_golden_single_view_posed(golden_sart):
+    geom = _desk()
+    grid = CylGrid(6, 12, 8, 6.0, 20.0, Pose(0.2, 0.15, -0.2, t=[0.4, -0.5, 0.3]))
+    v = CylVolume.zeros(grid)
+    sart_update_view(v, ProjectionSet(geom, golden_sart["sart_noisy"]), 3,
+                     SartConfig(relaxation=0.9))
+    assert rel_l2(v.mu, golden_sart["sart_view3_posed_mu"]) < 1e-5
+
+
+def test_golden_least_squares(golden_sart):
+    cg = CartGrid.centered(3, 3, 1, 1.0)
+    tg = ScanGeometry(15.0, 10.0, 9, 3, 0.7, (4.0, 1.0),
+                      make_circular_trajectory(8, np.radians(200.0)))
+    out, _ = sart_run(ProjectionSet(tg, golden_sart["ls_images"]), cg,
+                      SartConfig(relaxation=1.0, n_iterations=40, sampling=FINE))
+    assert rel_l2(out.mu.ravel(), golden_sart["ls_sart_mu"].ravel()) < RECON_TOL
+    assert np.abs(out.mu.ravel() - golden_sart["ls_mu_star"]).max() < 1e-3
+
+
+def _c1_inputs(oracle):
+    import hashlib
+    from paper_2005_11976_b200 import workloads as W
+    wl = W.c1_small()
+    clean = np.stack([oracle.forward(wl.mu, wl.grid, wl.geom, i)[0]
+                      for i in range(wl.geom.n_proj)]).astype(np.float32)
+    noisy = W.add_noise(clean, wl.noise_frac, wl.seed)
+    return wl, noisy, hashlib.sha256(noisy.tobytes()).hexdigest()
+
+
+def test_c1_full_sart_against_reference(oracle, golden_c1):
+    """Config 0 (C1) end to end: 10 SART iterations from zero, lambda 0.5, on the
+    reference's own noisy projections; within 1e-3 of the reference's volume."""
+    wl, noisy, digest = _c1_inputs(oracle)
+    assert digest == bytes(golden_c1["c1_noisy_sha256"]).decode()
+    out, rep = sart_run(ProjectionSet(wl.geom, noisy), wl.grid,
+                        SartConfig(relaxation=wl.relaxation, n_iterations=wl.n_iterations))
+    err = rel_l2(out.mu, golden_c1["c1_sart_mu"])
+    assert err < RECON_TOL, err
+    assert np.allclose(rep.residuals, golden_c1["c1_sart_res"], rtol=1e-3)
+
+
+def test_os_sart_against_oracle(oracle):
+    """A19 OS-SART (no reference symbol): against the oracle's composition of
+    reference primitives on a posed, weighted problem."""
+    rng = np.random.default_rng(31)
+    geom = ScanGeometry(400.0, 200.0, 48, 40, 0.2, (23.5, 19.5),
+                        P.full_turn_angles(24))
+    grid = CylGrid(20, 32, 16, 4.0, 8.0, Pose.tilt(0.7, 0.08, [0.3, -0.2, 0.1]))
+    truth = (rng.random(grid.shape) * 0.05).astype(np.float32)
+    weights = rng.uniform(0.2, 1.0, grid.shape).astype(np.float32)
+    images = np.stack([oracle.forward(truth, grid, geom, i)[0]
+                       for i in range(geom.n_proj)]).astype(np.float32)
+    order = np.random.default_rng(5).permutation(geom.n_proj)
+    mu_o, res_o = oracle.sart(images, grid, geom, relaxation=0.3, n_iterations=3,
+                              order=order, weights=weights, n_subsets=4)
+    out, rep = sart_run(ProjectionSet(geom, images), grid,
+                        SartConfig(relaxation=0.3, n_iterations=3, weights=weights,
+                                   projection_order="fixed_permutation", order_seed=5,
+                                   n_subsets=4))
+    assert rel_l2(out.mu, mu_o) < RECON_TOL
+    assert np.allclose(rep.residuals, res_o, rtol=1e-3)
+
+
+def test_os_sart_with_p_subsets_equals_sart(small_cyl_setup):
+    grid, vol, ps = small_cyl_setup
+    a, _ = sart_run(ps, grid, SartConfig(n_iterations=2, relaxation=0.6))
+    b, _ = sart_run(ps, grid, SartConfig(n_iterations=2, relaxation=0.6,
+                                         n_subsets=ps.geom.n_proj))
+    assert np.array_equal(a.mu, b.mu)
+
+
+def test_device_resident_run_matches_host(small_cyl_setup):
+    import torch
+    grid, vol, ps = small_cyl_setup
+    host, _ = sart_run(ps, grid, SartConfig(n_iterations=2, n_subsets=2))
+    dps = ProjectionSet(ps.geom, torch.as_tensor(ps.images, device="cuda"))
+    dev, _ = sart_run(dps, grid, SartConfig(n_iterations=2, n_subsets=2))
+    assert dev.mu.is_cuda
+    assert np.array_equal(dev.mu.cpu().numpy(), host.mu)
