@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define CT_ABI_VERSION 1
+#define CT_ABI_VERSION 2
 
 #define CT_OK 0
 #define CT_ERR_ARG (-1)   /* invalid argument (null pointer, bad size) */
@@ -113,14 +113,20 @@ const char *ct_arch(void);
 /* ---- forward projection (cyltomo/_kernels.py:238-293 forward_cyl,
  *      :296-343 forward_cart) ---------------------------------------------- */
 
+/* `gather` (optional, may be NULL): the gather layout of the same mu built by
+ * ct_pack_gather_* (8 floats per voxel: its 2x2x2 trilinear neighbourhood,
+ * one 32-byte sector).  With it every FP sample is two 16-byte loads from one
+ * sector instead of eight scattered 4-byte loads; results are identical.
+ * It must be rebuilt after mu changes. */
+
 /* forward_cyl over a batch of views: out_p / out_w are [n_batch][rows][cols]
  * (OVERWRITTEN).  out_w = in-support sample count * step / ss^2 (the SART row
  * sums, cyltomo/projector.py:100-103); out_w may be NULL. */
-int ct_fp_cyl(const float *mu, const ct_cyl_grid *grid, const ct_ray_view *views,
+int ct_fp_cyl(const float *mu, const float *gather, const ct_cyl_grid *grid, const ct_ray_view *views,
               const ct_batch *batch, const ct_sampling *sampling,
               float *out_p, float *out_w, ct_stream_t stream);
 
-int ct_fp_cart(const float *mu, const ct_cart_grid *grid, const ct_ray_view *views,
+int ct_fp_cart(const float *mu, const float *gather, const ct_cart_grid *grid, const ct_ray_view *views,
                const ct_batch *batch, const ct_sampling *sampling,
                float *out_p, float *out_w, ct_stream_t stream);
 
@@ -128,11 +134,11 @@ int ct_fp_cart(const float *mu, const ct_cart_grid *grid, const ct_ray_view *vie
  *   corr[b] = (w > row_thr[v]) ? (p_meas[v] - sim) / w : 0,   v = view_ids[b]
  * row_thr (device, float64, [P]) = ROW_SUM_SKIP_FRACTION * max_row per view
  * (ct_rowsum_max_*).  corr is [n_batch][rows][cols]. */
-int ct_fp_cyl_correction(const float *mu, const ct_cyl_grid *grid, const ct_ray_view *views,
+int ct_fp_cyl_correction(const float *mu, const float *gather, const ct_cyl_grid *grid, const ct_ray_view *views,
                          const ct_batch *batch, const ct_sampling *sampling,
                          const float *p_meas, const double *row_thr, float *corr,
                          ct_stream_t stream);
-int ct_fp_cart_correction(const float *mu, const ct_cart_grid *grid, const ct_ray_view *views,
+int ct_fp_cart_correction(const float *mu, const float *gather, const ct_cart_grid *grid, const ct_ray_view *views,
                           const ct_batch *batch, const ct_sampling *sampling,
                           const float *p_meas, const double *row_thr, float *corr,
                           ct_stream_t stream);
@@ -142,11 +148,11 @@ int ct_fp_cart_correction(const float *mu, const ct_cart_grid *grid, const ct_ra
  * *accum (device double).  `scratch` must hold ct_residual_scratch_len()
  * doubles. */
 int64_t ct_residual_scratch_len(const ct_batch *batch);
-int ct_fp_cyl_residual(const float *mu, const ct_cyl_grid *grid, const ct_ray_view *views,
+int ct_fp_cyl_residual(const float *mu, const float *gather, const ct_cyl_grid *grid, const ct_ray_view *views,
                        const ct_batch *batch, const ct_sampling *sampling,
                        const float *p_meas, double *scratch, double *accum,
                        ct_stream_t stream);
-int ct_fp_cart_residual(const float *mu, const ct_cart_grid *grid, const ct_ray_view *views,
+int ct_fp_cart_residual(const float *mu, const float *gather, const ct_cart_grid *grid, const ct_ray_view *views,
                         const ct_batch *batch, const ct_sampling *sampling,
                         const float *p_meas, double *scratch, double *accum,
                         ct_stream_t stream);
@@ -191,6 +197,16 @@ int ct_cyl_trig(const ct_cyl_grid *grid, double *trig, ct_stream_t stream);
  * (the multi-GPU path: BP partials -> NCCL reduce-scatter -> this). */
 int ct_sart_update(const float *num, const float *den, int64_t offset, int64_t count,
                    const ct_update *upd, ct_stream_t stream);
+
+/* ---- gather layout for the forward projector ------------------------------ */
+/* Number of floats of the gather buffer for a volume of n_voxels (8 per voxel). */
+int64_t ct_gather_floats(int64_t n_voxels);
+/* gather[8m..8m+7] = mu at (k,j,i),(k,j,i+1),(k,j+1,i),(k,j+1,i+1), then the same
+ * at k+1 (r/h clamp, theta wraps; Cartesian: all three clamp).  16B aligned. */
+int ct_pack_gather_cyl(const float *mu, const ct_cyl_grid *grid, float *gather,
+                       ct_stream_t stream);
+int ct_pack_gather_cart(const float *mu, const ct_cart_grid *grid, float *gather,
+                        ct_stream_t stream);
 
 /* ---- point sampling (cyltomo/_kernels.py:154-163, grid.py:261-319) ------- */
 int ct_sample_cyl(const float *mu, const ct_cyl_grid *grid, const double *rs,

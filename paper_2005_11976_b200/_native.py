@@ -19,7 +19,7 @@ LIB_NAME = "libcyltomo_b200.so"
 LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
 
 CT_OK = 0
-CT_ABI_VERSION = 1
+CT_ABI_VERSION = 2
 
 
 class CylGridC(C.Structure):
@@ -63,19 +63,22 @@ _SIGNATURES = {
     "ct_abi_version": (C.c_int, []),
     "ct_last_error": (C.c_char_p, []),
     "ct_arch": (C.c_char_p, []),
-    "ct_fp_cyl": (C.c_int, [P, C.POINTER(CylGridC), P, C.POINTER(BatchC),
+    "ct_fp_cyl": (C.c_int, [P, P, C.POINTER(CylGridC), P, C.POINTER(BatchC),
                             C.POINTER(SamplingC), P, P, P]),
-    "ct_fp_cart": (C.c_int, [P, C.POINTER(CartGridC), P, C.POINTER(BatchC),
+    "ct_fp_cart": (C.c_int, [P, P, C.POINTER(CartGridC), P, C.POINTER(BatchC),
                              C.POINTER(SamplingC), P, P, P]),
-    "ct_fp_cyl_correction": (C.c_int, [P, C.POINTER(CylGridC), P, C.POINTER(BatchC),
+    "ct_fp_cyl_correction": (C.c_int, [P, P, C.POINTER(CylGridC), P, C.POINTER(BatchC),
                                        C.POINTER(SamplingC), P, P, P, P]),
-    "ct_fp_cart_correction": (C.c_int, [P, C.POINTER(CartGridC), P, C.POINTER(BatchC),
+    "ct_fp_cart_correction": (C.c_int, [P, P, C.POINTER(CartGridC), P, C.POINTER(BatchC),
                                         C.POINTER(SamplingC), P, P, P, P]),
     "ct_residual_scratch_len": (C.c_int64, [C.POINTER(BatchC)]),
-    "ct_fp_cyl_residual": (C.c_int, [P, C.POINTER(CylGridC), P, C.POINTER(BatchC),
+    "ct_fp_cyl_residual": (C.c_int, [P, P, C.POINTER(CylGridC), P, C.POINTER(BatchC),
                                      C.POINTER(SamplingC), P, P, P, P]),
-    "ct_fp_cart_residual": (C.c_int, [P, C.POINTER(CartGridC), P, C.POINTER(BatchC),
+    "ct_fp_cart_residual": (C.c_int, [P, P, C.POINTER(CartGridC), P, C.POINTER(BatchC),
                                       C.POINTER(SamplingC), P, P, P, P]),
+    "ct_gather_floats": (C.c_int64, [C.c_int64]),
+    "ct_pack_gather_cyl": (C.c_int, [P, C.POINTER(CylGridC), P, P]),
+    "ct_pack_gather_cart": (C.c_int, [P, C.POINTER(CartGridC), P, P]),
     "ct_rowsum_max_cyl": (C.c_int, [C.POINTER(CylGridC), P, C.POINTER(BatchC),
                                     C.POINTER(SamplingC), P, P]),
     "ct_rowsum_max_cart": (C.c_int, [C.POINTER(CartGridC), P, C.POINTER(BatchC),

@@ -72,19 +72,79 @@ __device__ __forceinline__ void subray_dir(const ct_ray_view& v, double cu, doub
   d[2] = ddiv(dz, norm);
 }
 
+
+// ---------------------------------------------------------------------------
+// fp32 sampling helpers (no XU-pipe conversions on the hot loop)
+// ---------------------------------------------------------------------------
+// floor(x) for 0 <= x < 2^22 on the FMA pipe: x + 2^23 rounded toward -inf is
+// floor(x) + 2^23 exactly; its bit pattern minus 0x4B000000 is the integer.
+__device__ __forceinline__ float floor_pos(float x, int& i) {
+  const float t = __fadd_rd(x, 8388608.0f);
+  i = __float_as_int(t) - 0x4B000000;
+  return t - 8388608.0f;
+}
+
+// 1/x from the MUFU approximation + one Newton step (~1 ulp)
+__device__ __forceinline__ float rcp_nr(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return fmaf(r, fmaf(-x, r, 1.0f), r);
+}
+
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// theta = atan2(y, x) mapped to [0, 2pi) as the reference does (_kernels.py:287-289):
+// octant reduction + a degree-15 odd minimax polynomial (|err| < 4e-8 rad).
+__device__ __forceinline__ float theta_2pi(float y, float x) {
+  const float ax = fabsf(x), ay = fabsf(y);
+  const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+  float a = __fdividef(mn, mx);
+  a = (mx > 0.0f) ? a : 0.0f;
+  const float s = a * a;
+  float p = -0.004056010747295693f;
+  p = fmaf(p, s, 0.021868032862667357f);
+  p = fmaf(p, s, -0.05591941387629666f);
+  p = fmaf(p, s, 0.09642697029858746f);
+  p = fmaf(p, s, -0.1390881621254663f);
+  p = fmaf(p, s, 0.19946600950804824f);
+  p = fmaf(p, s, -0.33329863673815296f);
+  p = fmaf(p, s, 0.9999993362453462f);
+  float t = a * p;
+  t = (ay > ax) ? (1.57079632679489662f - t) : t;
+  t = (x < 0.0f) ? (3.14159265358979324f - t) : t;
+  return (y < 0.0f) ? (kTwoPiF - t) : t;
+}
+
+__device__ __forceinline__ float lerp8(float4 a, float4 b, float wr, float wt, float wh) {
+  // a = (k0,j0,i0) (k0,j0,i1) (k0,j1,i0) (k0,j1,i1); b = same at k1
+  const float c00 = fmaf(a.y - a.x, wr, a.x);
+  const float c01 = fmaf(a.w - a.z, wr, a.z);
+  const float c10 = fmaf(b.y - b.x, wr, b.x);
+  const float c11 = fmaf(b.w - b.z, wr, b.z);
+  const float q0 = fmaf(c01 - c00, wt, c00);
+  const float q1 = fmaf(c11 - c10, wt, c10);
+  return fmaf(q1 - q0, wh, q0);
+}
+
 // ---------------------------------------------------------------------------
 // grid policies: support interval (fp64), last-sample test (fp64) and the
 // fp32 trilinear sample
 // ---------------------------------------------------------------------------
 struct CylGeo {
   const float* __restrict__ mu;
+  const float4* __restrict__ oct;  // gather layout (ct_pack_gather_cyl) or null
   int nh, nt, nr;
   double radius, half_h;
   // fp32 sampling constants
   float inv_dr, inv_dth, inv_dh, h_off, nr_m1, nh_m1;
 
-  __host__ void init(const float* m, const ct_cyl_grid& g) {
+  __host__ void init(const float* m, const float* gather, const ct_cyl_grid& g) {
     mu = m;
+    oct = reinterpret_cast<const float4*>(gather);
     nh = g.n_h; nt = g.n_theta; nr = g.n_r;
     radius = g.radius;
     half_h = 0.5 * g.height;
@@ -140,57 +200,70 @@ struct CylGeo {
     return true;
   }
 
-  template <bool NEAREST>
+  // trilinear cell (index of its (k0, j0, i0) corner) and weights of a point
+  __device__ __forceinline__ int locate(float x, float y, float z, float& wr, float& wt,
+                                        float& wh) const {
+    const float r = sqrt_approx(fmaf(x, x, y * y));
+    const float th = theta_2pi(y, x);
+    const float fr = fminf(fmaxf(fmaf(r, inv_dr, -0.5f), 0.0f), nr_m1);
+    const float fh = fminf(fmaxf(fmaf(z, inv_dh, h_off), 0.0f), nh_m1);
+    const float ft1 = fmaf(th, inv_dth, 0.5f);
+    int i0, k0, g;
+    wr = fr - floor_pos(fr, i0);
+    wh = fh - floor_pos(fh, k0);
+    wt = ft1 - floor_pos(ft1, g);
+    int j0 = g - 1;
+    j0 = (j0 < 0) ? nt - 1 : j0;
+    return (k0 * nt + j0) * nr + i0;
+  }
+
+  template <bool NEAREST, bool OCT>
   __device__ __forceinline__ float sample(float x, float y, float z) const {
-    float r = sqrtf(fmaf(x, x, y * y));
-    float ft = atan2f(y, x) * inv_dth - 0.5f;
-    if (ft < -0.5f) ft += (float)nt;  // theta += 2*pi (_kernels.py:287-289)
-    float fr = fminf(fmaxf(fmaf(r, inv_dr, -0.5f), 0.0f), nr_m1);
-    float fh = fminf(fmaxf(fmaf(z, inv_dh, h_off), 0.0f), nh_m1);
+    const float r = sqrt_approx(fmaf(x, x, y * y));
+    const float th = theta_2pi(y, x);
+    const float fr = fminf(fmaxf(fmaf(r, inv_dr, -0.5f), 0.0f), nr_m1);
+    const float fh = fminf(fmaxf(fmaf(z, inv_dh, h_off), 0.0f), nh_m1);
+    const float ft1 = fmaf(th, inv_dth, 0.5f);  // theta index + 1, in [0.5, nt + 0.5]
     if (NEAREST) {
-      int ir = (int)rintf(fr), ih = (int)rintf(fh), it = (int)rintf(ft);
+      int ir = (int)rintf(fr), ih = (int)rintf(fh), it = (int)rintf(ft1 - 1.0f);
       if (it < 0) it += nt;
       if (it >= nt) it -= nt;
-      return __ldg(mu + ((size_t)ih * nt + it) * nr + ir);
+      return __ldg(mu + (ih * nt + it) * nr + ir);
     }
-    int i0 = (int)fr;  // fr >= 0
-    float wr = fr - (float)i0;
-    int i1 = min(i0 + 1, nr - 1);
-    int k0 = (int)fh;
-    float wh = fh - (float)k0;
-    int k1 = min(k0 + 1, nh - 1);
-    float jf = floorf(ft);
-    float wt = ft - jf;
-    int j0 = (int)jf;
-    if (j0 < 0) j0 += nt;
-    if (j0 >= nt) j0 -= nt;
-    int j1 = (j0 + 1 == nt) ? 0 : j0 + 1;
-    const float* p00 = mu + ((size_t)k0 * nt + j0) * nr;
-    const float* p01 = mu + ((size_t)k0 * nt + j1) * nr;
-    const float* p10 = mu + ((size_t)k1 * nt + j0) * nr;
-    const float* p11 = mu + ((size_t)k1 * nt + j1) * nr;
-    float a0 = __ldg(p00 + i0), a1 = __ldg(p00 + i1);
-    float b0 = __ldg(p01 + i0), b1 = __ldg(p01 + i1);
-    float c0 = __ldg(p10 + i0), c1 = __ldg(p10 + i1);
-    float e0 = __ldg(p11 + i0), e1 = __ldg(p11 + i1);
-    float c00 = fmaf(a1 - a0, wr, a0);
-    float c01 = fmaf(b1 - b0, wr, b0);
-    float c10 = fmaf(c1 - c0, wr, c0);
-    float c11 = fmaf(e1 - e0, wr, e0);
-    float q0 = fmaf(c01 - c00, wt, c00);
-    float q1 = fmaf(c11 - c10, wt, c10);
-    return fmaf(q1 - q0, wh, q0);
+    int i0, k0, g;
+    const float wr = fr - floor_pos(fr, i0);
+    const float wh = fh - floor_pos(fh, k0);
+    const float wt = ft1 - floor_pos(ft1, g);
+    int j0 = g - 1;
+    j0 = (j0 < 0) ? nt - 1 : j0;
+    const int idx = (k0 * nt + j0) * nr + i0;
+    if (OCT) {
+      const float4 a = __ldg(oct + 2 * idx);
+      const float4 b = __ldg(oct + 2 * idx + 1);
+      return lerp8(a, b, wr, wt, wh);
+    }
+    const int di = (i0 + 1 < nr) ? 1 : 0;
+    const int dj = (j0 + 1 < nt) ? nr : -(nt - 1) * nr;
+    const int dk = (k0 + 1 < nh) ? nt * nr : 0;
+    const float* p = mu + idx;
+    float4 a, b;
+    a.x = __ldg(p); a.y = __ldg(p + di); a.z = __ldg(p + dj); a.w = __ldg(p + dj + di);
+    p += dk;
+    b.x = __ldg(p); b.y = __ldg(p + di); b.z = __ldg(p + dj); b.w = __ldg(p + dj + di);
+    return lerp8(a, b, wr, wt, wh);
   }
 };
 
 struct CartGeo {
   const float* __restrict__ mu;
+  const float4* __restrict__ oct;  // gather layout (ct_pack_gather_cart) or null
   int nz, ny, nx;
   double vs, lo[3], hi[3];
   float inv_vs, off[3], nx_m1, ny_m1, nz_m1;
 
-  __host__ void init(const float* m, const ct_cart_grid& g) {
+  __host__ void init(const float* m, const float* gather, const ct_cart_grid& g) {
     mu = m;
+    oct = reinterpret_cast<const float4*>(gather);
     nz = g.n_z; ny = g.n_y; nx = g.n_x;
     vs = g.voxel_size;
     for (int a = 0; a < 3; ++a) lo[a] = g.origin[a];
@@ -244,32 +317,44 @@ struct CartGeo {
              f[2] < -0.5 || f[2] > nz - 0.5);
   }
 
-  template <bool NEAREST>
+  __device__ __forceinline__ int locate(float x, float y, float z, float& wx, float& wy,
+                                        float& wz) const {
+    const float fx = fminf(fmaxf(fmaf(x, inv_vs, off[0]), 0.0f), nx_m1);
+    const float fy = fminf(fmaxf(fmaf(y, inv_vs, off[1]), 0.0f), ny_m1);
+    const float fz = fminf(fmaxf(fmaf(z, inv_vs, off[2]), 0.0f), nz_m1);
+    int i0, j0, k0;
+    wx = fx - floor_pos(fx, i0);
+    wy = fy - floor_pos(fy, j0);
+    wz = fz - floor_pos(fz, k0);
+    return (k0 * ny + j0) * nx + i0;
+  }
+
+  template <bool NEAREST, bool OCT>
   __device__ __forceinline__ float sample(float x, float y, float z) const {
-    float fx = fminf(fmaxf(fmaf(x, inv_vs, off[0]), 0.0f), nx_m1);
-    float fy = fminf(fmaxf(fmaf(y, inv_vs, off[1]), 0.0f), ny_m1);
-    float fz = fminf(fmaxf(fmaf(z, inv_vs, off[2]), 0.0f), nz_m1);
-    if (NEAREST) {
-      return __ldg(mu + ((size_t)(int)rintf(fz) * ny + (int)rintf(fy)) * nx + (int)rintf(fx));
+    const float fx = fminf(fmaxf(fmaf(x, inv_vs, off[0]), 0.0f), nx_m1);
+    const float fy = fminf(fmaxf(fmaf(y, inv_vs, off[1]), 0.0f), ny_m1);
+    const float fz = fminf(fmaxf(fmaf(z, inv_vs, off[2]), 0.0f), nz_m1);
+    if (NEAREST)
+      return __ldg(mu + ((int)rintf(fz) * ny + (int)rintf(fy)) * nx + (int)rintf(fx));
+    int i0, j0, k0;
+    const float wx = fx - floor_pos(fx, i0);
+    const float wy = fy - floor_pos(fy, j0);
+    const float wz = fz - floor_pos(fz, k0);
+    const int idx = (k0 * ny + j0) * nx + i0;
+    if (OCT) {
+      const float4 a = __ldg(oct + 2 * idx);
+      const float4 b = __ldg(oct + 2 * idx + 1);
+      return lerp8(a, b, wx, wy, wz);
     }
-    int i0 = (int)fx, j0 = (int)fy, k0 = (int)fz;
-    float wx = fx - (float)i0, wy = fy - (float)j0, wz = fz - (float)k0;
-    int i1 = min(i0 + 1, nx - 1), j1 = min(j0 + 1, ny - 1), k1 = min(k0 + 1, nz - 1);
-    const float* p00 = mu + ((size_t)k0 * ny + j0) * nx;
-    const float* p01 = mu + ((size_t)k0 * ny + j1) * nx;
-    const float* p10 = mu + ((size_t)k1 * ny + j0) * nx;
-    const float* p11 = mu + ((size_t)k1 * ny + j1) * nx;
-    float a0 = __ldg(p00 + i0), a1 = __ldg(p00 + i1);
-    float b0 = __ldg(p01 + i0), b1 = __ldg(p01 + i1);
-    float c0 = __ldg(p10 + i0), c1 = __ldg(p10 + i1);
-    float e0 = __ldg(p11 + i0), e1 = __ldg(p11 + i1);
-    float c00 = fmaf(a1 - a0, wx, a0);
-    float c01 = fmaf(b1 - b0, wx, b0);
-    float c10 = fmaf(c1 - c0, wx, c0);
-    float c11 = fmaf(e1 - e0, wx, e0);
-    float q0 = fmaf(c01 - c00, wy, c00);
-    float q1 = fmaf(c11 - c10, wy, c10);
-    return fmaf(q1 - q0, wz, q0);
+    const int di = (i0 + 1 < nx) ? 1 : 0;
+    const int dj = (j0 + 1 < ny) ? nx : 0;
+    const int dk = (k0 + 1 < nz) ? ny * nx : 0;
+    const float* p = mu + idx;
+    float4 a, b;
+    a.x = __ldg(p); a.y = __ldg(p + di); a.z = __ldg(p + dj); a.w = __ldg(p + dj + di);
+    p += dk;
+    b.x = __ldg(p); b.y = __ldg(p + di); b.z = __ldg(p + dj); b.w = __ldg(p + dj + di);
+    return lerp8(a, b, wx, wy, wz);
   }
 };
 
@@ -296,7 +381,7 @@ struct FpArgs {
 
 // One sub-ray: returns the in-support sample count; adds the fp32 sum of
 // interpolated values into acc (skipped for COUNT_ONLY).
-template <class Geo, bool NEAREST, bool COUNT_ONLY>
+template <class Geo, bool NEAREST, bool OCT, bool COUNT_ONLY>
 __device__ __forceinline__ int march(const Geo& geo, const ct_ray_view& v, double cu, double cv,
                                      double step, float& acc) {
   double d[3];
@@ -319,24 +404,77 @@ __device__ __forceinline__ int march(const Geo& geo, const ct_ray_view& v, doubl
   const int n_int = n - 1;
   float sum = 0.0f;
   int k = 0;
+  if (OCT && !NEAREST) {
+    // Consecutive samples are half a voxel apart: when a sample falls in the
+    // same trilinear cell as its predecessor the two 16-byte loads are skipped
+    // (predicated off) and the cell's values are forwarded in registers.
+    // Same values, same lerp, same summation grouping as the plain path.
+    int prev = -1;
+    float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pb = pa;
+    for (; k + 4 <= n_int; k += 4) {
+      const float k0 = (float)k;
+      int id[4];
+      float w0[4], w1[4], w2[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float kq = k0 + (float)q;
+        id[q] = geo.locate(fmaf(kq, ix, ex), fmaf(kq, iy, ey), fmaf(kq, iz, ez), w0[q], w1[q],
+                           w2[q]);
+      }
+      float4 A[4], B[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int pid = q ? id[q - 1] : prev;
+        A[q] = pa;
+        B[q] = pb;
+        if (id[q] != pid) {
+          A[q] = __ldg(geo.oct + 2 * id[q]);
+          B[q] = __ldg(geo.oct + 2 * id[q] + 1);
+        }
+      }
+#pragma unroll
+      for (int q = 1; q < 4; ++q) {
+        if (id[q] == id[q - 1]) { A[q] = A[q - 1]; B[q] = B[q - 1]; }
+      }
+      const float s0 = lerp8(A[0], B[0], w0[0], w1[0], w2[0]);
+      const float s1 = lerp8(A[1], B[1], w0[1], w1[1], w2[1]);
+      const float s2 = lerp8(A[2], B[2], w0[2], w1[2], w2[2]);
+      const float s3 = lerp8(A[3], B[3], w0[3], w1[3], w2[3]);
+      sum += (s0 + s1) + (s2 + s3);
+      prev = id[3];
+      pa = A[3];
+      pb = B[3];
+    }
+    for (; k < n_int; ++k) {
+      const float kf = (float)k;
+      float a0, a1, a2;
+      const int idx = geo.locate(fmaf(kf, ix, ex), fmaf(kf, iy, ey), fmaf(kf, iz, ez), a0, a1, a2);
+      if (idx != prev) {
+        pa = __ldg(geo.oct + 2 * idx);
+        pb = __ldg(geo.oct + 2 * idx + 1);
+        prev = idx;
+      }
+      sum += lerp8(pa, pb, a0, a1, a2);
+    }
+  }
   for (; k + 4 <= n_int; k += 4) {
     const float k0 = (float)k;
-    float s0 = geo.template sample<NEAREST>(fmaf(k0, ix, ex), fmaf(k0, iy, ey), fmaf(k0, iz, ez));
-    float s1 = geo.template sample<NEAREST>(fmaf(k0 + 1.f, ix, ex), fmaf(k0 + 1.f, iy, ey),
+    float s0 = geo.template sample<NEAREST, OCT>(fmaf(k0, ix, ex), fmaf(k0, iy, ey), fmaf(k0, iz, ez));
+    float s1 = geo.template sample<NEAREST, OCT>(fmaf(k0 + 1.f, ix, ex), fmaf(k0 + 1.f, iy, ey),
                                             fmaf(k0 + 1.f, iz, ez));
-    float s2 = geo.template sample<NEAREST>(fmaf(k0 + 2.f, ix, ex), fmaf(k0 + 2.f, iy, ey),
+    float s2 = geo.template sample<NEAREST, OCT>(fmaf(k0 + 2.f, ix, ex), fmaf(k0 + 2.f, iy, ey),
                                             fmaf(k0 + 2.f, iz, ez));
-    float s3 = geo.template sample<NEAREST>(fmaf(k0 + 3.f, ix, ex), fmaf(k0 + 3.f, iy, ey),
+    float s3 = geo.template sample<NEAREST, OCT>(fmaf(k0 + 3.f, ix, ex), fmaf(k0 + 3.f, iy, ey),
                                             fmaf(k0 + 3.f, iz, ez));
     sum += (s0 + s1) + (s2 + s3);
   }
   for (; k < n_int; ++k) {
     const float kf = (float)k;
-    sum += geo.template sample<NEAREST>(fmaf(kf, ix, ex), fmaf(kf, iy, ey), fmaf(kf, iz, ez));
+    sum += geo.template sample<NEAREST, OCT>(fmaf(kf, ix, ex), fmaf(kf, iy, ey), fmaf(kf, iz, ez));
   }
   if (last_in && geo.interp_nonzero(v.src, d, t_last)) {
     const float kf = (float)n_int;
-    sum += geo.template sample<NEAREST>(fmaf(kf, ix, ex), fmaf(kf, iy, ey), fmaf(kf, iz, ez));
+    sum += geo.template sample<NEAREST, OCT>(fmaf(kf, ix, ex), fmaf(kf, iy, ey), fmaf(kf, iz, ez));
   }
   acc += sum;
   return n_int + (last_in ? 1 : 0);
@@ -353,7 +491,7 @@ __device__ __forceinline__ double warp_max(double x) {
   return x;
 }
 
-template <class Geo, int EPI, bool NEAREST>
+template <class Geo, int EPI, bool NEAREST, bool OCT>
 __global__ void __launch_bounds__(FP_THREADS) fp_kernel(const FpArgs<Geo> a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // each warp covers an 8x4 pixel patch; the block a 16x8 tile
@@ -374,7 +512,7 @@ __global__ void __launch_bounds__(FP_THREADS) fp_kernel(const FpArgs<Geo> a) {
       const double off_v = dsub(ddiv((double)sv + 0.5, (double)ss), 0.5);
       for (int su = 0; su < ss; ++su) {
         const double off_u = dsub(ddiv((double)su + 0.5, (double)ss), 0.5);
-        count += march<Geo, NEAREST, EPI == EPI_ROWMAX>(
+        count += march<Geo, NEAREST, OCT, EPI == EPI_ROWMAX>(
             a.geo, v, dadd((double)col, off_u), dadd((double)row, off_v), a.step, acc);
       }
     }
@@ -491,9 +629,11 @@ int launch_fp(const Geo& geo, const ct_ray_view* views, const ct_batch& b, const
   a.out1 = o1;
   a.red = red;
   if (s.nearest)
-    fp_kernel<Geo, EPI, true><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
+    fp_kernel<Geo, EPI, true, false><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
+  else if (EPI != EPI_ROWMAX && geo.oct)
+    fp_kernel<Geo, EPI, false, true><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
   else
-    fp_kernel<Geo, EPI, false><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
+    fp_kernel<Geo, EPI, false, false><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
   return check_launch("fp_kernel");
 }
 
@@ -578,9 +718,10 @@ struct BpArgs {
 // fp64 re-evaluation of one voxel-view with the reference's arithmetic
 // (_kernels.py:407-417 + _bilinear_gather :350-377); only taken for
 // footprints within BP_EDGE_EPS of the frame edge or near the source plane.
-__device__ __noinline__ void bp_refine(const ct_det_view& dv, const double w[3],
+__device__ __noinline__ void bp_refine(const ct_det_view& dv, double w0, double w1, double w2,
                                        const float* __restrict__ img, int rows, int cols,
                                        float& num, float& den) {
+  const double w[3] = {w0, w1, w2};
   const double xi = dsub(dmul(dv.cphi, w[0]), dmul(dv.sphi, w[1]));
   const double yi = dadd(dmul(dv.sphi, w[0]), dmul(dv.cphi, w[1]));
   const double depth = dadd(dv.sod, yi);
@@ -616,7 +757,7 @@ __global__ void __launch_bounds__(BP_THREADS) bp_kernel(const BpArgs<Vox> a) {
   double w64[3] = {0.0, 0.0, 0.0};
   if (active) a.vox.world(m, w64);
   const float xw = (float)w64[0], yw = (float)w64[1], zw = (float)w64[2];
-  const float W = (float)a.cols, H = (float)a.rows;
+  const float W1 = (float)a.cols + 1.0f, H1 = (float)a.rows + 1.0f;
   const size_t npix = (size_t)a.rows * a.cols;
   float num = 0.0f, den = 0.0f;
 
@@ -630,44 +771,57 @@ __global__ void __launch_bounds__(BP_THREADS) bp_kernel(const BpArgs<Vox> a) {
       f.cphi = (float)d.cphi; f.sphi = (float)d.sphi; f.sod = (float)d.sod;
       f.sdd_p = (float)(d.sdd / d.pitch);
       f.u0 = (float)d.u0; f.v0 = (float)d.v0;
-      f.depth_floor = (float)(1e-6 * d.sod);
+      f.depth_floor = (float)(2e-6 * d.sod);  // refine band: 2x the reference floor
       f._pad = 0.0f;
       sv[threadIdx.x] = f;
     }
     __syncthreads();
     if (!active) continue;
+#pragma unroll 2
     for (int i = 0; i < nc; ++i) {
       const BpViewF f = sv[i];
       const float* img = a.corr + (size_t)(c0 + i) * npix;
       const float xi = fmaf(f.cphi, xw, -f.sphi * yw);
       const float yi = fmaf(f.sphi, xw, f.cphi * yw);
       const float depth = f.sod + yi;
-      const float scale = f.sdd_p / depth;
-      const float u = fmaf(xi, scale, f.u0);
-      const float v = fmaf(zw, scale, f.v0);
-      const bool edge = fabsf(u + 1.0f) < BP_EDGE_EPS || fabsf(u - W) < BP_EDGE_EPS ||
-                        fabsf(v + 1.0f) < BP_EDGE_EPS || fabsf(v - H) < BP_EDGE_EPS ||
-                        depth <= 2.0f * f.depth_floor;
-      if (edge) {
-        const int vid = a.view_ids ? a.view_ids[c0 + i] : c0 + i;
-        bp_refine(a.dets[vid], w64, img, a.rows, a.cols, num, den);
+      const float scale = f.sdd_p * rcp_nr(depth);
+      const float u1 = fmaf(xi, scale, f.u0) + 1.0f;   // u + 1
+      const float v1 = fmaf(zw, scale, f.v0) + 1.0f;   // v + 1
+      // signed distance (px) of the footprint to the boundary of the set
+      // where den > 0, i.e. (-1, W) x (-1, H); near it, redo in fp64.
+      const float edge_d = fminf(fminf(u1, W1 - u1), fminf(v1, H1 - v1));
+      if (edge_d < BP_EDGE_EPS || depth <= f.depth_floor) {
+        if (edge_d > -BP_EDGE_EPS || depth <= f.depth_floor) {
+          const int vid = a.view_ids ? a.view_ids[c0 + i] : c0 + i;
+          bp_refine(a.dets[vid], w64[0], w64[1], w64[2], img, a.rows, a.cols, num, den);
+        }
         continue;
       }
-      if (!(u > -1.0f && u < W && v > -1.0f && v < H)) continue;
-      const float fiu = floorf(u), fiv = floorf(v);
-      const int iu = (int)fiu, iv = (int)fiv;
-      const float fu = u - fiu, fv = v - fiv;
-      const bool cu0 = iu >= 0, cu1 = iu + 1 < a.cols;
-      const bool rv0 = iv >= 0, rv1 = iv + 1 < a.rows;
-      const float* r0 = img + (size_t)iv * a.cols + iu;
-      const float* r1 = r0 + a.cols;
-      const float t00 = (rv0 && cu0) ? __ldg(r0) : 0.0f;
-      const float t01 = (rv0 && cu1) ? __ldg(r0 + 1) : 0.0f;
-      const float t10 = (rv1 && cu0) ? __ldg(r1) : 0.0f;
-      const float t11 = (rv1 && cu1) ? __ldg(r1 + 1) : 0.0f;
+      int iu, iv;                                       // floor(u), floor(v) >= -1
+      const float fu = u1 - floor_pos(u1, iu);
+      const float fv = v1 - floor_pos(v1, iv);
+      iu -= 1;
+      iv -= 1;
       const float wu0 = 1.0f - fu, wv0 = 1.0f - fv;
-      num += wv0 * (wu0 * t00 + fu * t01) + fv * (wu0 * t10 + fu * t11);
-      den += ((cu0 ? wu0 : 0.0f) + (cu1 ? fu : 0.0f)) * ((rv0 ? wv0 : 0.0f) + (rv1 ? fv : 0.0f));
+      if (iu >= 0 && iu + 1 < a.cols && iv >= 0 && iv + 1 < a.rows) {
+        // whole footprint on the detector: the four weights sum to 1
+        const float* r0 = img + (iv * a.cols + iu);
+        const float t00 = __ldg(r0), t01 = __ldg(r0 + 1);
+        const float t10 = __ldg(r0 + a.cols), t11 = __ldg(r0 + a.cols + 1);
+        num += wv0 * fmaf(wu0, t00, fu * t01) + fv * fmaf(wu0, t10, fu * t11);
+        den += 1.0f;
+      } else {
+        // frame edge: only in-bounds taps count (_kernels.py:365-376)
+        const bool cu0 = iu >= 0, cu1 = iu + 1 < a.cols;
+        const bool rv0 = iv >= 0, rv1 = iv + 1 < a.rows;
+        const float* r0 = img + (iv * a.cols + iu);
+        const float t00 = (rv0 && cu0) ? __ldg(r0) : 0.0f;
+        const float t01 = (rv0 && cu1) ? __ldg(r0 + 1) : 0.0f;
+        const float t10 = (rv1 && cu0) ? __ldg(r0 + a.cols) : 0.0f;
+        const float t11 = (rv1 && cu1) ? __ldg(r0 + a.cols + 1) : 0.0f;
+        num += wv0 * fmaf(wu0, t00, fu * t01) + fv * fmaf(wu0, t10, fu * t11);
+        den += ((cu0 ? wu0 : 0.0f) + (cu1 ? fu : 0.0f)) * ((rv0 ? wv0 : 0.0f) + (rv1 ? fv : 0.0f));
+      }
     }
   }
   if (!active) return;
@@ -848,6 +1002,36 @@ __global__ void resample_cyl_kernel(const float* __restrict__ src_mu, ct_cyl_gri
                         nearest != 0);
 }
 
+
+// ---------------------------------------------------------------------------
+// gather layout: voxel index m holds its 2x2x2 trilinear neighbourhood
+// (r/h or x/y/z clamp, theta wrap) as two float4 = one 32-byte sector, so one
+// FP sample is 2 x LDG.128 from a single sector instead of 8 scattered loads.
+// ---------------------------------------------------------------------------
+__global__ void pack_gather_cyl_kernel(const float* __restrict__ mu, int nh, int nt, int nr,
+                                       float4* __restrict__ oct) {
+  const int64_t n = (int64_t)nh * nt * nr;
+  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n) return;
+  const int i = (int)(m % nr), j = (int)((m / nr) % nt), k = (int)(m / ((int64_t)nr * nt));
+  const int i1 = min(i + 1, nr - 1), j1 = (j + 1 == nt) ? 0 : j + 1, k1 = min(k + 1, nh - 1);
+  auto M = [&](int kk, int jj, int ii) { return __ldg(mu + ((int64_t)kk * nt + jj) * nr + ii); };
+  oct[2 * m] = make_float4(M(k, j, i), M(k, j, i1), M(k, j1, i), M(k, j1, i1));
+  oct[2 * m + 1] = make_float4(M(k1, j, i), M(k1, j, i1), M(k1, j1, i), M(k1, j1, i1));
+}
+
+__global__ void pack_gather_cart_kernel(const float* __restrict__ mu, int nz, int ny, int nx,
+                                        float4* __restrict__ oct) {
+  const int64_t n = (int64_t)nz * ny * nx;
+  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n) return;
+  const int i = (int)(m % nx), j = (int)((m / nx) % ny), k = (int)(m / ((int64_t)nx * ny));
+  const int i1 = min(i + 1, nx - 1), j1 = min(j + 1, ny - 1), k1 = min(k + 1, nz - 1);
+  auto M = [&](int kk, int jj, int ii) { return __ldg(mu + ((int64_t)kk * ny + jj) * nx + ii); };
+  oct[2 * m] = make_float4(M(k, j, i), M(k, j, i1), M(k, j1, i), M(k, j1, i1));
+  oct[2 * m + 1] = make_float4(M(k1, j, i), M(k1, j, i1), M(k1, j1, i), M(k1, j1, i1));
+}
+
 unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
@@ -863,50 +1047,50 @@ const char* ct_arch(void) { return "sm_100a"; }
 
 #define CT_STREAM(s) (static_cast<cudaStream_t>(s))
 
-int ct_fp_cyl(const float* mu, const ct_cyl_grid* grid, const ct_ray_view* views,
+int ct_fp_cyl(const float* mu, const float* gather, const ct_cyl_grid* grid, const ct_ray_view* views,
               const ct_batch* batch, const ct_sampling* s, float* out_p, float* out_w,
               ct_stream_t stream) {
   int rc = check_batch(batch, views, s);
   if (rc || (rc = check_cyl(grid))) return rc;
   if (!mu || !out_p) return set_err(CT_ERR_ARG, "null mu/out_p");
   CylGeo geo;
-  geo.init(mu, *grid);
+  geo.init(mu, gather, *grid);
   return launch_fp<CylGeo, EPI_PROJECT>(geo, views, *batch, *s, nullptr, nullptr, out_p, out_w,
                                         nullptr, CT_STREAM(stream));
 }
 
-int ct_fp_cart(const float* mu, const ct_cart_grid* grid, const ct_ray_view* views,
+int ct_fp_cart(const float* mu, const float* gather, const ct_cart_grid* grid, const ct_ray_view* views,
                const ct_batch* batch, const ct_sampling* s, float* out_p, float* out_w,
                ct_stream_t stream) {
   int rc = check_batch(batch, views, s);
   if (rc || (rc = check_cart(grid))) return rc;
   if (!mu || !out_p) return set_err(CT_ERR_ARG, "null mu/out_p");
   CartGeo geo;
-  geo.init(mu, *grid);
+  geo.init(mu, gather, *grid);
   return launch_fp<CartGeo, EPI_PROJECT>(geo, views, *batch, *s, nullptr, nullptr, out_p, out_w,
                                          nullptr, CT_STREAM(stream));
 }
 
-int ct_fp_cyl_correction(const float* mu, const ct_cyl_grid* grid, const ct_ray_view* views,
+int ct_fp_cyl_correction(const float* mu, const float* gather, const ct_cyl_grid* grid, const ct_ray_view* views,
                          const ct_batch* batch, const ct_sampling* s, const float* p_meas,
                          const double* row_thr, float* corr, ct_stream_t stream) {
   int rc = check_batch(batch, views, s);
   if (rc || (rc = check_cyl(grid))) return rc;
   if (!mu || !p_meas || !row_thr || !corr) return set_err(CT_ERR_ARG, "null pointer");
   CylGeo geo;
-  geo.init(mu, *grid);
+  geo.init(mu, gather, *grid);
   return launch_fp<CylGeo, EPI_CORR>(geo, views, *batch, *s, p_meas, row_thr, corr, nullptr,
                                      nullptr, CT_STREAM(stream));
 }
 
-int ct_fp_cart_correction(const float* mu, const ct_cart_grid* grid, const ct_ray_view* views,
+int ct_fp_cart_correction(const float* mu, const float* gather, const ct_cart_grid* grid, const ct_ray_view* views,
                           const ct_batch* batch, const ct_sampling* s, const float* p_meas,
                           const double* row_thr, float* corr, ct_stream_t stream) {
   int rc = check_batch(batch, views, s);
   if (rc || (rc = check_cart(grid))) return rc;
   if (!mu || !p_meas || !row_thr || !corr) return set_err(CT_ERR_ARG, "null pointer");
   CartGeo geo;
-  geo.init(mu, *grid);
+  geo.init(mu, gather, *grid);
   return launch_fp<CartGeo, EPI_CORR>(geo, views, *batch, *s, p_meas, row_thr, corr, nullptr,
                                       nullptr, CT_STREAM(stream));
 }
@@ -923,27 +1107,27 @@ static int finish_residual(const ct_batch* batch, double* scratch, double* accum
   return check_launch("sum_partials_kernel");
 }
 
-int ct_fp_cyl_residual(const float* mu, const ct_cyl_grid* grid, const ct_ray_view* views,
+int ct_fp_cyl_residual(const float* mu, const float* gather, const ct_cyl_grid* grid, const ct_ray_view* views,
                        const ct_batch* batch, const ct_sampling* s, const float* p_meas,
                        double* scratch, double* accum, ct_stream_t stream) {
   int rc = check_batch(batch, views, s);
   if (rc || (rc = check_cyl(grid))) return rc;
   if (!mu || !p_meas || !scratch || !accum) return set_err(CT_ERR_ARG, "null pointer");
   CylGeo geo;
-  geo.init(mu, *grid);
+  geo.init(mu, gather, *grid);
   rc = launch_fp<CylGeo, EPI_RESID>(geo, views, *batch, *s, p_meas, nullptr, nullptr, nullptr,
                                     scratch, CT_STREAM(stream));
   return rc ? rc : finish_residual(batch, scratch, accum, CT_STREAM(stream));
 }
 
-int ct_fp_cart_residual(const float* mu, const ct_cart_grid* grid, const ct_ray_view* views,
+int ct_fp_cart_residual(const float* mu, const float* gather, const ct_cart_grid* grid, const ct_ray_view* views,
                         const ct_batch* batch, const ct_sampling* s, const float* p_meas,
                         double* scratch, double* accum, ct_stream_t stream) {
   int rc = check_batch(batch, views, s);
   if (rc || (rc = check_cart(grid))) return rc;
   if (!mu || !p_meas || !scratch || !accum) return set_err(CT_ERR_ARG, "null pointer");
   CartGeo geo;
-  geo.init(mu, *grid);
+  geo.init(mu, gather, *grid);
   rc = launch_fp<CartGeo, EPI_RESID>(geo, views, *batch, *s, p_meas, nullptr, nullptr, nullptr,
                                      scratch, CT_STREAM(stream));
   return rc ? rc : finish_residual(batch, scratch, accum, CT_STREAM(stream));
@@ -957,7 +1141,7 @@ int ct_rowsum_max_cyl(const ct_cyl_grid* grid, const ct_ray_view* views, const c
   if (cudaMemsetAsync(max_row, 0, sizeof(double) * batch->n_batch, CT_STREAM(stream)))
     return check_launch("memset");
   CylGeo geo;
-  geo.init(nullptr, *grid);
+  geo.init(nullptr, nullptr, *grid);
   return launch_fp<CylGeo, EPI_ROWMAX>(geo, views, *batch, *s, nullptr, nullptr, nullptr,
                                        nullptr, max_row, CT_STREAM(stream));
 }
@@ -971,7 +1155,7 @@ int ct_rowsum_max_cart(const ct_cart_grid* grid, const ct_ray_view* views,
   if (cudaMemsetAsync(max_row, 0, sizeof(double) * batch->n_batch, CT_STREAM(stream)))
     return check_launch("memset");
   CartGeo geo;
-  geo.init(nullptr, *grid);
+  geo.init(nullptr, nullptr, *grid);
   return launch_fp<CartGeo, EPI_ROWMAX>(geo, views, *batch, *s, nullptr, nullptr, nullptr,
                                         nullptr, max_row, CT_STREAM(stream));
 }
@@ -1081,6 +1265,32 @@ int ct_resample_cyl_to_cyl(const float* src_mu, const ct_cyl_grid* src, const ct
   resample_cyl_kernel<<<blocks_for(n, 256), 256, 0, CT_STREAM(stream)>>>(src_mu, *src, *dst,
                                                                          nearest, dst_mu);
   return check_launch("resample_cyl_kernel");
+}
+
+int64_t ct_gather_floats(int64_t n_voxels) { return n_voxels < 0 ? 0 : 8 * n_voxels; }
+
+int ct_pack_gather_cyl(const float* mu, const ct_cyl_grid* grid, float* gather,
+                       ct_stream_t stream) {
+  int rc = check_cyl(grid);
+  if (rc) return rc;
+  if (!mu || !gather) return set_err(CT_ERR_ARG, "null mu/gather");
+  if (reinterpret_cast<uintptr_t>(gather) % 16) return set_err(CT_ERR_ARG, "gather not 16B-aligned");
+  const int64_t n = (int64_t)grid->n_h * grid->n_theta * grid->n_r;
+  pack_gather_cyl_kernel<<<blocks_for(n, 256), 256, 0, CT_STREAM(stream)>>>(
+      mu, grid->n_h, grid->n_theta, grid->n_r, reinterpret_cast<float4*>(gather));
+  return check_launch("pack_gather_cyl_kernel");
+}
+
+int ct_pack_gather_cart(const float* mu, const ct_cart_grid* grid, float* gather,
+                        ct_stream_t stream) {
+  int rc = check_cart(grid);
+  if (rc) return rc;
+  if (!mu || !gather) return set_err(CT_ERR_ARG, "null mu/gather");
+  if (reinterpret_cast<uintptr_t>(gather) % 16) return set_err(CT_ERR_ARG, "gather not 16B-aligned");
+  const int64_t n = (int64_t)grid->n_z * grid->n_y * grid->n_x;
+  pack_gather_cart_kernel<<<blocks_for(n, 256), 256, 0, CT_STREAM(stream)>>>(
+      mu, grid->n_z, grid->n_y, grid->n_x, reinterpret_cast<float4*>(gather));
+  return check_launch("pack_gather_cart_kernel");
 }
 
 }  // extern "C"

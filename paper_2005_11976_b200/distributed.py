@@ -104,6 +104,7 @@ class GpuEngine:
         self.p_meas = D.to_device(ps.images, device=self.device)
         self.weights = _device_weights(cfg, grid.shape, self.device)
         self.cfg = cfg
+        self.gather = None
 
     def tensor(self, shape, dtype="float32"):
         torch = self.D.torch_mod()
@@ -116,7 +117,10 @@ class GpuEngine:
         return self.D.upload_i32(views)
 
     def correction(self, mu, slots, n, corr):
-        self.eng.correction(mu, self.p_meas, slots, n, corr)
+        if self.gather is None:
+            self.gather = self.eng.alloc_gather()
+        self.eng.pack(mu, self.gather)
+        self.eng.correction(mu, self.p_meas, slots, n, corr, self.gather)
 
     def bp_partial(self, corr, slots, n, num, den):
         self.eng.bp_partial(corr, slots, n, num, den)
@@ -129,7 +133,10 @@ class GpuEngine:
                C.byref(upd), self.D.stream_handle())
 
     def residual(self, mu, slots, n, accum):
-        self.eng.residual(mu, self.p_meas, slots, n, accum)
+        if self.gather is None:
+            self.gather = self.eng.alloc_gather()
+        self.eng.pack(mu, self.gather)
+        self.eng.residual(mu, self.p_meas, slots, n, accum, self.gather)
 
     def synchronize(self):
         self.D.torch_mod().cuda.synchronize(self.device)

@@ -27,6 +27,7 @@ from .grid import CartGrid, CartVolume, CylGrid, CylVolume, is_device_array
 
 LINE_INTEGRAL = "line_integral"
 INTENSITY = "intensity"
+GATHER_MIN_VIEWS = 4   # batched FP builds the gather layout (identical results)
 
 
 @dataclass
@@ -108,10 +109,16 @@ def _project(vol, geom: ScanGeometry, views, cfg: RaySamplingConfig, want_w: boo
     table = D.upload_f64(D.ray_view_table(vol.grid, geom, views))
     s = D.sampling_c(cfg.step_for(vol), cfg.supersample, cfg.interpolation == "nearest")
     b = D.batch_c(nv, H, W)
-    fn = "ct_fp_cyl" if isinstance(vol, CylVolume) else "ct_fp_cart"
+    cyl = isinstance(vol, CylVolume)
     g = D.grid_c(vol.grid)
-    N.call(fn, D.ptr(mu), C.byref(g), D.ptr(table), C.byref(b), C.byref(s), D.ptr(out_p),
-           D.ptr(out_w), D.stream_handle())
+    gather = None
+    if nv >= GATHER_MIN_VIEWS and cfg.interpolation == "linear":
+        # multi-view launches amortise building the sector-per-sample layout
+        gather = torch.empty(vol.grid.n_voxels * 8, dtype=torch.float32, device=dev)
+        N.call("ct_pack_gather_cyl" if cyl else "ct_pack_gather_cart", D.ptr(mu), C.byref(g),
+               D.ptr(gather), D.stream_handle())
+    N.call("ct_fp_cyl" if cyl else "ct_fp_cart", D.ptr(mu), D.ptr(gather), C.byref(g),
+           D.ptr(table), C.byref(b), C.byref(s), D.ptr(out_p), D.ptr(out_w), D.stream_handle())
     return out_p, out_w
 
 

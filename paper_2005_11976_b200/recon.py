@@ -159,11 +159,25 @@ class SartEngine:
         return max_row
 
     # -- launchers -------------------------------------------------------------
-    def correction(self, mu, p_meas, slots, n: int, corr) -> None:
+    def alloc_gather(self):
+        """Buffer for the FP gather layout (8 floats per voxel, 16B aligned)."""
+        torch = D.torch_mod()
+        if self.samp.nearest:
+            return None
+        n = int(N.load_library().ct_gather_floats(int(np.prod(self.grid.shape))))
+        return torch.empty(n, dtype=torch.float32, device=self.device)
+
+    def pack(self, mu, gather) -> None:
+        if gather is None:
+            return
+        fn = "ct_pack_gather_cyl" if self.cyl else "ct_pack_gather_cart"
+        N.call(fn, D.ptr(mu), C.byref(self.gc), D.ptr(gather), D.stream_handle())
+
+    def correction(self, mu, p_meas, slots, n: int, corr, gather=None) -> None:
         b = D.batch_c(n, self.rows, self.cols, slots)
         fn = "ct_fp_cyl_correction" if self.cyl else "ct_fp_cart_correction"
-        N.call(fn, D.ptr(mu), C.byref(self.gc), D.ptr(self.fp_views), C.byref(b),
-               C.byref(self.samp), D.ptr(p_meas), D.ptr(self.row_thr), D.ptr(corr),
+        N.call(fn, D.ptr(mu), D.ptr(gather), C.byref(self.gc), D.ptr(self.fp_views),
+               C.byref(b), C.byref(self.samp), D.ptr(p_meas), D.ptr(self.row_thr), D.ptr(corr),
                D.stream_handle())
 
     def bp_update(self, corr, slots, n: int, upd: N.UpdateC) -> None:
@@ -185,18 +199,22 @@ class SartEngine:
             N.call("ct_bp_cart", D.ptr(corr), D.ptr(self.bp_dets), C.byref(b),
                    C.byref(self.gc), D.ptr(num), D.ptr(den), 0, D.stream_handle())
 
-    def residual(self, mu, p_meas, slots, n: int, accum) -> None:
-        """accum (device f64 scalar view) += sum (p - A mu)^2 over the batch."""
+    def residual_scratch(self, n: int):
         torch = D.torch_mod()
-        b = D.batch_c(n, self.rows, self.cols, slots)
+        b = D.batch_c(n, self.rows, self.cols)
         length = int(N.load_library().ct_residual_scratch_len(C.byref(b)))
-        key = (n, length)
-        if key not in self._scratch:
-            self._scratch[key] = torch.empty(length, dtype=torch.float64, device=self.device)
+        if n not in self._scratch:
+            self._scratch[n] = torch.empty(length, dtype=torch.float64, device=self.device)
+        return self._scratch[n]
+
+    def residual(self, mu, p_meas, slots, n: int, accum, gather=None) -> None:
+        """accum (device f64 scalar view) += sum (p - A mu)^2 over the batch."""
+        b = D.batch_c(n, self.rows, self.cols, slots)
+        scratch = self.residual_scratch(n)
         fn = "ct_fp_cyl_residual" if self.cyl else "ct_fp_cart_residual"
-        N.call(fn, D.ptr(mu), C.byref(self.gc), D.ptr(self.fp_views), C.byref(b),
-               C.byref(self.samp), D.ptr(p_meas), D.ptr(self._scratch[key]), D.ptr(accum),
-               D.stream_handle())
+        N.call(fn, D.ptr(mu), D.ptr(gather), C.byref(self.gc), D.ptr(self.fp_views),
+               C.byref(b), C.byref(self.samp), D.ptr(p_meas), D.ptr(scratch),
+               D.ptr(accum), D.stream_handle())
 
 
 def make_update(mu, weights, cfg: SartConfig) -> N.UpdateC:
@@ -278,7 +296,9 @@ class SartRun:
     driver use the object directly to time passes and reuse buffers.
     """
 
-    def __init__(self, ps: ProjectionSet, grid, cfg: SartConfig):
+    GRAPH_MIN_SUBSETS = 16   # per-view SART (many small launches) replays a CUDA graph
+
+    def __init__(self, ps: ProjectionSet, grid, cfg: SartConfig, use_graph: bool | None = None):
         if ps.kind != LINE_INTEGRAL:
             raise ConfigError("SART needs line-integral projections")
         torch = D.torch_mod()
@@ -297,20 +317,62 @@ class SartRun:
         self.corr = torch.empty((nmax, self.eng.rows, self.eng.cols), dtype=torch.float32,
                                 device=dev)
         self.upd = make_update(self.mu, self.weights, cfg)
+        self.gather = self.eng.alloc_gather()
         self.resid = torch.zeros(cfg.n_iterations, dtype=torch.float64, device=dev)
+        self.resid_cur = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.eng.residual_scratch(ps.geom.n_proj)      # no allocation inside a pass
         self.passes_done = 0
+        self.launch_log = None   # list -> (kind, subset, start_event, end_event) per launch
+        self.use_graph = (len(self.subsets) >= self.GRAPH_MIN_SUBSETS
+                          if use_graph is None else bool(use_graph))
+        self._graphs = {}
+
+    def _timed(self, kind, s, fn, *args):
+        if self.launch_log is None:
+            fn(*args)
+            return
+        torch = D.torch_mod()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn(*args)
+        b.record()
+        self.launch_log.append((kind, s, a, b))
+
+    def _pass_body(self, residual: bool) -> None:
+        e = self.eng
+        for k, (s, slots) in enumerate(zip(self.subsets, self.subset_slots)):
+            self._timed("pack_gather", k, e.pack, self.mu, self.gather)
+            self._timed("fp_correction", k, e.correction, self.mu, self.p_meas, slots, len(s),
+                        self.corr, self.gather)
+            self._timed("bp_update", k, e.bp_update, self.corr, slots, len(s), self.upd)
+        if residual:
+            self.resid_cur.zero_()
+            self._timed("pack_gather", -1, e.pack, self.mu, self.gather)
+            self._timed("fp_residual", -1, e.residual, self.mu, self.p_meas, self.all_slots,
+                        self.ps.geom.n_proj, self.resid_cur, self.gather)
 
     def run_pass(self, residual: bool | None = None) -> None:
-        """One pass over all subsets (+ the residual FP if enabled)."""
-        e = self.eng
-        for s, slots in zip(self.subsets, self.subset_slots):
-            e.correction(self.mu, self.p_meas, slots, len(s), self.corr)
-            e.bp_update(self.corr, slots, len(s), self.upd)
+        """One pass over all subsets (+ the residual FP if enabled).
+
+        With use_graph the whole pass is captured once as a CUDA graph and
+        replayed (same kernels, same bits) -- per-view SART issues 3 launches
+        per view, which would otherwise be launch-bound."""
         want = self.cfg.compute_residuals if residual is None else residual
+        if self.use_graph and self.launch_log is None:
+            torch = D.torch_mod()
+            g = self._graphs.get(want)
+            if g is None:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._pass_body(want)
+                self._graphs[want] = g
+            g.replay()
+        else:
+            self._pass_body(want)
         if want:
             k = min(self.passes_done, self.resid.numel() - 1)
-            e.residual(self.mu, self.p_meas, self.all_slots, self.ps.geom.n_proj,
-                       self.resid[k:k + 1])
+            self.resid[k:k + 1].copy_(self.resid_cur)
         self.passes_done += 1
 
     def run(self):
