@@ -102,8 +102,9 @@ __device__ __forceinline__ float sqrt_approx(float x) {
 __device__ __forceinline__ float theta_2pi(float y, float x) {
   const float ax = fabsf(x), ay = fabsf(y);
   const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
-  float a = __fdividef(mn, mx);
-  a = (mx > 0.0f) ? a : 0.0f;
+  float rc;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(fmaxf(mx, 1e-30f)));
+  const float a = mn * rc;   // in [0, 1]; 0 on the axis (atan2(0, 0) = 0)
   const float s = a * a;
   float p = -0.004056010747295693f;
   p = fmaf(p, s, 0.021868032862667357f);
@@ -411,51 +412,29 @@ __device__ __forceinline__ int march(const Geo& geo, const ct_ray_view& v, doubl
     // Same values, same lerp, same summation grouping as the plain path.
     int prev = -1;
     float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pb = pa;
-    for (; k + 4 <= n_int; k += 4) {
-      const float k0 = (float)k;
-      int id[4];
-      float w0[4], w1[4], w2[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float kq = k0 + (float)q;
-        id[q] = geo.locate(fmaf(kq, ix, ex), fmaf(kq, iy, ey), fmaf(kq, iz, ez), w0[q], w1[q],
-                           w2[q]);
-      }
-      float4 A[4], B[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int pid = q ? id[q - 1] : prev;
-        A[q] = pa;
-        B[q] = pb;
-        if (id[q] != pid) {
-          A[q] = __ldg(geo.oct + 2 * id[q]);
-          B[q] = __ldg(geo.oct + 2 * id[q] + 1);
-        }
-      }
-#pragma unroll
-      for (int q = 1; q < 4; ++q) {
-        if (id[q] == id[q - 1]) { A[q] = A[q - 1]; B[q] = B[q - 1]; }
-      }
-      const float s0 = lerp8(A[0], B[0], w0[0], w1[0], w2[0]);
-      const float s1 = lerp8(A[1], B[1], w0[1], w1[1], w2[1]);
-      const float s2 = lerp8(A[2], B[2], w0[2], w1[2], w2[2]);
-      const float s3 = lerp8(A[3], B[3], w0[3], w1[3], w2[3]);
-      sum += (s0 + s1) + (s2 + s3);
-      prev = id[3];
-      pa = A[3];
-      pb = B[3];
-    }
-    for (; k < n_int; ++k) {
-      const float kf = (float)k;
-      float a0, a1, a2;
-      const int idx = geo.locate(fmaf(kf, ix, ex), fmaf(kf, iy, ey), fmaf(kf, iz, ez), a0, a1, a2);
+    // one live cell (pa, pb): the loads are predicated on a cell change and
+    // land in the same registers -- no forwarding copies; resident warps hide
+    // the resulting load->lerp serialisation.
+    auto cell_sample = [&](float kq) -> float {
+      float w0, w1, w2;
+      const int idx = geo.locate(fmaf(kq, ix, ex), fmaf(kq, iy, ey), fmaf(kq, iz, ez), w0, w1, w2);
       if (idx != prev) {
         pa = __ldg(geo.oct + 2 * idx);
         pb = __ldg(geo.oct + 2 * idx + 1);
         prev = idx;
       }
-      sum += lerp8(pa, pb, a0, a1, a2);
+      return lerp8(pa, pb, w0, w1, w2);
+    };
+#pragma unroll 1
+    for (; k + 4 <= n_int; k += 4) {
+      const float k0 = (float)k;
+      const float s0 = cell_sample(k0);
+      const float s1 = cell_sample(k0 + 1.0f);
+      const float s2 = cell_sample(k0 + 2.0f);
+      const float s3 = cell_sample(k0 + 3.0f);
+      sum += (s0 + s1) + (s2 + s3);
     }
+    for (; k < n_int; ++k) sum += cell_sample((float)k);
   }
   for (; k + 4 <= n_int; k += 4) {
     const float k0 = (float)k;
@@ -540,7 +519,9 @@ __global__ void __launch_bounds__(FP_THREADS) fp_kernel(const FpArgs<Geo> a) {
     double x = 0.0;
     if (active) {
       if (EPI == EPI_RESID) {
-        const double r = (double)a.p_meas[(size_t)vid * npix + pix] - p64;
+        // compare with the fp32 simulation, i.e. what a stored projection of
+        // this volume holds: consistent data gives exactly 0, as in the reference
+        const double r = (double)a.p_meas[(size_t)vid * npix + pix] - (double)(float)p64;
         x = r * r;
       } else {
         x = w64;
@@ -718,20 +699,24 @@ struct BpArgs {
 // fp64 re-evaluation of one voxel-view with the reference's arithmetic
 // (_kernels.py:407-417 + _bilinear_gather :350-377); only taken for
 // footprints within BP_EDGE_EPS of the frame edge or near the source plane.
-__device__ __noinline__ void bp_refine(const ct_det_view& dv, double w0, double w1, double w2,
-                                       const float* __restrict__ img, int rows, int cols,
-                                       float& num, float& den) {
-  const double w[3] = {w0, w1, w2};
-  const double xi = dsub(dmul(dv.cphi, w[0]), dmul(dv.sphi, w[1]));
-  const double yi = dadd(dmul(dv.sphi, w[0]), dmul(dv.cphi, w[1]));
+template <class Vox>
+__device__ __noinline__ float2 bp_refine(const Vox& vox, int m, const ct_det_view& dv,
+                                         const float* __restrict__ img, int rows, int cols) {
+  float2 acc = make_float2(0.0f, 0.0f);   // (num, den) -- returned by value so the
+                                          // caller's accumulators stay in registers
+  double w[3];
+  vox.world(m, w);                        // fp64 voxel centre, reference op order
+  const double w0 = w[0], w1 = w[1], w2 = w[2];
+  const double xi = dsub(dmul(dv.cphi, w0), dmul(dv.sphi, w1));
+  const double yi = dadd(dmul(dv.sphi, w0), dmul(dv.cphi, w1));
   const double depth = dadd(dv.sod, yi);
-  if (depth <= dmul(1e-6, dv.sod)) return;
+  if (depth <= dmul(1e-6, dv.sod)) return acc;
   const double scale = ddiv(dv.sdd, dmul(depth, dv.pitch));
   const double u = dadd(dv.u0, dmul(xi, scale));
-  const double v = dadd(dv.v0, dmul(w[2], scale));
+  const double v = dadd(dv.v0, dmul(w2, scale));
   const double fiu = floor(u), fiv = floor(v);
   const double fu = dsub(u, fiu), fv = dsub(v, fiv);
-  if (!(fiu >= -2.0 && fiu <= (double)cols) || !(fiv >= -2.0 && fiv <= (double)rows)) return;
+  if (!(fiu >= -2.0 && fiu <= (double)cols) || !(fiv >= -2.0 && fiv <= (double)rows)) return acc;
   const int iu = (int)fiu, iv = (int)fiv;
   for (int dvv = 0; dvv < 2; ++dvv) {
     const int rr = iv + dvv;
@@ -742,21 +727,27 @@ __device__ __noinline__ void bp_refine(const ct_det_view& dv, double w0, double 
       if (cc < 0 || cc >= cols) continue;
       const double wu = duu == 1 ? fu : dsub(1.0, fu);
       const double wt = dmul(wu, wv);
-      num += (float)wt * img[(size_t)rr * cols + cc];
-      den += (float)wt;
+      acc.x += (float)wt * img[(size_t)rr * cols + cc];
+      acc.y += (float)wt;
     }
   }
+  return acc;
 }
 
 template <class Vox, int MODE>
-__global__ void __launch_bounds__(BP_THREADS) bp_kernel(const BpArgs<Vox> a) {
+__global__ void __launch_bounds__(BP_THREADS) bp_kernel(const __grid_constant__ BpArgs<Vox> a) {
   __shared__ BpViewF sv[BP_CHUNK];
   const int64_t nvox = a.vox.count();
   const int m = blockIdx.x * BP_THREADS + threadIdx.x;
   const bool active = m < nvox;
-  double w64[3] = {0.0, 0.0, 0.0};
-  if (active) a.vox.world(m, w64);
-  const float xw = (float)w64[0], yw = (float)w64[1], zw = (float)w64[2];
+  float xw = 0.0f, yw = 0.0f, zw = 0.0f;
+  if (active) {
+    double w64[3];
+    a.vox.world(m, w64);
+    xw = (float)w64[0];
+    yw = (float)w64[1];
+    zw = (float)w64[2];
+  }
   const float W1 = (float)a.cols + 1.0f, H1 = (float)a.rows + 1.0f;
   const size_t npix = (size_t)a.rows * a.cols;
   float num = 0.0f, den = 0.0f;
@@ -777,10 +768,10 @@ __global__ void __launch_bounds__(BP_THREADS) bp_kernel(const BpArgs<Vox> a) {
     }
     __syncthreads();
     if (!active) continue;
+    const float* __restrict__ img = a.corr + (size_t)c0 * npix;
 #pragma unroll 2
-    for (int i = 0; i < nc; ++i) {
+    for (int i = 0; i < nc; ++i, img += npix) {
       const BpViewF f = sv[i];
-      const float* img = a.corr + (size_t)(c0 + i) * npix;
       const float xi = fmaf(f.cphi, xw, -f.sphi * yw);
       const float yi = fmaf(f.sphi, xw, f.cphi * yw);
       const float depth = f.sod + yi;
@@ -793,7 +784,9 @@ __global__ void __launch_bounds__(BP_THREADS) bp_kernel(const BpArgs<Vox> a) {
       if (edge_d < BP_EDGE_EPS || depth <= f.depth_floor) {
         if (edge_d > -BP_EDGE_EPS || depth <= f.depth_floor) {
           const int vid = a.view_ids ? a.view_ids[c0 + i] : c0 + i;
-          bp_refine(a.dets[vid], w64[0], w64[1], w64[2], img, a.rows, a.cols, num, den);
+          const float2 nd = bp_refine(a.vox, m, a.dets[vid], img, a.rows, a.cols);
+          num += nd.x;
+          den += nd.y;
         }
         continue;
       }

@@ -207,3 +207,20 @@ def intensities_to_line_integrals(ps: ProjectionSet, i0) -> ProjectionSet:
     i0t = torch.as_tensor(i0, device=dev)
     p = (-torch.log(img.to(torch.float64) / i0t)).to(torch.float32)
     return ProjectionSet(ps.geom, p if ps.on_device else D.to_host(p), LINE_INTEGRAL)
+
+
+def simulate_scan(vol, geom: ScanGeometry, sampling: RaySamplingConfig | None = None,
+                  noise_sigma: float = 0.0, rng=None) -> ProjectionSet:
+    """All views (one batched FP launch) plus optional Gaussian pixel noise
+    (``cyltomo/experiments.py:31-39``).  The noise is drawn on the host from
+    ``rng`` (default ``default_rng(0)``) with the reference's call, so a seeded
+    scan has the same noise realisation as the reference's."""
+    ps = forward_project_all(vol, geom, sampling)
+    if noise_sigma <= 0.0:
+        return ps
+    rng = rng or np.random.default_rng(0)
+    host = D.to_host(ps.images) if ps.on_device else ps.images
+    noisy = host.astype(np.float64) + rng.normal(0.0, noise_sigma, host.shape)
+    if ps.on_device:
+        return ProjectionSet(geom, D.to_device(noisy.astype(np.float32)), ps.kind)
+    return ProjectionSet(geom, noisy, ps.kind)

@@ -29,5 +29,7 @@ for _ in range(args.reps):
     run.eng.pack(run.mu, run.gather)
     run.eng.correction(run.mu, run.p_meas, slots, len(s), run.corr, run.gather)
     run.eng.bp_update(run.corr, slots, len(s), run.upd)
+run.eng.pack(run.mu, run.gather)
+run.eng.residual(run.mu, run.p_meas, run.all_slots, wl.geom.n_proj, run.resid_cur, run.gather)
 torch.cuda.synchronize()
 print("prof driver done")
