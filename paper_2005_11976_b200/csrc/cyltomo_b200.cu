@@ -142,6 +142,7 @@ struct CylGeo {
   double radius, half_h;
   // fp32 sampling constants
   float inv_dr, inv_dth, inv_dh, h_off, nr_m1, nh_m1;
+  unsigned ntnr, idx_bias;
 
   __host__ void init(const float* m, const float* gather, const ct_cyl_grid& g) {
     mu = m;
@@ -155,6 +156,9 @@ struct CylGeo {
     h_off = (float)(0.5 * g.n_h - 0.5);
     nr_m1 = (float)(g.n_r - 1);
     nh_m1 = (float)(g.n_h - 1);
+    const unsigned B = 0x4B000000u;
+    ntnr = (unsigned)g.n_theta * (unsigned)g.n_r;
+    idx_bias = 0u - (B * ntnr + (B + 1u) * (unsigned)g.n_r + B);   // mod 2^32
   }
 
   // _kernels.py:170-204 (same operation order)
@@ -201,21 +205,27 @@ struct CylGeo {
     return true;
   }
 
-  // trilinear cell (index of its (k0, j0, i0) corner) and weights of a point
+  // trilinear cell (index of its (k0, j0, i0) corner) and weights of a point.
+  // floor() via x + 2^23 rounded toward -inf: the float's bit pattern is
+  // floor(x) + 0x4B000000, and the three 0x4B000000 offsets are folded into
+  // one constant (idx_bias) of the modular uint32 index arithmetic.
   __device__ __forceinline__ int locate(float x, float y, float z, float& wr, float& wt,
                                         float& wh) const {
     const float r = sqrt_approx(fmaf(x, x, y * y));
     const float th = theta_2pi(y, x);
     const float fr = fminf(fmaxf(fmaf(r, inv_dr, -0.5f), 0.0f), nr_m1);
     const float fh = fminf(fmaxf(fmaf(z, inv_dh, h_off), 0.0f), nh_m1);
-    const float ft1 = fmaf(th, inv_dth, 0.5f);
-    int i0, k0, g;
-    wr = fr - floor_pos(fr, i0);
-    wh = fh - floor_pos(fh, k0);
-    wt = ft1 - floor_pos(ft1, g);
-    int j0 = g - 1;
-    j0 = (j0 < 0) ? nt - 1 : j0;
-    return (k0 * nt + j0) * nr + i0;
+    const float ft1 = fmaf(th, inv_dth, 0.5f);   // theta index + 1, in [0.5, nt + 0.5]
+    const float tr = __fadd_rd(fr, 8388608.0f);
+    const float th_ = __fadd_rd(fh, 8388608.0f);
+    const float tt = __fadd_rd(ft1, 8388608.0f);
+    wr = fr - (tr - 8388608.0f);
+    wh = fh - (th_ - 8388608.0f);
+    wt = ft1 - (tt - 8388608.0f);
+    const unsigned ib = __float_as_uint(tr), kb = __float_as_uint(th_);
+    unsigned gb = __float_as_uint(tt);            // (j0 + 1) + 0x4B000000, j0 = -1 wraps
+    gb = (gb == 0x4B000000u) ? gb + (unsigned)nt : gb;
+    return (int)(kb * ntnr + gb * (unsigned)nr + ib + idx_bias);
   }
 
   template <bool NEAREST, bool OCT>
@@ -261,6 +271,7 @@ struct CartGeo {
   int nz, ny, nx;
   double vs, lo[3], hi[3];
   float inv_vs, off[3], nx_m1, ny_m1, nz_m1;
+  unsigned nynx, idx_bias;
 
   __host__ void init(const float* m, const float* gather, const ct_cart_grid& g) {
     mu = m;
@@ -274,6 +285,9 @@ struct CartGeo {
     inv_vs = (float)(1.0 / g.voxel_size);
     for (int a = 0; a < 3; ++a) off[a] = (float)(-g.origin[a] / g.voxel_size - 0.5);
     nx_m1 = (float)(nx - 1); ny_m1 = (float)(ny - 1); nz_m1 = (float)(nz - 1);
+    const unsigned B = 0x4B000000u;
+    nynx = (unsigned)ny * (unsigned)nx;
+    idx_bias = 0u - (B * nynx + B * (unsigned)nx + B);              // mod 2^32
   }
 
   // _kernels.py:207-231
@@ -323,11 +337,14 @@ struct CartGeo {
     const float fx = fminf(fmaxf(fmaf(x, inv_vs, off[0]), 0.0f), nx_m1);
     const float fy = fminf(fmaxf(fmaf(y, inv_vs, off[1]), 0.0f), ny_m1);
     const float fz = fminf(fmaxf(fmaf(z, inv_vs, off[2]), 0.0f), nz_m1);
-    int i0, j0, k0;
-    wx = fx - floor_pos(fx, i0);
-    wy = fy - floor_pos(fy, j0);
-    wz = fz - floor_pos(fz, k0);
-    return (k0 * ny + j0) * nx + i0;
+    const float tx = __fadd_rd(fx, 8388608.0f);
+    const float ty = __fadd_rd(fy, 8388608.0f);
+    const float tz = __fadd_rd(fz, 8388608.0f);
+    wx = fx - (tx - 8388608.0f);
+    wy = fy - (ty - 8388608.0f);
+    wz = fz - (tz - 8388608.0f);
+    return (int)(__float_as_uint(tz) * nynx + __float_as_uint(ty) * (unsigned)nx +
+                 __float_as_uint(tx) + idx_bias);
   }
 
   template <bool NEAREST, bool OCT>
@@ -365,6 +382,7 @@ struct CartGeo {
 enum FpEpi { EPI_PROJECT = 0, EPI_CORR = 1, EPI_RESID = 2, EPI_ROWMAX = 3 };
 
 constexpr int FP_TILE_W = 16, FP_TILE_H = 8, FP_THREADS = 128;
+constexpr int FP_MIN_BLOCKS = 9;   // <= 56 registers: 36 resident warps per SM
 
 template <class Geo>
 struct FpArgs {
@@ -412,6 +430,7 @@ __device__ __forceinline__ int march(const Geo& geo, const ct_ray_view& v, doubl
     // Same values, same lerp, same summation grouping as the plain path.
     int prev = -1;
     float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pb = pa;
+    const float4* __restrict__ oct = geo.oct;
     // one live cell (pa, pb): the loads are predicated on a cell change and
     // land in the same registers -- no forwarding copies; resident warps hide
     // the resulting load->lerp serialisation.
@@ -419,8 +438,9 @@ __device__ __forceinline__ int march(const Geo& geo, const ct_ray_view& v, doubl
       float w0, w1, w2;
       const int idx = geo.locate(fmaf(kq, ix, ex), fmaf(kq, iy, ey), fmaf(kq, iz, ez), w0, w1, w2);
       if (idx != prev) {
-        pa = __ldg(geo.oct + 2 * idx);
-        pb = __ldg(geo.oct + 2 * idx + 1);
+        const float4* cell = oct + 2 * (size_t)(unsigned)idx;
+        pa = __ldg(cell);
+        pb = __ldg(cell + 1);
         prev = idx;
       }
       return lerp8(pa, pb, w0, w1, w2);
@@ -471,7 +491,7 @@ __device__ __forceinline__ double warp_max(double x) {
 }
 
 template <class Geo, int EPI, bool NEAREST, bool OCT>
-__global__ void __launch_bounds__(FP_THREADS) fp_kernel(const FpArgs<Geo> a) {
+__global__ void __launch_bounds__(FP_THREADS, FP_MIN_BLOCKS) fp_kernel(const FpArgs<Geo> a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // each warp covers an 8x4 pixel patch; the block a 16x8 tile
   const int col = blockIdx.x * FP_TILE_W + (warp & 1) * 8 + (lane & 7);
@@ -761,7 +781,7 @@ __global__ void __launch_bounds__(BP_THREADS) bp_kernel(const __grid_constant__ 
       BpViewF f;
       f.cphi = (float)d.cphi; f.sphi = (float)d.sphi; f.sod = (float)d.sod;
       f.sdd_p = (float)(d.sdd / d.pitch);
-      f.u0 = (float)d.u0; f.v0 = (float)d.v0;
+      f.u0 = (float)(d.u0 + 1.0); f.v0 = (float)(d.v0 + 1.0);   // stores u0 + 1, v0 + 1
       f.depth_floor = (float)(2e-6 * d.sod);  // refine band: 2x the reference floor
       f._pad = 0.0f;
       sv[threadIdx.x] = f;
@@ -776,8 +796,8 @@ __global__ void __launch_bounds__(BP_THREADS) bp_kernel(const __grid_constant__ 
       const float yi = fmaf(f.sphi, xw, f.cphi * yw);
       const float depth = f.sod + yi;
       const float scale = f.sdd_p * rcp_nr(depth);
-      const float u1 = fmaf(xi, scale, f.u0) + 1.0f;   // u + 1
-      const float v1 = fmaf(zw, scale, f.v0) + 1.0f;   // v + 1
+      const float u1 = fmaf(xi, scale, f.u0);   // u + 1
+      const float v1 = fmaf(zw, scale, f.v0);   // v + 1
       // signed distance (px) of the footprint to the boundary of the set
       // where den > 0, i.e. (-1, W) x (-1, H); near it, redo in fp64.
       const float edge_d = fminf(fminf(u1, W1 - u1), fminf(v1, H1 - v1));
@@ -796,7 +816,8 @@ __global__ void __launch_bounds__(BP_THREADS) bp_kernel(const __grid_constant__ 
       iu -= 1;
       iv -= 1;
       const float wu0 = 1.0f - fu, wv0 = 1.0f - fv;
-      if (iu >= 0 && iu + 1 < a.cols && iv >= 0 && iv + 1 < a.rows) {
+      // edge_d > 1 <=> 0 <= floor(u), floor(u)+1 < W (same for v): all 4 taps in bounds
+      if (edge_d > 1.0f) {
         // whole footprint on the detector: the four weights sum to 1
         const float* r0 = img + (iv * a.cols + iu);
         const float t00 = __ldg(r0), t01 = __ldg(r0 + 1);
