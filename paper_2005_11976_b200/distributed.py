@@ -220,7 +220,7 @@ class ShardedSartRun:
         res = ([math.sqrt(float(x)) for x in self.resid.cpu().numpy()]
                if self.cfg.compute_residuals else [])
         mu = self.mu if self.ps.on_device else self.mu.cpu().numpy()
-        return (_volume_cls(self.grid)(self.grid, mu),
+        return (_volume_cls(self.grid)._trusted(self.grid, mu),
                 ReconReport(residuals=res, wall_time=wall, config=_config_echo(self.cfg)))
 
 

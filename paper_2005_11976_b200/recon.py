@@ -384,8 +384,8 @@ class SartRun:
         wall = time.perf_counter() - t0
         residuals = ([math.sqrt(float(x)) for x in D.to_host(self.resid)]
                      if self.cfg.compute_residuals else [])
-        mu = self.mu if self.ps.on_device else D.to_host(self.mu)
-        vol = _volume_cls(self.grid)(self.grid, mu)
+        mu = self.mu if self.ps.on_device else D.to_host(self.mu, pinned=True)
+        vol = _volume_cls(self.grid)._trusted(self.grid, mu)
         return vol, ReconReport(residuals=residuals, wall_time=wall,
                                 config=_config_echo(self.cfg))
 
