@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define CT_ABI_VERSION 2
+#define CT_ABI_VERSION 3
 
 #define CT_OK 0
 #define CT_ERR_ARG (-1)   /* invalid argument (null pointer, bad size) */
@@ -199,10 +199,15 @@ int ct_sart_update(const float *num, const float *den, int64_t offset, int64_t c
                    const ct_update *upd, ct_stream_t stream);
 
 /* ---- gather layout for the forward projector ------------------------------ */
-/* Number of floats of the gather buffer for a volume of n_voxels (8 per voxel). */
-int64_t ct_gather_floats(int64_t n_voxels);
-/* gather[8m..8m+7] = mu at (k,j,i),(k,j,i+1),(k,j+1,i),(k,j+1,i+1), then the same
- * at k+1 (r/h clamp, theta wraps; Cartesian: all three clamp).  16B aligned. */
+/* Number of floats of the gather buffer: 8 per cell, cells (n_h+1, n_theta,
+ * n_r+1) for a cylindrical grid, (n_z+1, n_y+1, n_x+1) for a Cartesian one. */
+int64_t ct_gather_floats_cyl(const ct_cyl_grid *grid);
+int64_t ct_gather_floats_cart(const ct_cart_grid *grid);
+/* Cell (kc, j, ic) holds the trilinear corner (k, j, i) = (kc-1, j, ic-1) with a
+ * one-cell halo at index -1 (duplicating index 0): v00, d00, v01, d01, then the
+ * same at k+1, where vXY = mu(k+X, j+Y, i) and dXY = mu(k+X, j+Y, i+1) - vXY
+ * (r/h clamp to the grid, theta wraps; Cartesian: y plays theta's role and all
+ * three axes clamp).  16-byte aligned. */
 int ct_pack_gather_cyl(const float *mu, const ct_cyl_grid *grid, float *gather,
                        ct_stream_t stream);
 int ct_pack_gather_cart(const float *mu, const ct_cart_grid *grid, float *gather,

@@ -106,6 +106,14 @@ def grid_c(grid):
     raise TypeError(f"cannot project onto {type(grid).__name__}")
 
 
+def alloc_gather(grid, device):
+    """Device buffer for the FP gather layout of `grid` (ct_pack_gather_*)."""
+    lib = N.load_library()
+    g = grid_c(grid)
+    fn = lib.ct_gather_floats_cyl if isinstance(grid, CylGrid) else lib.ct_gather_floats_cart
+    return torch_mod().empty(int(fn(C.byref(g))), dtype=torch_mod().float32, device=device)
+
+
 def sampling_c(step: float, supersample: int, nearest: bool) -> N.SamplingC:
     s = N.SamplingC()
     s.step = float(step)

@@ -16,10 +16,11 @@ from pathlib import Path
 from .errors import NativeError, NativeUnavailable
 
 LIB_NAME = "libcyltomo_b200.so"
-LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
+# CT_LIBRARY overrides the in-tree library (A/B builds of the same ABI)
+LIB_PATH = Path(os.environ.get("CT_LIBRARY") or Path(__file__).resolve().parent / LIB_NAME)
 
 CT_OK = 0
-CT_ABI_VERSION = 2
+CT_ABI_VERSION = 3
 
 
 class CylGridC(C.Structure):
@@ -76,7 +77,8 @@ _SIGNATURES = {
                                      C.POINTER(SamplingC), P, P, P, P]),
     "ct_fp_cart_residual": (C.c_int, [P, P, C.POINTER(CartGridC), P, C.POINTER(BatchC),
                                       C.POINTER(SamplingC), P, P, P, P]),
-    "ct_gather_floats": (C.c_int64, [C.c_int64]),
+    "ct_gather_floats_cyl": (C.c_int64, [C.POINTER(CylGridC)]),
+    "ct_gather_floats_cart": (C.c_int64, [C.POINTER(CartGridC)]),
     "ct_pack_gather_cyl": (C.c_int, [P, C.POINTER(CylGridC), P, P]),
     "ct_pack_gather_cart": (C.c_int, [P, C.POINTER(CartGridC), P, P]),
     "ct_rowsum_max_cyl": (C.c_int, [C.POINTER(CylGridC), P, C.POINTER(BatchC),

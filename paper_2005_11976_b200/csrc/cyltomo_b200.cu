@@ -120,6 +120,34 @@ __device__ __forceinline__ float theta_2pi(float y, float x) {
   return (y < 0.0f) ? (kTwoPiF - t) : t;
 }
 
+// trilinear value from a gather cell: a = (v00, d00, v01, d01) at k0, b = the
+// same at k1, vXY = mu at (j0+Y, i0), dXY = mu(j0+Y, i0+1) - vXY.  The
+// differences are the ones lerp8 computes in-kernel (same fp32 op), so both
+// paths give identical bits.
+__device__ __forceinline__ float lerp8d(float4 a, float4 b, float wr, float wt, float wh) {
+  const float c00 = fmaf(a.y, wr, a.x);
+  const float c01 = fmaf(a.w, wr, a.z);
+  const float c10 = fmaf(b.y, wr, b.x);
+  const float c11 = fmaf(b.w, wr, b.z);
+  const float q0 = fmaf(c01 - c00, wt, c00);
+  const float q1 = fmaf(c11 - c10, wt, c10);
+  return fmaf(q1 - q0, wh, q0);
+}
+
+// one 32-byte cell of the gather layout with a single 256-bit load
+// (sm_100 LDG.E.ENL2.256; read-only path)
+__device__ __forceinline__ void ld_cell(const float4* p, float4& a, float4& b) {
+#if defined(CT_CELL_LOAD_128)
+  a = __ldg(p);
+  b = __ldg(p + 1);
+#else
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z),
+                 "=f"(b.w)
+               : "l"(p));
+#endif
+}
+
 __device__ __forceinline__ float lerp8(float4 a, float4 b, float wr, float wt, float wh) {
   // a = (k0,j0,i0) (k0,j0,i1) (k0,j1,i0) (k0,j1,i1); b = same at k1
   const float c00 = fmaf(a.y - a.x, wr, a.x);
@@ -141,8 +169,8 @@ struct CylGeo {
   int nh, nt, nr;
   double radius, half_h;
   // fp32 sampling constants
-  float inv_dr, inv_dth, inv_dh, h_off, nr_m1, nh_m1;
-  unsigned ntnr, idx_bias;
+  float inv_dr, inv_dth, inv_dh, h_off, h_off1, nr_m1, nh_m1;
+  unsigned cell_kstride, cell_jstride, idx_bias;   // gather layout (nh+1, nt, nr+1)
 
   __host__ void init(const float* m, const float* gather, const ct_cyl_grid& g) {
     mu = m;
@@ -156,9 +184,11 @@ struct CylGeo {
     h_off = (float)(0.5 * g.n_h - 0.5);
     nr_m1 = (float)(g.n_r - 1);
     nh_m1 = (float)(g.n_h - 1);
+    h_off1 = h_off + 1.0f;
     const unsigned B = 0x4B000000u;
-    ntnr = (unsigned)g.n_theta * (unsigned)g.n_r;
-    idx_bias = 0u - (B * ntnr + (B + 1u) * (unsigned)g.n_r + B);   // mod 2^32
+    cell_jstride = (unsigned)g.n_r + 1u;
+    cell_kstride = (unsigned)g.n_theta * cell_jstride;
+    idx_bias = 0u - (B * cell_kstride + (B + 1u) * cell_jstride + B);   // mod 2^32
   }
 
   // _kernels.py:170-204 (same operation order)
@@ -205,54 +235,64 @@ struct CylGeo {
     return true;
   }
 
-  // trilinear cell (index of its (k0, j0, i0) corner) and weights of a point.
-  // floor() via x + 2^23 rounded toward -inf: the float's bit pattern is
-  // floor(x) + 0x4B000000, and the three 0x4B000000 offsets are folded into
-  // one constant (idx_bias) of the modular uint32 index arithmetic.
+  // Gather-layout cell of a point and its trilinear weights.  The layout has a
+  // one-cell halo at r/h index -1 (duplicating index 0, r-difference 0), so no
+  // clamps are needed: at a clamped position the reference's weight is 0 and
+  // here the weight multiplies an exact 0 -- same value.  floor() via
+  // x + 2^23 rounded toward -inf (bits = floor(x) + 0x4B000000); the offsets
+  // fold into idx_bias (modular uint32 arithmetic).
   __device__ __forceinline__ int locate(float x, float y, float z, float& wr, float& wt,
                                         float& wh) const {
     const float r = sqrt_approx(fmaf(x, x, y * y));
     const float th = theta_2pi(y, x);
-    const float fr = fminf(fmaxf(fmaf(r, inv_dr, -0.5f), 0.0f), nr_m1);
-    const float fh = fminf(fmaxf(fmaf(z, inv_dh, h_off), 0.0f), nh_m1);
-    const float ft1 = fmaf(th, inv_dth, 0.5f);   // theta index + 1, in [0.5, nt + 0.5]
-    const float tr = __fadd_rd(fr, 8388608.0f);
-    const float th_ = __fadd_rd(fh, 8388608.0f);
+    const float fr1 = fmaf(r, inv_dr, 0.5f);      // r index + 1 (halo), >= 0.5
+    const float fh1 = fmaf(z, inv_dh, h_off1);    // h index + 1 (halo), >= 0.5
+    const float ft1 = fmaf(th, inv_dth, 0.5f);    // theta index + 1, in [0.5, nt + 0.5]
+    const float tr = __fadd_rd(fr1, 8388608.0f);
+    const float th_ = __fadd_rd(fh1, 8388608.0f);
     const float tt = __fadd_rd(ft1, 8388608.0f);
-    wr = fr - (tr - 8388608.0f);
-    wh = fh - (th_ - 8388608.0f);
+    wr = fr1 - (tr - 8388608.0f);
+    wh = fh1 - (th_ - 8388608.0f);
     wt = ft1 - (tt - 8388608.0f);
-    const unsigned ib = __float_as_uint(tr), kb = __float_as_uint(th_);
     unsigned gb = __float_as_uint(tt);            // (j0 + 1) + 0x4B000000, j0 = -1 wraps
     gb = (gb == 0x4B000000u) ? gb + (unsigned)nt : gb;
-    return (int)(kb * ntnr + gb * (unsigned)nr + ib + idx_bias);
+    return (int)(__float_as_uint(th_) * cell_kstride + gb * cell_jstride +
+                 __float_as_uint(tr) + idx_bias);
   }
 
   template <bool NEAREST, bool OCT>
   __device__ __forceinline__ float sample(float x, float y, float z) const {
+    if (OCT && !NEAREST) {
+      float wr, wt, wh;
+      const int idx = locate(x, y, z, wr, wt, wh);
+      float4 a, b;
+      ld_cell(oct + 2 * (size_t)(unsigned)idx, a, b);
+      return lerp8d(a, b, wr, wt, wh);
+    }
     const float r = sqrt_approx(fmaf(x, x, y * y));
     const float th = theta_2pi(y, x);
-    const float fr = fminf(fmaxf(fmaf(r, inv_dr, -0.5f), 0.0f), nr_m1);
-    const float fh = fminf(fmaxf(fmaf(z, inv_dh, h_off), 0.0f), nh_m1);
     const float ft1 = fmaf(th, inv_dth, 0.5f);  // theta index + 1, in [0.5, nt + 0.5]
     if (NEAREST) {
+      const float fr = fminf(fmaxf(fmaf(r, inv_dr, -0.5f), 0.0f), nr_m1);
+      const float fh = fminf(fmaxf(fmaf(z, inv_dh, h_off), 0.0f), nh_m1);
       int ir = (int)rintf(fr), ih = (int)rintf(fh), it = (int)rintf(ft1 - 1.0f);
       if (it < 0) it += nt;
       if (it >= nt) it -= nt;
       return __ldg(mu + (ih * nt + it) * nr + ir);
     }
+    // plain layout: same "+1" index formulation as locate(), clamped to
+    // [1, n] (the reference's [0, n-1] clamp), so weights are bit-identical
+    const float fr1 = fminf(fmaxf(fmaf(r, inv_dr, 0.5f), 1.0f), nr_m1 + 1.0f);
+    const float fh1 = fminf(fmaxf(fmaf(z, inv_dh, h_off1), 1.0f), nh_m1 + 1.0f);
     int i0, k0, g;
-    const float wr = fr - floor_pos(fr, i0);
-    const float wh = fh - floor_pos(fh, k0);
+    const float wr = fr1 - floor_pos(fr1, i0);
+    const float wh = fh1 - floor_pos(fh1, k0);
     const float wt = ft1 - floor_pos(ft1, g);
+    i0 -= 1;
+    k0 -= 1;
     int j0 = g - 1;
     j0 = (j0 < 0) ? nt - 1 : j0;
     const int idx = (k0 * nt + j0) * nr + i0;
-    if (OCT) {
-      const float4 a = __ldg(oct + 2 * idx);
-      const float4 b = __ldg(oct + 2 * idx + 1);
-      return lerp8(a, b, wr, wt, wh);
-    }
     const int di = (i0 + 1 < nr) ? 1 : 0;
     const int dj = (j0 + 1 < nt) ? nr : -(nt - 1) * nr;
     const int dk = (k0 + 1 < nh) ? nt * nr : 0;
@@ -270,8 +310,8 @@ struct CartGeo {
   const float4* __restrict__ oct;  // gather layout (ct_pack_gather_cart) or null
   int nz, ny, nx;
   double vs, lo[3], hi[3];
-  float inv_vs, off[3], nx_m1, ny_m1, nz_m1;
-  unsigned nynx, idx_bias;
+  float inv_vs, off[3], off1[3], nx_m1, ny_m1, nz_m1;
+  unsigned cell_kstride, cell_jstride, idx_bias;   // gather layout (nz+1, ny+1, nx+1)
 
   __host__ void init(const float* m, const float* gather, const ct_cart_grid& g) {
     mu = m;
@@ -285,9 +325,11 @@ struct CartGeo {
     inv_vs = (float)(1.0 / g.voxel_size);
     for (int a = 0; a < 3; ++a) off[a] = (float)(-g.origin[a] / g.voxel_size - 0.5);
     nx_m1 = (float)(nx - 1); ny_m1 = (float)(ny - 1); nz_m1 = (float)(nz - 1);
+    for (int a = 0; a < 3; ++a) off1[a] = off[a] + 1.0f;
     const unsigned B = 0x4B000000u;
-    nynx = (unsigned)ny * (unsigned)nx;
-    idx_bias = 0u - (B * nynx + B * (unsigned)nx + B);              // mod 2^32
+    cell_jstride = (unsigned)nx + 1u;
+    cell_kstride = ((unsigned)ny + 1u) * cell_jstride;
+    idx_bias = 0u - B * (cell_kstride + cell_jstride + 1u);          // mod 2^32
   }
 
   // _kernels.py:207-231
@@ -332,38 +374,49 @@ struct CartGeo {
              f[2] < -0.5 || f[2] > nz - 0.5);
   }
 
+  // gather-layout cell (halo at index -1 on all three axes, see CylGeo)
   __device__ __forceinline__ int locate(float x, float y, float z, float& wx, float& wy,
                                         float& wz) const {
-    const float fx = fminf(fmaxf(fmaf(x, inv_vs, off[0]), 0.0f), nx_m1);
-    const float fy = fminf(fmaxf(fmaf(y, inv_vs, off[1]), 0.0f), ny_m1);
-    const float fz = fminf(fmaxf(fmaf(z, inv_vs, off[2]), 0.0f), nz_m1);
-    const float tx = __fadd_rd(fx, 8388608.0f);
-    const float ty = __fadd_rd(fy, 8388608.0f);
-    const float tz = __fadd_rd(fz, 8388608.0f);
-    wx = fx - (tx - 8388608.0f);
-    wy = fy - (ty - 8388608.0f);
-    wz = fz - (tz - 8388608.0f);
-    return (int)(__float_as_uint(tz) * nynx + __float_as_uint(ty) * (unsigned)nx +
+    const float fx1 = fmaf(x, inv_vs, off1[0]);
+    const float fy1 = fmaf(y, inv_vs, off1[1]);
+    const float fz1 = fmaf(z, inv_vs, off1[2]);
+    const float tx = __fadd_rd(fx1, 8388608.0f);
+    const float ty = __fadd_rd(fy1, 8388608.0f);
+    const float tz = __fadd_rd(fz1, 8388608.0f);
+    wx = fx1 - (tx - 8388608.0f);
+    wy = fy1 - (ty - 8388608.0f);
+    wz = fz1 - (tz - 8388608.0f);
+    return (int)(__float_as_uint(tz) * cell_kstride + __float_as_uint(ty) * cell_jstride +
                  __float_as_uint(tx) + idx_bias);
   }
 
   template <bool NEAREST, bool OCT>
   __device__ __forceinline__ float sample(float x, float y, float z) const {
-    const float fx = fminf(fmaxf(fmaf(x, inv_vs, off[0]), 0.0f), nx_m1);
-    const float fy = fminf(fmaxf(fmaf(y, inv_vs, off[1]), 0.0f), ny_m1);
-    const float fz = fminf(fmaxf(fmaf(z, inv_vs, off[2]), 0.0f), nz_m1);
-    if (NEAREST)
-      return __ldg(mu + ((int)rintf(fz) * ny + (int)rintf(fy)) * nx + (int)rintf(fx));
-    int i0, j0, k0;
-    const float wx = fx - floor_pos(fx, i0);
-    const float wy = fy - floor_pos(fy, j0);
-    const float wz = fz - floor_pos(fz, k0);
-    const int idx = (k0 * ny + j0) * nx + i0;
-    if (OCT) {
-      const float4 a = __ldg(oct + 2 * idx);
-      const float4 b = __ldg(oct + 2 * idx + 1);
-      return lerp8(a, b, wx, wy, wz);
+    if (OCT && !NEAREST) {
+      float wx, wy, wz;
+      const int idx = locate(x, y, z, wx, wy, wz);
+      float4 a, b;
+      ld_cell(oct + 2 * (size_t)(unsigned)idx, a, b);
+      return lerp8d(a, b, wx, wy, wz);
     }
+    if (NEAREST) {
+      const float fx = fminf(fmaxf(fmaf(x, inv_vs, off[0]), 0.0f), nx_m1);
+      const float fy = fminf(fmaxf(fmaf(y, inv_vs, off[1]), 0.0f), ny_m1);
+      const float fz = fminf(fmaxf(fmaf(z, inv_vs, off[2]), 0.0f), nz_m1);
+      return __ldg(mu + ((int)rintf(fz) * ny + (int)rintf(fy)) * nx + (int)rintf(fx));
+    }
+    // "+1" formulation clamped to [1, n], as locate() (bit-identical weights)
+    const float fx1 = fminf(fmaxf(fmaf(x, inv_vs, off1[0]), 1.0f), nx_m1 + 1.0f);
+    const float fy1 = fminf(fmaxf(fmaf(y, inv_vs, off1[1]), 1.0f), ny_m1 + 1.0f);
+    const float fz1 = fminf(fmaxf(fmaf(z, inv_vs, off1[2]), 1.0f), nz_m1 + 1.0f);
+    int i0, j0, k0;
+    const float wx = fx1 - floor_pos(fx1, i0);
+    const float wy = fy1 - floor_pos(fy1, j0);
+    const float wz = fz1 - floor_pos(fz1, k0);
+    i0 -= 1;
+    j0 -= 1;
+    k0 -= 1;
+    const int idx = (k0 * ny + j0) * nx + i0;
     const int di = (i0 + 1 < nx) ? 1 : 0;
     const int dj = (j0 + 1 < ny) ? nx : 0;
     const int dk = (k0 + 1 < nz) ? ny * nx : 0;
@@ -382,7 +435,10 @@ struct CartGeo {
 enum FpEpi { EPI_PROJECT = 0, EPI_CORR = 1, EPI_RESID = 2, EPI_ROWMAX = 3 };
 
 constexpr int FP_TILE_W = 16, FP_TILE_H = 8, FP_THREADS = 128;
-constexpr int FP_MIN_BLOCKS = 9;   // <= 56 registers: 36 resident warps per SM
+#ifndef CT_FP_MIN_BLOCKS
+#define CT_FP_MIN_BLOCKS 9
+#endif
+constexpr int FP_MIN_BLOCKS = CT_FP_MIN_BLOCKS;   // 9: <= 56 registers, 36 warps/SM
 
 template <class Geo>
 struct FpArgs {
@@ -438,12 +494,10 @@ __device__ __forceinline__ int march(const Geo& geo, const ct_ray_view& v, doubl
       float w0, w1, w2;
       const int idx = geo.locate(fmaf(kq, ix, ex), fmaf(kq, iy, ey), fmaf(kq, iz, ez), w0, w1, w2);
       if (idx != prev) {
-        const float4* cell = oct + 2 * (size_t)(unsigned)idx;
-        pa = __ldg(cell);
-        pb = __ldg(cell + 1);
+        ld_cell(oct + 2 * (size_t)(unsigned)idx, pa, pb);
         prev = idx;
       }
-      return lerp8(pa, pb, w0, w1, w2);
+      return lerp8d(pa, pb, w0, w1, w2);
     };
 #pragma unroll 1
     for (; k + 4 <= n_int; k += 4) {
@@ -504,7 +558,13 @@ __global__ void __launch_bounds__(FP_THREADS, FP_MIN_BLOCKS) fp_kernel(const FpA
 
   float acc = 0.0f;
   int count = 0;
-  if (active) {
+  if (active && a.ss == 1) {
+    // one sub-ray at the pixel centre ((0 + .5)/1 - .5 = 0 exactly): the view
+    // basis is dead after the per-ray setup, keeping the march loop's
+    // register footprint small
+    count = march<Geo, NEAREST, OCT, EPI == EPI_ROWMAX>(a.geo, a.views[vid], (double)col,
+                                                       (double)row, a.step, acc);
+  } else if (active) {
     const ct_ray_view& v = a.views[vid];
     const int ss = a.ss;
     for (int sv = 0; sv < ss; ++sv) {
@@ -1024,26 +1084,43 @@ __global__ void resample_cyl_kernel(const float* __restrict__ src_mu, ct_cyl_gri
 // ---------------------------------------------------------------------------
 __global__ void pack_gather_cyl_kernel(const float* __restrict__ mu, int nh, int nt, int nr,
                                        float4* __restrict__ oct) {
-  const int64_t n = (int64_t)nh * nt * nr;
+  // cells (kc, j, ic), kc in [0, nh], ic in [0, nr]: corner (kc-1, j, ic-1)
+  const int64_t n = (int64_t)(nh + 1) * nt * (nr + 1);
   const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= n) return;
-  const int i = (int)(m % nr), j = (int)((m / nr) % nt), k = (int)(m / ((int64_t)nr * nt));
-  const int i1 = min(i + 1, nr - 1), j1 = (j + 1 == nt) ? 0 : j + 1, k1 = min(k + 1, nh - 1);
+  const int ic = (int)(m % (nr + 1)), j = (int)((m / (nr + 1)) % nt);
+  const int kc = (int)(m / ((int64_t)(nr + 1) * nt));
+  const int i = max(ic - 1, 0), i1 = min(ic, nr - 1);
+  const int k = max(kc - 1, 0), k1 = min(kc, nh - 1);
+  const int j1 = (j + 1 == nt) ? 0 : j + 1;
   auto M = [&](int kk, int jj, int ii) { return __ldg(mu + ((int64_t)kk * nt + jj) * nr + ii); };
-  oct[2 * m] = make_float4(M(k, j, i), M(k, j, i1), M(k, j1, i), M(k, j1, i1));
-  oct[2 * m + 1] = make_float4(M(k1, j, i), M(k1, j, i1), M(k1, j1, i), M(k1, j1, i1));
+  const float v00 = M(k, j, i), v01 = M(k, j1, i), v10 = M(k1, j, i), v11 = M(k1, j1, i);
+  oct[2 * m] = make_float4(v00, M(k, j, i1) - v00, v01, M(k, j1, i1) - v01);
+  oct[2 * m + 1] = make_float4(v10, M(k1, j, i1) - v10, v11, M(k1, j1, i1) - v11);
 }
 
 __global__ void pack_gather_cart_kernel(const float* __restrict__ mu, int nz, int ny, int nx,
                                         float4* __restrict__ oct) {
-  const int64_t n = (int64_t)nz * ny * nx;
+  // cells (kc, jc, ic) in [0, n] per axis: corner (kc-1, jc-1, ic-1)
+  const int64_t n = (int64_t)(nz + 1) * (ny + 1) * (nx + 1);
   const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= n) return;
-  const int i = (int)(m % nx), j = (int)((m / nx) % ny), k = (int)(m / ((int64_t)nx * ny));
-  const int i1 = min(i + 1, nx - 1), j1 = min(j + 1, ny - 1), k1 = min(k + 1, nz - 1);
+  const int ic = (int)(m % (nx + 1)), jc = (int)((m / (nx + 1)) % (ny + 1));
+  const int kc = (int)(m / ((int64_t)(nx + 1) * (ny + 1)));
+  const int i = max(ic - 1, 0), i1 = min(ic, nx - 1);
+  const int j = max(jc - 1, 0), j1 = min(jc, ny - 1);
+  const int k = max(kc - 1, 0), k1 = min(kc, nz - 1);
   auto M = [&](int kk, int jj, int ii) { return __ldg(mu + ((int64_t)kk * ny + jj) * nx + ii); };
-  oct[2 * m] = make_float4(M(k, j, i), M(k, j, i1), M(k, j1, i), M(k, j1, i1));
-  oct[2 * m + 1] = make_float4(M(k1, j, i), M(k1, j, i1), M(k1, j1, i), M(k1, j1, i1));
+  const float v00 = M(k, j, i), v01 = M(k, j1, i), v10 = M(k1, j, i), v11 = M(k1, j1, i);
+  oct[2 * m] = make_float4(v00, M(k, j, i1) - v00, v01, M(k, j1, i1) - v01);
+  oct[2 * m + 1] = make_float4(v10, M(k1, j, i1) - v10, v11, M(k1, j1, i1) - v11);
+}
+
+int64_t gather_cells_cyl(const ct_cyl_grid& g) {
+  return (int64_t)(g.n_h + 1) * g.n_theta * (g.n_r + 1);
+}
+int64_t gather_cells_cart(const ct_cart_grid& g) {
+  return (int64_t)(g.n_z + 1) * (g.n_y + 1) * (g.n_x + 1);
 }
 
 unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -1281,7 +1358,12 @@ int ct_resample_cyl_to_cyl(const float* src_mu, const ct_cyl_grid* src, const ct
   return check_launch("resample_cyl_kernel");
 }
 
-int64_t ct_gather_floats(int64_t n_voxels) { return n_voxels < 0 ? 0 : 8 * n_voxels; }
+int64_t ct_gather_floats_cyl(const ct_cyl_grid* grid) {
+  return check_cyl(grid) ? 0 : 8 * gather_cells_cyl(*grid);
+}
+int64_t ct_gather_floats_cart(const ct_cart_grid* grid) {
+  return check_cart(grid) ? 0 : 8 * gather_cells_cart(*grid);
+}
 
 int ct_pack_gather_cyl(const float* mu, const ct_cyl_grid* grid, float* gather,
                        ct_stream_t stream) {
@@ -1289,7 +1371,7 @@ int ct_pack_gather_cyl(const float* mu, const ct_cyl_grid* grid, float* gather,
   if (rc) return rc;
   if (!mu || !gather) return set_err(CT_ERR_ARG, "null mu/gather");
   if (reinterpret_cast<uintptr_t>(gather) % 16) return set_err(CT_ERR_ARG, "gather not 16B-aligned");
-  const int64_t n = (int64_t)grid->n_h * grid->n_theta * grid->n_r;
+  const int64_t n = gather_cells_cyl(*grid);
   pack_gather_cyl_kernel<<<blocks_for(n, 256), 256, 0, CT_STREAM(stream)>>>(
       mu, grid->n_h, grid->n_theta, grid->n_r, reinterpret_cast<float4*>(gather));
   return check_launch("pack_gather_cyl_kernel");
@@ -1301,7 +1383,7 @@ int ct_pack_gather_cart(const float* mu, const ct_cart_grid* grid, float* gather
   if (rc) return rc;
   if (!mu || !gather) return set_err(CT_ERR_ARG, "null mu/gather");
   if (reinterpret_cast<uintptr_t>(gather) % 16) return set_err(CT_ERR_ARG, "gather not 16B-aligned");
-  const int64_t n = (int64_t)grid->n_z * grid->n_y * grid->n_x;
+  const int64_t n = gather_cells_cart(*grid);
   pack_gather_cart_kernel<<<blocks_for(n, 256), 256, 0, CT_STREAM(stream)>>>(
       mu, grid->n_z, grid->n_y, grid->n_x, reinterpret_cast<float4*>(gather));
   return check_launch("pack_gather_cart_kernel");

@@ -114,7 +114,7 @@ def _project(vol, geom: ScanGeometry, views, cfg: RaySamplingConfig, want_w: boo
     gather = None
     if nv >= GATHER_MIN_VIEWS and cfg.interpolation == "linear":
         # multi-view launches amortise building the sector-per-sample layout
-        gather = torch.empty(vol.grid.n_voxels * 8, dtype=torch.float32, device=dev)
+        gather = D.alloc_gather(vol.grid, dev)
         N.call("ct_pack_gather_cyl" if cyl else "ct_pack_gather_cart", D.ptr(mu), C.byref(g),
                D.ptr(gather), D.stream_handle())
     N.call("ct_fp_cyl" if cyl else "ct_fp_cart", D.ptr(mu), D.ptr(gather), C.byref(g),

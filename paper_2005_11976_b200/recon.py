@@ -164,8 +164,7 @@ class SartEngine:
         torch = D.torch_mod()
         if self.samp.nearest:
             return None
-        n = int(N.load_library().ct_gather_floats(int(np.prod(self.grid.shape))))
-        return torch.empty(n, dtype=torch.float32, device=self.device)
+        return D.alloc_gather(self.grid, self.device)
 
     def pack(self, mu, gather) -> None:
         if gather is None:

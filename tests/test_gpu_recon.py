@@ -300,24 +300,30 @@ def test_graph_replay_bit_identical(small_cyl_setup):
     assert ra.residuals == rb.residuals
 
 
-def test_gather_layout_matches_plain_path(rng):
-    """The sector-per-sample gather layout changes the loads, not the result."""
+@pytest.mark.parametrize("kind", ["cyl", "cart"])
+def test_gather_layout_matches_plain_path(rng, kind):
+    """The gather layout (halo, stored differences, 256-bit loads, cell reuse)
+    changes the loads, not the result: bit-identical to the plain path."""
     import ctypes as C
     import torch
     from paper_2005_11976_b200 import _device as D, _native as N
-    grid = CylGrid(12, 20, 10, 5.0, 9.0, Pose.tilt(0.2, 0.1, [0.3, 0.1, 0.2]))
+    if kind == "cyl":
+        grid = CylGrid(12, 20, 10, 5.0, 9.0, Pose.tilt(0.2, 0.1, [0.3, 0.1, 0.2]))
+    else:
+        grid = CartGrid.centered(11, 9, 13, 0.7, center=(0.2, -0.3, 0.1))
     geom = ScanGeometry(300.0, 150.0, 40, 36, 0.25, (19.5, 17.5), P.full_turn_angles(6))
     mu = torch.as_tensor(rng.random(grid.shape, dtype=np.float32), device="cuda")
     table = D.upload_f64(D.ray_view_table(grid, geom, range(6)))
-    g = D.cyl_grid_c(grid)
+    g = D.grid_c(grid)
     s = D.sampling_c(RaySamplingConfig().step_for(grid), 1, False)
     b = D.batch_c(6, geom.det_rows, geom.det_cols)
-    gather = torch.empty(grid.n_voxels * 8, device="cuda")
-    N.call("ct_pack_gather_cyl", D.ptr(mu), C.byref(g), D.ptr(gather), D.stream_handle())
+    gather = D.alloc_gather(grid, "cuda")
+    N.call(f"ct_pack_gather_{kind}", D.ptr(mu), C.byref(g), D.ptr(gather), D.stream_handle())
     outs = []
     for gp in (None, gather):
         p = torch.empty((6, geom.det_rows, geom.det_cols), device="cuda")
-        N.call("ct_fp_cyl", D.ptr(mu), D.ptr(gp), C.byref(g), D.ptr(table), C.byref(b),
+        N.call(f"ct_fp_{kind}", D.ptr(mu), D.ptr(gp), C.byref(g), D.ptr(table), C.byref(b),
                C.byref(s), D.ptr(p), None, D.stream_handle())
         outs.append(p)
+    assert outs[0].abs().max() > 0
     assert torch.equal(outs[0], outs[1])
