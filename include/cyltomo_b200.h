@@ -199,12 +199,13 @@ int ct_sart_update(const float *num, const float *den, int64_t offset, int64_t c
                    const ct_update *upd, ct_stream_t stream);
 
 /* ---- gather layout for the forward projector ------------------------------ */
-/* Number of floats of the gather buffer: 8 per cell, cells (n_h+1, n_theta,
+/* Number of floats of the gather buffer: 8 per cell, cells (n_h+1, n_theta+1,
  * n_r+1) for a cylindrical grid, (n_z+1, n_y+1, n_x+1) for a Cartesian one. */
 int64_t ct_gather_floats_cyl(const ct_cyl_grid *grid);
 int64_t ct_gather_floats_cart(const ct_cart_grid *grid);
 /* Cell (kc, j, ic) holds the trilinear corner (k, j, i) = (kc-1, j, ic-1) with a
- * one-cell halo at index -1 (duplicating index 0): v00, d00, v01, d01, then the
+ * one-cell halo at index -1 (r/h: a copy of index 0; theta: the wrapped row
+ * n_theta-1): v00, d00, v01, d01, then the
  * same at k+1, where vXY = mu(k+X, j+Y, i) and dXY = mu(k+X, j+Y, i+1) - vXY
  * (r/h clamp to the grid, theta wraps; Cartesian: y plays theta's role and all
  * three axes clamp).  16-byte aligned. */

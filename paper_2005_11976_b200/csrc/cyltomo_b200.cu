@@ -98,7 +98,9 @@ __device__ __forceinline__ float sqrt_approx(float x) {
 }
 
 // theta = atan2(y, x) mapped to [0, 2pi) as the reference does (_kernels.py:287-289):
-// octant reduction + a degree-15 odd minimax polynomial (|err| < 4e-8 rad).
+// octant reduction + a degree-13 odd minimax polynomial (|err| < 3.3e-7 rad in
+// fp32, i.e. < 6e-5 of a theta cell at n_theta = 1024 -- the same size as the
+// fp32 resolution of the theta index itself).
 __device__ __forceinline__ float theta_2pi(float y, float x) {
   const float ax = fabsf(x), ay = fabsf(y);
   const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
@@ -106,14 +108,13 @@ __device__ __forceinline__ float theta_2pi(float y, float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(fmaxf(mx, 1e-30f)));
   const float a = mn * rc;   // in [0, 1]; 0 on the axis (atan2(0, 0) = 0)
   const float s = a * a;
-  float p = -0.004056010747295693f;
-  p = fmaf(p, s, 0.021868032862667357f);
-  p = fmaf(p, s, -0.05591941387629666f);
-  p = fmaf(p, s, 0.09642697029858746f);
-  p = fmaf(p, s, -0.1390881621254663f);
-  p = fmaf(p, s, 0.19946600950804824f);
-  p = fmaf(p, s, -0.33329863673815296f);
-  p = fmaf(p, s, 0.9999993362453462f);
+  float p = 0.0068140108452664225f;
+  p = fmaf(p, s, -0.033610868703448114f);
+  p = fmaf(p, s, 0.07963126616806604f);
+  p = fmaf(p, s, -0.13233753525313302f);
+  p = fmaf(p, s, 0.19807922265216282f);
+  p = fmaf(p, s, -0.3331737967047227f);
+  p = fmaf(p, s, 0.999996115058577f);
   float t = a * p;
   t = (ay > ax) ? (1.57079632679489662f - t) : t;
   t = (x < 0.0f) ? (3.14159265358979324f - t) : t;
@@ -170,7 +171,7 @@ struct CylGeo {
   double radius, half_h;
   // fp32 sampling constants
   float inv_dr, inv_dth, inv_dh, h_off, h_off1, nr_m1, nh_m1;
-  unsigned cell_kstride, cell_jstride, idx_bias;   // gather layout (nh+1, nt, nr+1)
+  unsigned cell_kstride, cell_jstride, idx_bias;   // gather layout (nh+1, nt+1, nr+1)
 
   __host__ void init(const float* m, const float* gather, const ct_cyl_grid& g) {
     mu = m;
@@ -187,8 +188,8 @@ struct CylGeo {
     h_off1 = h_off + 1.0f;
     const unsigned B = 0x4B000000u;
     cell_jstride = (unsigned)g.n_r + 1u;
-    cell_kstride = (unsigned)g.n_theta * cell_jstride;
-    idx_bias = 0u - (B * cell_kstride + (B + 1u) * cell_jstride + B);   // mod 2^32
+    cell_kstride = ((unsigned)g.n_theta + 1u) * cell_jstride;
+    idx_bias = 0u - B * (cell_kstride + cell_jstride + 1u);            // mod 2^32
   }
 
   // _kernels.py:170-204 (same operation order)
@@ -254,9 +255,8 @@ struct CylGeo {
     wr = fr1 - (tr - 8388608.0f);
     wh = fh1 - (th_ - 8388608.0f);
     wt = ft1 - (tt - 8388608.0f);
-    unsigned gb = __float_as_uint(tt);            // (j0 + 1) + 0x4B000000, j0 = -1 wraps
-    gb = (gb == 0x4B000000u) ? gb + (unsigned)nt : gb;
-    return (int)(__float_as_uint(th_) * cell_kstride + gb * cell_jstride +
+    // theta cell row jc = j0 + 1 in [0, nt]; row 0 is the wrapped j0 = -1
+    return (int)(__float_as_uint(th_) * cell_kstride + __float_as_uint(tt) * cell_jstride +
                  __float_as_uint(tr) + idx_bias);
   }
 
@@ -1084,15 +1084,16 @@ __global__ void resample_cyl_kernel(const float* __restrict__ src_mu, ct_cyl_gri
 // ---------------------------------------------------------------------------
 __global__ void pack_gather_cyl_kernel(const float* __restrict__ mu, int nh, int nt, int nr,
                                        float4* __restrict__ oct) {
-  // cells (kc, j, ic), kc in [0, nh], ic in [0, nr]: corner (kc-1, j, ic-1)
-  const int64_t n = (int64_t)(nh + 1) * nt * (nr + 1);
+  // cells (kc, jc, ic), kc in [0, nh], jc in [0, nt], ic in [0, nr]: corner
+  // (kc-1, jc-1, ic-1); index -1 is a halo (r/h: copy of 0; theta: row nt-1)
+  const int64_t n = (int64_t)(nh + 1) * (nt + 1) * (nr + 1);
   const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= n) return;
-  const int ic = (int)(m % (nr + 1)), j = (int)((m / (nr + 1)) % nt);
-  const int kc = (int)(m / ((int64_t)(nr + 1) * nt));
+  const int ic = (int)(m % (nr + 1)), jc = (int)((m / (nr + 1)) % (nt + 1));
+  const int kc = (int)(m / ((int64_t)(nr + 1) * (nt + 1)));
   const int i = max(ic - 1, 0), i1 = min(ic, nr - 1);
   const int k = max(kc - 1, 0), k1 = min(kc, nh - 1);
-  const int j1 = (j + 1 == nt) ? 0 : j + 1;
+  const int j = (jc == 0) ? nt - 1 : jc - 1, j1 = (jc == nt) ? 0 : jc;
   auto M = [&](int kk, int jj, int ii) { return __ldg(mu + ((int64_t)kk * nt + jj) * nr + ii); };
   const float v00 = M(k, j, i), v01 = M(k, j1, i), v10 = M(k1, j, i), v11 = M(k1, j1, i);
   oct[2 * m] = make_float4(v00, M(k, j, i1) - v00, v01, M(k, j1, i1) - v01);
@@ -1117,7 +1118,7 @@ __global__ void pack_gather_cart_kernel(const float* __restrict__ mu, int nz, in
 }
 
 int64_t gather_cells_cyl(const ct_cyl_grid& g) {
-  return (int64_t)(g.n_h + 1) * g.n_theta * (g.n_r + 1);
+  return (int64_t)(g.n_h + 1) * (g.n_theta + 1) * (g.n_r + 1);
 }
 int64_t gather_cells_cart(const ct_cart_grid& g) {
   return (int64_t)(g.n_z + 1) * (g.n_y + 1) * (g.n_x + 1);
