@@ -434,7 +434,7 @@ struct CartGeo {
 // ---------------------------------------------------------------------------
 enum FpEpi { EPI_PROJECT = 0, EPI_CORR = 1, EPI_RESID = 2, EPI_ROWMAX = 3 };
 
-constexpr int FP_TILE_W = 16, FP_TILE_H = 8, FP_THREADS = 128;
+constexpr int FP_THREADS = 128;
 #ifndef CT_FP_MIN_BLOCKS
 #define CT_FP_MIN_BLOCKS 9
 #endif
@@ -446,6 +446,7 @@ struct FpArgs {
   const ct_ray_view* __restrict__ views;
   const int32_t* __restrict__ view_ids;
   int rows, cols, ss;
+  int lanes;            // K lanes per ray (lanes_for(rows, cols))
   double step;
   const float* __restrict__ p_meas;
   const double* __restrict__ row_thr;
@@ -454,11 +455,28 @@ struct FpArgs {
   double* __restrict__ red;  // residual partials / per-view max_row
 };
 
-// One sub-ray: returns the in-support sample count; adds the fp32 sum of
-// interpolated values into acc (skipped for COUNT_ONLY).
+// Lanes per ray.  Small detectors cannot fill 148 SMs with one thread per
+// ray, so each ray's samples are split into K contiguous chunks on K adjacent
+// lanes and summed with a fixed shuffle tree.  K is a function of the detector
+// size only, so every FP mode (projection, correction, residual; one view or a
+// batch) produces identical bits for the same ray.
+__host__ __device__ inline int lanes_for(int rows, int cols) {
+#ifdef CT_FORCE_LANES
+  return CT_FORCE_LANES;
+#endif
+  const long long px = (long long)rows * cols;
+  return px >= 131072 ? 1 : px >= 65536 ? 2 : px >= 32768 ? 4 : 8;
+}
+// warp pixel patch: K=1 8x4, K=2 4x4, K=4 4x2, K=8 2x2; block = 2x2 warps
+__host__ __device__ inline int tile_ww(int K) { return K == 1 ? 8 : (K == 8 ? 2 : 4); }
+__host__ __device__ inline int tile_wh(int K) { return (32 / K) / tile_ww(K); }
+
+// One sub-ray, chunk `chunk` of `K`: returns this chunk's in-support sample
+// count and adds the fp32 sum of its interpolated values into acc (COUNT_ONLY:
+// chunk 0 returns the whole ray's count, without marching).
 template <class Geo, bool NEAREST, bool OCT, bool COUNT_ONLY>
 __device__ __forceinline__ int march(const Geo& geo, const ct_ray_view& v, double cu, double cv,
-                                     double step, float& acc) {
+                                     double step, float& acc, int chunk, int K) {
   double d[3];
   subray_dir(v, cu, cv, d);
   double t0, t1;
@@ -467,7 +485,7 @@ __device__ __forceinline__ int march(const Geo& geo, const ct_ray_view& v, doubl
   const int n = (int)ceil(ddiv(dsub(t1, t0), step));
   const double t_last = dadd(t0, dmul((double)(n - 1) + 0.5, step));
   const bool last_in = geo.inside(v.src, d, t_last);
-  if (COUNT_ONLY) return n - 1 + (last_in ? 1 : 0);
+  if (COUNT_ONLY) return chunk == 0 ? n - 1 + (last_in ? 1 : 0) : 0;
   // fp32 march relative to the first sample position
   const double ts = dadd(t0, dmul(0.5, step));
   const float ex = (float)(v.src[0] + ts * d[0]);
@@ -477,8 +495,11 @@ __device__ __forceinline__ int march(const Geo& geo, const ct_ray_view& v, doubl
   const float iy = (float)(step * d[1]);
   const float iz = (float)(step * d[2]);
   const int n_int = n - 1;
+  // interior samples [k, k_end) of this chunk; the last sample goes to chunk K-1
+  int k = (chunk * n_int) / K;
+  const int k_end = ((chunk + 1) * n_int) / K;
+  const bool own_last = chunk == K - 1;
   float sum = 0.0f;
-  int k = 0;
   if (OCT && !NEAREST) {
     // Consecutive samples are half a voxel apart: when a sample falls in the
     // same trilinear cell as its predecessor the two 16-byte loads are skipped
@@ -500,7 +521,7 @@ __device__ __forceinline__ int march(const Geo& geo, const ct_ray_view& v, doubl
       return lerp8d(pa, pb, w0, w1, w2);
     };
 #pragma unroll 1
-    for (; k + 4 <= n_int; k += 4) {
+    for (; k + 4 <= k_end; k += 4) {
       const float k0 = (float)k;
       const float s0 = cell_sample(k0);
       const float s1 = cell_sample(k0 + 1.0f);
@@ -508,9 +529,9 @@ __device__ __forceinline__ int march(const Geo& geo, const ct_ray_view& v, doubl
       const float s3 = cell_sample(k0 + 3.0f);
       sum += (s0 + s1) + (s2 + s3);
     }
-    for (; k < n_int; ++k) sum += cell_sample((float)k);
+    for (; k < k_end; ++k) sum += cell_sample((float)k);
   }
-  for (; k + 4 <= n_int; k += 4) {
+  for (; k + 4 <= k_end; k += 4) {
     const float k0 = (float)k;
     float s0 = geo.template sample<NEAREST, OCT>(fmaf(k0, ix, ex), fmaf(k0, iy, ey), fmaf(k0, iz, ez));
     float s1 = geo.template sample<NEAREST, OCT>(fmaf(k0 + 1.f, ix, ex), fmaf(k0 + 1.f, iy, ey),
@@ -521,16 +542,16 @@ __device__ __forceinline__ int march(const Geo& geo, const ct_ray_view& v, doubl
                                             fmaf(k0 + 3.f, iz, ez));
     sum += (s0 + s1) + (s2 + s3);
   }
-  for (; k < n_int; ++k) {
+  for (; k < k_end; ++k) {
     const float kf = (float)k;
     sum += geo.template sample<NEAREST, OCT>(fmaf(kf, ix, ex), fmaf(kf, iy, ey), fmaf(kf, iz, ez));
   }
-  if (last_in && geo.interp_nonzero(v.src, d, t_last)) {
+  if (own_last && last_in && geo.interp_nonzero(v.src, d, t_last)) {
     const float kf = (float)n_int;
     sum += geo.template sample<NEAREST, OCT>(fmaf(kf, ix, ex), fmaf(kf, iy, ey), fmaf(kf, iz, ez));
   }
   acc += sum;
-  return n_int + (last_in ? 1 : 0);
+  return (k_end - (chunk * n_int) / K) + ((own_last && last_in) ? 1 : 0);
 }
 
 __device__ __forceinline__ double warp_sum(double x) {
@@ -547,9 +568,13 @@ __device__ __forceinline__ double warp_max(double x) {
 template <class Geo, int EPI, bool NEAREST, bool OCT>
 __global__ void __launch_bounds__(FP_THREADS, FP_MIN_BLOCKS) fp_kernel(const FpArgs<Geo> a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // each warp covers an 8x4 pixel patch; the block a 16x8 tile
-  const int col = blockIdx.x * FP_TILE_W + (warp & 1) * 8 + (lane & 7);
-  const int row = blockIdx.z * FP_TILE_H + (warp >> 1) * 4 + (lane >> 3);
+  const int K = a.lanes;
+  const int ww = tile_ww(K), wh = tile_wh(K);
+  const int chunk = lane & (K - 1);
+  const int rslot = lane / K;
+  // each warp covers a ww x wh pixel patch, the block 2x2 warps
+  const int col = blockIdx.x * (2 * ww) + (warp & 1) * ww + rslot % ww;
+  const int row = blockIdx.z * (2 * wh) + (warp >> 1) * wh + rslot / ww;
   const int b = blockIdx.y;
   const int vid = a.view_ids ? a.view_ids[b] : b;
   const bool active = row < a.rows && col < a.cols;
@@ -563,7 +588,7 @@ __global__ void __launch_bounds__(FP_THREADS, FP_MIN_BLOCKS) fp_kernel(const FpA
     // basis is dead after the per-ray setup, keeping the march loop's
     // register footprint small
     count = march<Geo, NEAREST, OCT, EPI == EPI_ROWMAX>(a.geo, a.views[vid], (double)col,
-                                                       (double)row, a.step, acc);
+                                                       (double)row, a.step, acc, chunk, K);
   } else if (active) {
     const ct_ray_view& v = a.views[vid];
     const int ss = a.ss;
@@ -572,22 +597,30 @@ __global__ void __launch_bounds__(FP_THREADS, FP_MIN_BLOCKS) fp_kernel(const FpA
       for (int su = 0; su < ss; ++su) {
         const double off_u = dsub(ddiv((double)su + 0.5, (double)ss), 0.5);
         count += march<Geo, NEAREST, OCT, EPI == EPI_ROWMAX>(
-            a.geo, v, dadd((double)col, off_u), dadd((double)row, off_v), a.step, acc);
+            a.geo, v, dadd((double)col, off_u), dadd((double)row, off_v), a.step, acc, chunk, K);
       }
     }
   }
+  if (K > 1) {
+    // fixed-order tree over the K chunks of a ray (lanes of a ray are adjacent)
+    for (int o = 1; o < K; o <<= 1) {
+      acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      count += __shfl_xor_sync(0xffffffffu, count, o);
+    }
+  }
+  const bool lead = chunk == 0;   // writes the ray's outputs
   const double inv_ss2 = ddiv(1.0, (double)(a.ss * a.ss));
   // out_w = wacc * step * inv_ss2, out_p = acc * step * inv_ss2 (_kernels.py:292-293)
   const double w64 = dmul(dmul((double)count, a.step), inv_ss2);
   const double p64 = (double)acc * a.step * inv_ss2;
 
   if (EPI == EPI_PROJECT) {
-    if (active) {
+    if (active && lead) {
       a.out0[(size_t)b * npix + pix] = (float)p64;
       if (a.out1) a.out1[(size_t)b * npix + pix] = (float)w64;
     }
   } else if (EPI == EPI_CORR) {
-    if (active) {
+    if (active && lead) {
       float c = 0.0f;
       if (w64 > a.row_thr[vid]) {
         const float pm = a.p_meas[(size_t)vid * npix + pix];
@@ -597,7 +630,7 @@ __global__ void __launch_bounds__(FP_THREADS, FP_MIN_BLOCKS) fp_kernel(const FpA
     }
   } else {
     double x = 0.0;
-    if (active) {
+    if (active && lead) {
       if (EPI == EPI_RESID) {
         // compare with the fp32 simulation, i.e. what a stored projection of
         // this volume holds: consistent data gives exactly 0, as in the reference
@@ -644,14 +677,15 @@ __global__ void __launch_bounds__(1024) sum_partials_kernel(const double* __rest
 }
 
 dim3 fp_grid(const ct_batch& b) {
-  return dim3((b.det_cols + FP_TILE_W - 1) / FP_TILE_W, b.n_batch,
-              (b.det_rows + FP_TILE_H - 1) / FP_TILE_H);
+  const int K = lanes_for(b.det_rows, b.det_cols);
+  const int tw = 2 * tile_ww(K), th = 2 * tile_wh(K);
+  return dim3((b.det_cols + tw - 1) / tw, b.n_batch, (b.det_rows + th - 1) / th);
 }
 
 int check_batch(const ct_batch* b, const void* views, const ct_sampling* s) {
   if (!b || !views || !s) return set_err(CT_ERR_ARG, "null batch/views/sampling");
   if (b->n_batch < 1 || b->n_batch > 65535 || b->det_rows < 1 || b->det_cols < 1 ||
-      (b->det_rows + FP_TILE_H - 1) / FP_TILE_H > 65535)
+      fp_grid(*b).z > 65535)
     return set_err(CT_ERR_ARG, "bad batch dimensions");
   if (!(s->step > 0.0) || s->supersample < 1) return set_err(CT_ERR_ARG, "bad sampling");
   return CT_OK;
@@ -683,6 +717,7 @@ int launch_fp(const Geo& geo, const ct_ray_view* views, const ct_batch& b, const
   a.rows = b.det_rows;
   a.cols = b.det_cols;
   a.ss = s.supersample;
+  a.lanes = lanes_for(b.det_rows, b.det_cols);
   a.step = s.step;
   a.p_meas = p_meas;
   a.row_thr = thr;

@@ -362,9 +362,18 @@ class SartRun:
             torch = D.torch_mod()
             g = self._graphs.get(want)
             if g is None:
+                # low-level capture on a side stream: torch.cuda.graph() would
+                # also gc.collect() and empty the caching allocator every time
                 g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g):
-                    self._pass_body(want)
+                side = torch.cuda.Stream(self.eng.device)
+                side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(side):
+                    g.capture_begin()
+                    try:
+                        self._pass_body(want)
+                    finally:
+                        g.capture_end()
+                torch.cuda.current_stream().wait_stream(side)
                 self._graphs[want] = g
             g.replay()
         else:

@@ -40,3 +40,7 @@ for rep in range(2):
     mu = t("D2H mu", lambda: D.to_host(run.mu))
     t("CylVolume(host mu) check", lambda: P.CylVolume(wl.grid, mu))
     t("sart_run total", lambda: P.sart_run(ps, wl.grid, cfg))
+
+vol = None
+for rep in range(4):
+    vol = t(f"sart_run (previous result alive) #{rep}", lambda: P.sart_run(ps, wl.grid, cfg))
