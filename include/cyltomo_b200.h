@@ -214,6 +214,14 @@ int ct_pack_gather_cyl(const float *mu, const ct_cyl_grid *grid, float *gather,
 int ct_pack_gather_cart(const float *mu, const ct_cart_grid *grid, float *gather,
                         ct_stream_t stream);
 
+/* ---- input conversion (cyltomo/projector.py:169-181) ---------------------- */
+/* out[i] = -ln(intensity[i] / I0) with I0 = flat[i % npix] (flat != NULL, one
+ * image broadcast over the views) or flat_scalar.  Computed in fp64 from the
+ * fp32 inputs.  If any I <= 0 or I0 <= 0, *bad (device int, caller-zeroed) is
+ * set to 1 (the reference raises NonPositiveIntensity). */
+int ct_line_integrals(const float *intensity, int64_t n, int64_t npix, const float *flat,
+                      double flat_scalar, float *out, int *bad, ct_stream_t stream);
+
 /* ---- point sampling (cyltomo/_kernels.py:154-163, grid.py:261-319) ------- */
 int ct_sample_cyl(const float *mu, const ct_cyl_grid *grid, const double *rs,
                   const double *ths, const double *hs, int64_t n, int nearest,

@@ -95,6 +95,7 @@ _SIGNATURES = {
                                     C.POINTER(UpdateC), P]),
     "ct_cyl_trig": (C.c_int, [C.POINTER(CylGridC), P, P]),
     "ct_sart_update": (C.c_int, [P, P, C.c_int64, C.c_int64, C.POINTER(UpdateC), P]),
+    "ct_line_integrals": (C.c_int, [P, C.c_int64, C.c_int64, P, C.c_double, P, P, P]),
     "ct_sample_cyl": (C.c_int, [P, C.POINTER(CylGridC), P, P, P, C.c_int64, C.c_int, P, P]),
     "ct_sample_cart": (C.c_int, [P, C.POINTER(CartGridC), P, P, P, C.c_int64, C.c_int,
                                  P, P]),

@@ -1159,6 +1159,24 @@ int64_t gather_cells_cart(const ct_cart_grid& g) {
   return (int64_t)(g.n_z + 1) * (g.n_y + 1) * (g.n_x + 1);
 }
 
+// Beer-Lambert p = -ln(I / I0) (cyltomo/projector.py:169-181), fp64 log of the
+// fp32 inputs; flat field is a scalar or one image broadcast over the views.
+// Any I <= 0 or I0 <= 0 sets *bad (the caller raises NonPositiveIntensity).
+__global__ void line_integral_kernel(const float* __restrict__ in, int64_t n, int64_t npix,
+                                     const float* __restrict__ flat, double flat_scalar,
+                                     float* __restrict__ out, int* bad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double I = in[i];
+  const double I0 = flat ? (double)flat[i % npix] : flat_scalar;
+  if (!(I > 0.0) || !(I0 > 0.0)) {
+    atomicOr(bad, 1);
+    out[i] = 0.0f;
+    return;
+  }
+  out[i] = (float)(-log(I / I0));
+}
+
 unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
@@ -1392,6 +1410,16 @@ int ct_resample_cyl_to_cyl(const float* src_mu, const ct_cyl_grid* src, const ct
   resample_cyl_kernel<<<blocks_for(n, 256), 256, 0, CT_STREAM(stream)>>>(src_mu, *src, *dst,
                                                                          nearest, dst_mu);
   return check_launch("resample_cyl_kernel");
+}
+
+int ct_line_integrals(const float* intensity, int64_t n, int64_t npix, const float* flat,
+                      double flat_scalar, float* out, int* bad, ct_stream_t stream) {
+  if (!intensity || !out || !bad || n < 0 || npix < 1)
+    return set_err(CT_ERR_ARG, "bad line-integral arguments");
+  if (n == 0) return CT_OK;
+  line_integral_kernel<<<blocks_for(n, 256), 256, 0, CT_STREAM(stream)>>>(
+      intensity, n, npix, flat, flat_scalar, out, bad);
+  return check_launch("line_integral_kernel");
 }
 
 int64_t ct_gather_floats_cyl(const ct_cyl_grid* grid) {

@@ -195,18 +195,31 @@ def back_project(correction, geom: ScanGeometry, i: int, grid, out=None):
 
 
 def intensities_to_line_integrals(ps: ProjectionSet, i0) -> ProjectionSet:
-    """Beer-Lambert p = -ln(I / I0) (``cyltomo/projector.py:169-181``)."""
+    """Beer-Lambert p = -ln(I / I0) (``cyltomo/projector.py:169-181``), as the
+    ``ct_line_integrals`` kernel.  i0 is a scalar or an (H, W) flat field
+    broadcast over all views; raises NonPositiveIntensity if any I or I0 <= 0."""
+    torch = D.torch_mod()
     i0 = np.asarray(i0, dtype=np.float64)
     if np.any(i0 <= 0.0):
         raise NonPositiveIntensity("flat field contains values <= 0")
-    torch = D.torch_mod()
     dev = D.require_cuda()
     img = D.to_device(ps.images, device=dev)
-    if bool((img <= 0).any()):
+    H, W = ps.geom.det_rows, ps.geom.det_cols
+    flat = None
+    scalar = 1.0
+    if i0.ndim == 0:
+        scalar = float(i0)
+    else:
+        if i0.shape != (H, W):
+            raise ValueError("flat field must be a scalar or an (H, W) image")
+        flat = D.to_device(i0.astype(np.float32), device=dev)
+    out = torch.empty_like(img)
+    bad = torch.zeros(1, dtype=torch.int32, device=dev)
+    N.call("ct_line_integrals", D.ptr(img), img.numel(), H * W, D.ptr(flat), scalar,
+           D.ptr(out), D.ptr(bad), D.stream_handle())
+    if int(bad.item()):
         raise NonPositiveIntensity("intensity images contain values <= 0")
-    i0t = torch.as_tensor(i0, device=dev)
-    p = (-torch.log(img.to(torch.float64) / i0t)).to(torch.float32)
-    return ProjectionSet(ps.geom, p if ps.on_device else D.to_host(p), LINE_INTEGRAL)
+    return ProjectionSet(ps.geom, out if ps.on_device else D.to_host(out), LINE_INTEGRAL)
 
 
 def simulate_scan(vol, geom: ScanGeometry, sampling: RaySamplingConfig | None = None,

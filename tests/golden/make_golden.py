@@ -236,10 +236,32 @@ def c2_cases():
     return g
 
 
+def io_cases():
+    """Artifacts written by the reference's own writers (cyltomo/io.py), read
+    back by tests/test_io.py: volume (cyl + cart), projections, geometry, pose."""
+    import cyltomo.io as rio
+    d = OUT / "io_ref"
+    d.mkdir(exist_ok=True)
+    rng = np.random.default_rng(99)
+    pose = ref.Pose(0.3, 0.2, -0.4, t=[0.5, -0.3, 1.0])
+    cg = ref.CylGrid(3, 5, 4, 2.0, 3.0, pose)
+    rio.write_volume(ref.CylVolume(cg, f32(rng.random(cg.shape))), d / "cylvol")
+    xg = ref.CartGrid.centered(4, 3, 2, 0.5, center=(0.1, 0.2, 0.3))
+    rio.write_volume(ref.CartVolume(xg, f32(rng.random(xg.shape))), d / "cartvol")
+    geom = desk_geometry()
+    imgs = f32(rng.random((geom.n_proj, geom.det_rows, geom.det_cols)))
+    rio.write_projections(ref.ProjectionSet(geom, imgs), d / "proj")
+    rio.write_geometry(geom, d / "geom.json")
+    rio.write_pose(pose, d / "pose.json")
+    return {"io_cyl_mu": np.fromfile(d / "cylvol.raw", dtype="<f4"),
+            "io_proj_sum": np.asarray([imgs.sum()])}
+
+
 def main():
     t = time.time()
     groups = {"golden_small.npz": small_cases, "golden_sart.npz": sart_cases,
-              "golden_c1.npz": c1_cases, "golden_c2.npz": c2_cases}
+              "golden_c1.npz": c1_cases, "golden_c2.npz": c2_cases,
+              "golden_io.npz": io_cases}
     only = set(sys.argv[1:])
     for fname, fn in groups.items():
         if only and fname not in only:
