@@ -161,6 +161,67 @@ __device__ __forceinline__ float lerp8(float4 a, float4 b, float wr, float wt, f
 }
 
 // ---------------------------------------------------------------------------
+// packed fp32x2 arithmetic (sm_100 FFMA2 / FADD2 / FMUL2): two samples per
+// instruction for the per-sample coordinate / index / weight math.  Each lane
+// of an f32x2 op is the IEEE op of the scalar code, and both the gather and
+// the plain path use the same paired code for the same samples, so their
+// results are bit-identical.
+// ---------------------------------------------------------------------------
+typedef unsigned long long f32x2;
+
+__device__ __forceinline__ f32x2 pk(float a, float b) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk(f32x2 v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 add2_rd(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 dup2(float a) { return pk(a, a); }
+
+// Per-ray march constants, splatted for the paired path
+struct RayF {
+  float ex, ey, ez, ix, iy, iz;
+  f32x2 EX, EY, EZ, IX, IY, IZ;
+};
+
+// One sample's trilinear cell: bit patterns of floor(index + 1) (+0x4B000000,
+// the "+1" being the gather layout's halo offset) and the three weights.
+struct Cell {
+  unsigned ib, jb, kb;
+  float w0, w1, w2;
+};
+
+constexpr unsigned kMagicBits = 0x4B000000u;   // bits of 2^23
+
+// octant fixups of theta_2pi, shared by the scalar and the paired code
+__device__ __forceinline__ float theta_fix(float t, float x, float y, bool y_major) {
+  t = y_major ? (1.57079632679489662f - t) : t;
+  t = (x < 0.0f) ? (3.14159265358979324f - t) : t;
+  return (y < 0.0f) ? (kTwoPiF - t) : t;
+}
+
+// ---------------------------------------------------------------------------
 // grid policies: support interval (fp64), last-sample test (fp64) and the
 // fp32 trilinear sample
 // ---------------------------------------------------------------------------
@@ -186,7 +247,7 @@ struct CylGeo {
     nr_m1 = (float)(g.n_r - 1);
     nh_m1 = (float)(g.n_h - 1);
     h_off1 = h_off + 1.0f;
-    const unsigned B = 0x4B000000u;
+    const unsigned B = kMagicBits;
     cell_jstride = (unsigned)g.n_r + 1u;
     cell_kstride = ((unsigned)g.n_theta + 1u) * cell_jstride;
     idx_bias = 0u - B * (cell_kstride + cell_jstride + 1u);            // mod 2^32
@@ -236,14 +297,11 @@ struct CylGeo {
     return true;
   }
 
-  // Gather-layout cell of a point and its trilinear weights.  The layout has a
-  // one-cell halo at r/h index -1 (duplicating index 0, r-difference 0), so no
-  // clamps are needed: at a clamped position the reference's weight is 0 and
-  // here the weight multiplies an exact 0 -- same value.  floor() via
-  // x + 2^23 rounded toward -inf (bits = floor(x) + 0x4B000000); the offsets
-  // fold into idx_bias (modular uint32 arithmetic).
-  __device__ __forceinline__ int locate(float x, float y, float z, float& wr, float& wt,
-                                        float& wh) const {
+  // Trilinear cell of a point.  The gather layout has a one-cell halo at
+  // r/h/theta index -1, so no clamps are needed: where the reference clamps,
+  // the halo's r/h difference is an exact 0 (theta: the wrapped row).
+  // floor() via x + 2^23 rounded toward -inf (bits = floor(x) + 0x4B000000).
+  __device__ __forceinline__ Cell locate(float x, float y, float z) const {
     const float r = sqrt_approx(fmaf(x, x, y * y));
     const float th = theta_2pi(y, x);
     const float fr1 = fmaf(r, inv_dr, 0.5f);      // r index + 1 (halo), >= 0.5
@@ -252,56 +310,91 @@ struct CylGeo {
     const float tr = __fadd_rd(fr1, 8388608.0f);
     const float th_ = __fadd_rd(fh1, 8388608.0f);
     const float tt = __fadd_rd(ft1, 8388608.0f);
-    wr = fr1 - (tr - 8388608.0f);
-    wh = fh1 - (th_ - 8388608.0f);
-    wt = ft1 - (tt - 8388608.0f);
-    // theta cell row jc = j0 + 1 in [0, nt]; row 0 is the wrapped j0 = -1
-    return (int)(__float_as_uint(th_) * cell_kstride + __float_as_uint(tt) * cell_jstride +
-                 __float_as_uint(tr) + idx_bias);
+    Cell c;
+    c.w0 = fr1 - (tr - 8388608.0f);
+    c.w1 = ft1 - (tt - 8388608.0f);
+    c.w2 = fh1 - (th_ - 8388608.0f);
+    c.ib = __float_as_uint(tr);
+    c.jb = __float_as_uint(tt);
+    c.kb = __float_as_uint(th_);
+    return c;
   }
 
-  template <bool NEAREST, bool OCT>
-  __device__ __forceinline__ float sample(float x, float y, float z) const {
-    if (OCT && !NEAREST) {
-      float wr, wt, wh;
-      const int idx = locate(x, y, z, wr, wt, wh);
-      float4 a, b;
-      ld_cell(oct + 2 * (size_t)(unsigned)idx, a, b);
-      return lerp8d(a, b, wr, wt, wh);
-    }
+  // the same for samples k0, k0+1 of a ray, two per f32x2 instruction
+  __device__ __forceinline__ void locate2(float k0, const RayF& ry, Cell& ca, Cell& cb) const {
+    const f32x2 K = pk(k0, k0 + 1.0f);
+    const f32x2 X = fma2(K, ry.IX, ry.EX), Y = fma2(K, ry.IY, ry.EY), Z = fma2(K, ry.IZ, ry.EZ);
+    const f32x2 R2 = fma2(X, X, mul2(Y, Y));
+    float xa, xb, ya, yb, r2a, r2b;
+    upk(X, xa, xb);
+    upk(Y, ya, yb);
+    upk(R2, r2a, r2b);
+    const float mxa = fmaxf(fabsf(xa), fabsf(ya)), mna = fminf(fabsf(xa), fabsf(ya));
+    const float mxb = fmaxf(fabsf(xb), fabsf(yb)), mnb = fminf(fabsf(xb), fabsf(yb));
+    float rca, rcb;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rca) : "f"(fmaxf(mxa, 1e-30f)));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rcb) : "f"(fmaxf(mxb, 1e-30f)));
+    const f32x2 A = mul2(pk(mna, mnb), pk(rca, rcb));
+    const f32x2 S = mul2(A, A);
+    f32x2 P = fma2(dup2(0.0068140108452664225f), S, dup2(-0.033610868703448114f));
+    P = fma2(P, S, dup2(0.07963126616806604f));
+    P = fma2(P, S, dup2(-0.13233753525313302f));
+    P = fma2(P, S, dup2(0.19807922265216282f));
+    P = fma2(P, S, dup2(-0.3331737967047227f));
+    P = fma2(P, S, dup2(0.999996115058577f));
+    float ta, tb;
+    upk(mul2(A, P), ta, tb);
+    ta = theta_fix(ta, xa, ya, fabsf(ya) > fabsf(xa));
+    tb = theta_fix(tb, xb, yb, fabsf(yb) > fabsf(xb));
+    const f32x2 FT1 = fma2(pk(ta, tb), dup2(inv_dth), dup2(0.5f));
+    const f32x2 FR1 = fma2(pk(sqrt_approx(r2a), sqrt_approx(r2b)), dup2(inv_dr), dup2(0.5f));
+    const f32x2 FH1 = fma2(Z, dup2(inv_dh), dup2(h_off1));
+    const f32x2 BIG = dup2(8388608.0f);
+    const f32x2 TR = add2_rd(FR1, BIG), TT = add2_rd(FT1, BIG), TH = add2_rd(FH1, BIG);
+    const f32x2 WR = sub2(FR1, sub2(TR, BIG)), WT = sub2(FT1, sub2(TT, BIG));
+    const f32x2 WH = sub2(FH1, sub2(TH, BIG));
+    upk(WR, ca.w0, cb.w0);
+    upk(WT, ca.w1, cb.w1);
+    upk(WH, ca.w2, cb.w2);
+    float t0, t1;
+    upk(TR, t0, t1);
+    ca.ib = __float_as_uint(t0); cb.ib = __float_as_uint(t1);
+    upk(TT, t0, t1);
+    ca.jb = __float_as_uint(t0); cb.jb = __float_as_uint(t1);
+    upk(TH, t0, t1);
+    ca.kb = __float_as_uint(t0); cb.kb = __float_as_uint(t1);
+  }
+
+  // gather-layout cell index (modular uint32; one constant for all offsets)
+  __device__ __forceinline__ int gather_index(const Cell& c) const {
+    return (int)(c.kb * cell_kstride + c.jb * cell_jstride + c.ib + idx_bias);
+  }
+
+  // the same 8 values from the plain mu layout (r/h clamp, theta wrap)
+  __device__ __forceinline__ void fetch_plain(const Cell& c, float4& a, float4& b) const {
+    const int i0 = (int)(c.ib - kMagicBits) - 1, g = (int)(c.jb - kMagicBits);
+    const int k0 = (int)(c.kb - kMagicBits) - 1;
+    const int ia = max(i0, 0), ib1 = min(i0 + 1, nr - 1);
+    const int ka = max(k0, 0), kb1 = min(k0 + 1, nh - 1);
+    const int ja = (g == 0) ? nt - 1 : g - 1, jb1 = (g == nt) ? 0 : g;
+    const float* p0 = mu + ((size_t)ka * nt + ja) * nr;
+    const float* p1 = mu + ((size_t)ka * nt + jb1) * nr;
+    const float* p2 = mu + ((size_t)kb1 * nt + ja) * nr;
+    const float* p3 = mu + ((size_t)kb1 * nt + jb1) * nr;
+    a = make_float4(__ldg(p0 + ia), __ldg(p0 + ib1), __ldg(p1 + ia), __ldg(p1 + ib1));
+    b = make_float4(__ldg(p2 + ia), __ldg(p2 + ib1), __ldg(p3 + ia), __ldg(p3 + ib1));
+  }
+
+  __device__ __forceinline__ float sample_nearest(float x, float y, float z) const {
     const float r = sqrt_approx(fmaf(x, x, y * y));
     const float th = theta_2pi(y, x);
-    const float ft1 = fmaf(th, inv_dth, 0.5f);  // theta index + 1, in [0.5, nt + 0.5]
-    if (NEAREST) {
-      const float fr = fminf(fmaxf(fmaf(r, inv_dr, -0.5f), 0.0f), nr_m1);
-      const float fh = fminf(fmaxf(fmaf(z, inv_dh, h_off), 0.0f), nh_m1);
-      int ir = (int)rintf(fr), ih = (int)rintf(fh), it = (int)rintf(ft1 - 1.0f);
-      if (it < 0) it += nt;
-      if (it >= nt) it -= nt;
-      return __ldg(mu + (ih * nt + it) * nr + ir);
-    }
-    // plain layout: same "+1" index formulation as locate(), clamped to
-    // [1, n] (the reference's [0, n-1] clamp), so weights are bit-identical
-    const float fr1 = fminf(fmaxf(fmaf(r, inv_dr, 0.5f), 1.0f), nr_m1 + 1.0f);
-    const float fh1 = fminf(fmaxf(fmaf(z, inv_dh, h_off1), 1.0f), nh_m1 + 1.0f);
-    int i0, k0, g;
-    const float wr = fr1 - floor_pos(fr1, i0);
-    const float wh = fh1 - floor_pos(fh1, k0);
-    const float wt = ft1 - floor_pos(ft1, g);
-    i0 -= 1;
-    k0 -= 1;
-    int j0 = g - 1;
-    j0 = (j0 < 0) ? nt - 1 : j0;
-    const int idx = (k0 * nt + j0) * nr + i0;
-    const int di = (i0 + 1 < nr) ? 1 : 0;
-    const int dj = (j0 + 1 < nt) ? nr : -(nt - 1) * nr;
-    const int dk = (k0 + 1 < nh) ? nt * nr : 0;
-    const float* p = mu + idx;
-    float4 a, b;
-    a.x = __ldg(p); a.y = __ldg(p + di); a.z = __ldg(p + dj); a.w = __ldg(p + dj + di);
-    p += dk;
-    b.x = __ldg(p); b.y = __ldg(p + di); b.z = __ldg(p + dj); b.w = __ldg(p + dj + di);
-    return lerp8(a, b, wr, wt, wh);
+    const float ft1 = fmaf(th, inv_dth, 0.5f);
+    const float fr = fminf(fmaxf(fmaf(r, inv_dr, -0.5f), 0.0f), nr_m1);
+    const float fh = fminf(fmaxf(fmaf(z, inv_dh, h_off), 0.0f), nh_m1);
+    int ir = (int)rintf(fr), ih = (int)rintf(fh), it = (int)rintf(ft1 - 1.0f);
+    if (it < 0) it += nt;
+    if (it >= nt) it -= nt;
+    return __ldg(mu + (ih * nt + it) * nr + ir);
   }
 };
 
@@ -326,7 +419,7 @@ struct CartGeo {
     for (int a = 0; a < 3; ++a) off[a] = (float)(-g.origin[a] / g.voxel_size - 0.5);
     nx_m1 = (float)(nx - 1); ny_m1 = (float)(ny - 1); nz_m1 = (float)(nz - 1);
     for (int a = 0; a < 3; ++a) off1[a] = off[a] + 1.0f;
-    const unsigned B = 0x4B000000u;
+    const unsigned B = kMagicBits;
     cell_jstride = (unsigned)nx + 1u;
     cell_kstride = ((unsigned)ny + 1u) * cell_jstride;
     idx_bias = 0u - B * (cell_kstride + cell_jstride + 1u);          // mod 2^32
@@ -374,58 +467,67 @@ struct CartGeo {
              f[2] < -0.5 || f[2] > nz - 0.5);
   }
 
-  // gather-layout cell (halo at index -1 on all three axes, see CylGeo)
-  __device__ __forceinline__ int locate(float x, float y, float z, float& wx, float& wy,
-                                        float& wz) const {
+  // cell with a halo at index -1 on all three axes (see CylGeo::locate)
+  __device__ __forceinline__ Cell locate(float x, float y, float z) const {
     const float fx1 = fmaf(x, inv_vs, off1[0]);
     const float fy1 = fmaf(y, inv_vs, off1[1]);
     const float fz1 = fmaf(z, inv_vs, off1[2]);
     const float tx = __fadd_rd(fx1, 8388608.0f);
     const float ty = __fadd_rd(fy1, 8388608.0f);
     const float tz = __fadd_rd(fz1, 8388608.0f);
-    wx = fx1 - (tx - 8388608.0f);
-    wy = fy1 - (ty - 8388608.0f);
-    wz = fz1 - (tz - 8388608.0f);
-    return (int)(__float_as_uint(tz) * cell_kstride + __float_as_uint(ty) * cell_jstride +
-                 __float_as_uint(tx) + idx_bias);
+    Cell c;
+    c.w0 = fx1 - (tx - 8388608.0f);
+    c.w1 = fy1 - (ty - 8388608.0f);
+    c.w2 = fz1 - (tz - 8388608.0f);
+    c.ib = __float_as_uint(tx);
+    c.jb = __float_as_uint(ty);
+    c.kb = __float_as_uint(tz);
+    return c;
   }
 
-  template <bool NEAREST, bool OCT>
-  __device__ __forceinline__ float sample(float x, float y, float z) const {
-    if (OCT && !NEAREST) {
-      float wx, wy, wz;
-      const int idx = locate(x, y, z, wx, wy, wz);
-      float4 a, b;
-      ld_cell(oct + 2 * (size_t)(unsigned)idx, a, b);
-      return lerp8d(a, b, wx, wy, wz);
-    }
-    if (NEAREST) {
-      const float fx = fminf(fmaxf(fmaf(x, inv_vs, off[0]), 0.0f), nx_m1);
-      const float fy = fminf(fmaxf(fmaf(y, inv_vs, off[1]), 0.0f), ny_m1);
-      const float fz = fminf(fmaxf(fmaf(z, inv_vs, off[2]), 0.0f), nz_m1);
-      return __ldg(mu + ((int)rintf(fz) * ny + (int)rintf(fy)) * nx + (int)rintf(fx));
-    }
-    // "+1" formulation clamped to [1, n], as locate() (bit-identical weights)
-    const float fx1 = fminf(fmaxf(fmaf(x, inv_vs, off1[0]), 1.0f), nx_m1 + 1.0f);
-    const float fy1 = fminf(fmaxf(fmaf(y, inv_vs, off1[1]), 1.0f), ny_m1 + 1.0f);
-    const float fz1 = fminf(fmaxf(fmaf(z, inv_vs, off1[2]), 1.0f), nz_m1 + 1.0f);
-    int i0, j0, k0;
-    const float wx = fx1 - floor_pos(fx1, i0);
-    const float wy = fy1 - floor_pos(fy1, j0);
-    const float wz = fz1 - floor_pos(fz1, k0);
-    i0 -= 1;
-    j0 -= 1;
-    k0 -= 1;
-    const int idx = (k0 * ny + j0) * nx + i0;
-    const int di = (i0 + 1 < nx) ? 1 : 0;
-    const int dj = (j0 + 1 < ny) ? nx : 0;
-    const int dk = (k0 + 1 < nz) ? ny * nx : 0;
-    const float* p = mu + idx;
-    float4 a, b;
-    a.x = __ldg(p); a.y = __ldg(p + di); a.z = __ldg(p + dj); a.w = __ldg(p + dj + di);
-    p += dk;
-    b.x = __ldg(p); b.y = __ldg(p + di); b.z = __ldg(p + dj); b.w = __ldg(p + dj + di);
-    return lerp8(a, b, wx, wy, wz);
+  __device__ __forceinline__ void locate2(float k0, const RayF& ry, Cell& ca, Cell& cb) const {
+    const f32x2 K = pk(k0, k0 + 1.0f);
+    const f32x2 X = fma2(K, ry.IX, ry.EX), Y = fma2(K, ry.IY, ry.EY), Z = fma2(K, ry.IZ, ry.EZ);
+    const f32x2 IV = dup2(inv_vs);
+    const f32x2 FX = fma2(X, IV, dup2(off1[0])), FY = fma2(Y, IV, dup2(off1[1]));
+    const f32x2 FZ = fma2(Z, IV, dup2(off1[2]));
+    const f32x2 BIG = dup2(8388608.0f);
+    const f32x2 TX = add2_rd(FX, BIG), TY = add2_rd(FY, BIG), TZ = add2_rd(FZ, BIG);
+    upk(sub2(FX, sub2(TX, BIG)), ca.w0, cb.w0);
+    upk(sub2(FY, sub2(TY, BIG)), ca.w1, cb.w1);
+    upk(sub2(FZ, sub2(TZ, BIG)), ca.w2, cb.w2);
+    float t0, t1;
+    upk(TX, t0, t1);
+    ca.ib = __float_as_uint(t0); cb.ib = __float_as_uint(t1);
+    upk(TY, t0, t1);
+    ca.jb = __float_as_uint(t0); cb.jb = __float_as_uint(t1);
+    upk(TZ, t0, t1);
+    ca.kb = __float_as_uint(t0); cb.kb = __float_as_uint(t1);
+  }
+
+  __device__ __forceinline__ int gather_index(const Cell& c) const {
+    return (int)(c.kb * cell_kstride + c.jb * cell_jstride + c.ib + idx_bias);
+  }
+
+  __device__ __forceinline__ void fetch_plain(const Cell& c, float4& a, float4& b) const {
+    const int i0 = (int)(c.ib - kMagicBits) - 1, j0 = (int)(c.jb - kMagicBits) - 1;
+    const int k0 = (int)(c.kb - kMagicBits) - 1;
+    const int ia = max(i0, 0), ib1 = min(i0 + 1, nx - 1);
+    const int ja = max(j0, 0), jb1 = min(j0 + 1, ny - 1);
+    const int ka = max(k0, 0), kb1 = min(k0 + 1, nz - 1);
+    const float* p0 = mu + ((size_t)ka * ny + ja) * nx;
+    const float* p1 = mu + ((size_t)ka * ny + jb1) * nx;
+    const float* p2 = mu + ((size_t)kb1 * ny + ja) * nx;
+    const float* p3 = mu + ((size_t)kb1 * ny + jb1) * nx;
+    a = make_float4(__ldg(p0 + ia), __ldg(p0 + ib1), __ldg(p1 + ia), __ldg(p1 + ib1));
+    b = make_float4(__ldg(p2 + ia), __ldg(p2 + ib1), __ldg(p3 + ia), __ldg(p3 + ib1));
+  }
+
+  __device__ __forceinline__ float sample_nearest(float x, float y, float z) const {
+    const float fx = fminf(fmaxf(fmaf(x, inv_vs, off[0]), 0.0f), nx_m1);
+    const float fy = fminf(fmaxf(fmaf(y, inv_vs, off[1]), 0.0f), ny_m1);
+    const float fz = fminf(fmaxf(fmaf(z, inv_vs, off[2]), 0.0f), nz_m1);
+    return __ldg(mu + ((int)rintf(fz) * ny + (int)rintf(fy)) * nx + (int)rintf(fx));
   }
 };
 
@@ -488,67 +590,83 @@ __device__ __forceinline__ int march(const Geo& geo, const ct_ray_view& v, doubl
   if (COUNT_ONLY) return chunk == 0 ? n - 1 + (last_in ? 1 : 0) : 0;
   // fp32 march relative to the first sample position
   const double ts = dadd(t0, dmul(0.5, step));
-  const float ex = (float)(v.src[0] + ts * d[0]);
-  const float ey = (float)(v.src[1] + ts * d[1]);
-  const float ez = (float)(v.src[2] + ts * d[2]);
-  const float ix = (float)(step * d[0]);
-  const float iy = (float)(step * d[1]);
-  const float iz = (float)(step * d[2]);
+  RayF ry;
+  ry.ex = (float)(v.src[0] + ts * d[0]);
+  ry.ey = (float)(v.src[1] + ts * d[1]);
+  ry.ez = (float)(v.src[2] + ts * d[2]);
+  ry.ix = (float)(step * d[0]);
+  ry.iy = (float)(step * d[1]);
+  ry.iz = (float)(step * d[2]);
   const int n_int = n - 1;
   // interior samples [k, k_end) of this chunk; the last sample goes to chunk K-1
   int k = (chunk * n_int) / K;
   const int k_end = ((chunk + 1) * n_int) / K;
   const bool own_last = chunk == K - 1;
   float sum = 0.0f;
-  if (OCT && !NEAREST) {
-    // Consecutive samples are half a voxel apart: when a sample falls in the
-    // same trilinear cell as its predecessor the two 16-byte loads are skipped
-    // (predicated off) and the cell's values are forwarded in registers.
-    // Same values, same lerp, same summation grouping as the plain path.
-    int prev = -1;
-    float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pb = pa;
-    const float4* __restrict__ oct = geo.oct;
-    // one live cell (pa, pb): the loads are predicated on a cell change and
-    // land in the same registers -- no forwarding copies; resident warps hide
-    // the resulting load->lerp serialisation.
-    auto cell_sample = [&](float kq) -> float {
-      float w0, w1, w2;
-      const int idx = geo.locate(fmaf(kq, ix, ex), fmaf(kq, iy, ey), fmaf(kq, iz, ez), w0, w1, w2);
+  if (NEAREST) {
+    for (; k + 4 <= k_end; k += 4) {
+      float s4[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float kq = (float)(k + q);
+        s4[q] = geo.sample_nearest(fmaf(kq, ry.ix, ry.ex), fmaf(kq, ry.iy, ry.ey),
+                                   fmaf(kq, ry.iz, ry.ez));
+      }
+      sum += (s4[0] + s4[1]) + (s4[2] + s4[3]);
+    }
+    for (; k < k_end; ++k) {
+      const float kf = (float)k;
+      sum += geo.sample_nearest(fmaf(kf, ry.ix, ry.ex), fmaf(kf, ry.iy, ry.ey),
+                                fmaf(kf, ry.iz, ry.ez));
+    }
+    if (own_last && last_in && geo.interp_nonzero(v.src, d, t_last)) {
+      const float kf = (float)n_int;
+      sum += geo.sample_nearest(fmaf(kf, ry.ix, ry.ex), fmaf(kf, ry.iy, ry.ey),
+                                fmaf(kf, ry.iz, ry.ez));
+    }
+    acc += sum;
+    return (k_end - (chunk * n_int) / K) + ((own_last && last_in) ? 1 : 0);
+  }
+  // Linear interpolation.  OCT: consecutive samples are half a voxel apart, so
+  // a sample in the same cell as its predecessor skips its (predicated-off)
+  // 32-byte load and reuses the live cell (pa, pb).  Plain: the same 8 values
+  // from mu.  Same cells, weights and summation grouping either way.
+  int prev = -1;
+  float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pb = pa;
+  auto value = [&](const Cell& c) -> float {
+    if (OCT) {
+      const int idx = geo.gather_index(c);
       if (idx != prev) {
-        ld_cell(oct + 2 * (size_t)(unsigned)idx, pa, pb);
+        ld_cell(geo.oct + 2 * (size_t)(unsigned)idx, pa, pb);
         prev = idx;
       }
-      return lerp8d(pa, pb, w0, w1, w2);
-    };
-#pragma unroll 1
-    for (; k + 4 <= k_end; k += 4) {
-      const float k0 = (float)k;
-      const float s0 = cell_sample(k0);
-      const float s1 = cell_sample(k0 + 1.0f);
-      const float s2 = cell_sample(k0 + 2.0f);
-      const float s3 = cell_sample(k0 + 3.0f);
-      sum += (s0 + s1) + (s2 + s3);
+      return lerp8d(pa, pb, c.w0, c.w1, c.w2);
     }
-    for (; k < k_end; ++k) sum += cell_sample((float)k);
-  }
+    float4 a, b;
+    geo.fetch_plain(c, a, b);
+    return lerp8(a, b, c.w0, c.w1, c.w2);
+  };
+  ry.EX = dup2(ry.ex); ry.EY = dup2(ry.ey); ry.EZ = dup2(ry.ez);
+  ry.IX = dup2(ry.ix); ry.IY = dup2(ry.iy); ry.IZ = dup2(ry.iz);
+#pragma unroll 1
   for (; k + 4 <= k_end; k += 4) {
     const float k0 = (float)k;
-    float s0 = geo.template sample<NEAREST, OCT>(fmaf(k0, ix, ex), fmaf(k0, iy, ey), fmaf(k0, iz, ez));
-    float s1 = geo.template sample<NEAREST, OCT>(fmaf(k0 + 1.f, ix, ex), fmaf(k0 + 1.f, iy, ey),
-                                            fmaf(k0 + 1.f, iz, ez));
-    float s2 = geo.template sample<NEAREST, OCT>(fmaf(k0 + 2.f, ix, ex), fmaf(k0 + 2.f, iy, ey),
-                                            fmaf(k0 + 2.f, iz, ez));
-    float s3 = geo.template sample<NEAREST, OCT>(fmaf(k0 + 3.f, ix, ex), fmaf(k0 + 3.f, iy, ey),
-                                            fmaf(k0 + 3.f, iz, ez));
+    Cell c0, c1, c2, c3;
+    geo.locate2(k0, ry, c0, c1);
+    geo.locate2(k0 + 2.0f, ry, c2, c3);
+    const float s0 = value(c0);
+    const float s1 = value(c1);
+    const float s2 = value(c2);
+    const float s3 = value(c3);
     sum += (s0 + s1) + (s2 + s3);
   }
   for (; k < k_end; ++k) {
     const float kf = (float)k;
-    sum += geo.template sample<NEAREST, OCT>(fmaf(kf, ix, ex), fmaf(kf, iy, ey), fmaf(kf, iz, ez));
+    sum += value(geo.locate(fmaf(kf, ry.ix, ry.ex), fmaf(kf, ry.iy, ry.ey), fmaf(kf, ry.iz, ry.ez)));
   }
   if (own_last && last_in && geo.interp_nonzero(v.src, d, t_last)) {
     const float kf = (float)n_int;
-    sum += geo.template sample<NEAREST, OCT>(fmaf(kf, ix, ex), fmaf(kf, iy, ey), fmaf(kf, iz, ez));
+    sum += value(geo.locate(fmaf(kf, ry.ix, ry.ex), fmaf(kf, ry.iy, ry.ey), fmaf(kf, ry.iz, ry.ez)));
   }
   acc += sum;
   return (k_end - (chunk * n_int) / K) + ((own_last && last_in) ? 1 : 0);
