@@ -180,23 +180,42 @@ class ShardedSartRun:
         self.den_c = self.e.tensor(self.chunk)
         self.resid = self.e.tensor(cfg.n_iterations, "float64")
         self.passes_done = 0
+        self.launch_log = None
+
+    def _timed(self, kind, s, fn, *args):
+        """Run fn; with launch_log set (GPU engine), bracket it with CUDA events."""
+        if self.launch_log is None:
+            fn(*args)
+            return
+        import torch
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn(*args)
+        b.record()
+        self.launch_log.append((kind, s, a, b))
 
     def run_subset(self, s: int) -> None:
         views, slots = self.local[s], self.local_slots[s]
         nv = self.num[:self.nvox].view(self.grid.shape)
         dv = self.den[:self.nvox].view(self.grid.shape)
         if len(views):
-            self.e.correction(self.mu, slots, len(views), self.corr)
-            self.e.bp_partial(self.corr, slots, len(views), nv, dv)
+            self._timed("fp_correction", s, self.e.correction, self.mu, slots, len(views),
+                        self.corr)
+            self._timed("bp_partial", s, self.e.bp_partial, self.corr, slots, len(views), nv, dv)
         else:
             self.num.zero_()
             self.den.zero_()
-        _reduce_scatter(self.num, self.num_c, self.group)
-        _reduce_scatter(self.den, self.den_c, self.group)
+        def exchange():
+            _reduce_scatter(self.num, self.num_c, self.group)
+            _reduce_scatter(self.den, self.den_c, self.group)
+        self._timed("reduce_scatter", s, exchange)
         if self.count:
-            self.e.update(self.num_c, self.den_c, self.offset, self.count, self.mu)
-        _all_gather(self.mu_flat, self.mu_flat[self.rank * self.chunk:
-                                               (self.rank + 1) * self.chunk], self.group)
+            self._timed("update", s, self.e.update, self.num_c, self.den_c, self.offset,
+                        self.count, self.mu)
+        self._timed("all_gather", s, _all_gather, self.mu_flat,
+                    self.mu_flat[self.rank * self.chunk:(self.rank + 1) * self.chunk],
+                    self.group)
 
     def run_pass(self, residual: bool | None = None) -> None:
         for s in range(len(self.subsets)):
@@ -206,7 +225,8 @@ class ShardedSartRun:
             k = min(self.passes_done, self.cfg.n_iterations - 1)
             acc = self.resid[k:k + 1]
             if self.resid_slots is not None:
-                self.e.residual(self.mu, self.resid_slots, len(self.resid_views), acc)
+                self._timed("fp_residual", -1, self.e.residual, self.mu, self.resid_slots,
+                            len(self.resid_views), acc)
             _dist().all_reduce(acc, group=self.group)
         self.passes_done += 1
 
