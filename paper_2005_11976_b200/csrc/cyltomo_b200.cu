@@ -856,7 +856,14 @@ int launch_fp(const Geo& geo, const ct_ray_view* views, const ct_batch& b, const
 // ---------------------------------------------------------------------------
 enum BpMode { BP_ACC = 0, BP_WRITE = 1, BP_UPDATE = 2 };
 
-constexpr int BP_THREADS = 256;
+#ifndef CT_BP_THREADS
+#define CT_BP_THREADS 256
+#endif
+constexpr int BP_THREADS = CT_BP_THREADS;
+#ifndef CT_BP_UNROLL
+#define CT_BP_UNROLL 2
+#endif
+constexpr int BP_UNROLL = CT_BP_UNROLL;
 constexpr int BP_CHUNK = 64;   // views staged in shared memory per pass
 constexpr float BP_EDGE_EPS = 1e-3f;  // px band around the frame edge refined in fp64
 
@@ -1002,7 +1009,7 @@ __global__ void __launch_bounds__(BP_THREADS) bp_kernel(const __grid_constant__ 
     __syncthreads();
     if (!active) continue;
     const float* __restrict__ img = a.corr + (size_t)c0 * npix;
-#pragma unroll 2
+#pragma unroll BP_UNROLL
     for (int i = 0; i < nc; ++i, img += npix) {
       const BpViewF f = sv[i];
       const float xi = fmaf(f.cphi, xw, -f.sphi * yw);
