@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define CT_ABI_VERSION 3
+#define CT_ABI_VERSION 4
 
 #define CT_OK 0
 #define CT_ERR_ARG (-1)   /* invalid argument (null pointer, bad size) */
@@ -234,6 +234,37 @@ int ct_sample_cart(const float *mu, const ct_cart_grid *grid, const double *xs,
 int ct_resample_cyl_to_cyl(const float *src_mu, const ct_cyl_grid *src,
                            const ct_cyl_grid *dst, int nearest, float *dst_mu,
                            ct_stream_t stream);
+
+/* ---- projection-image statistics for the pose step (cyltomo/imgproc.py) ---- */
+/* Per-view min / max of images[n_views][npix] (mn, mx: device float[n_views]). */
+int ct_image_minmax(const float *images, int n_views, int64_t npix, float *mn, float *mx,
+                    ct_stream_t stream);
+/* np.histogram(view, bins, range=(lo[v], hi[v])) per view, same fp64 binning
+ * and edge corrections as numpy's uniform-bin path; counts[n_views][bins]. */
+int ct_image_histogram(const float *images, int n_views, int64_t npix, const double *lo,
+                       const double *hi, int bins, unsigned *counts, ct_stream_t stream);
+/* mask[v] = dilate(images[v] > levels[v], square of half-width radius) (uint8). */
+int ct_threshold_dilate(const float *images, int n_views, int rows, int cols,
+                        const double *levels, int radius, unsigned char *mask,
+                        ct_stream_t stream);
+/* Per view and row: leftmost / rightmost column of mask & ~remove outside the
+ * n_rects (row0, row1, col0, col1) half-open rectangles; -1 when empty.
+ * remove and rects may be NULL.  left/right: int[n_views][rows]. */
+int ct_row_extents(const unsigned char *mask, const unsigned char *remove, int n_views,
+                   int rows, int cols, const int *rects, int n_rects, int *left, int *right,
+                   ct_stream_t stream);
+/* Fused threshold + extents for a ladder of n_levels (<= 16) thresholds per
+ * view (levels[n_views][n_levels], foreground = image > level) in one pass;
+ * left/right: int[n_levels][n_views][rows]. */
+int ct_row_extents_levels(const float *images, const double *levels, int n_levels,
+                          const unsigned char *remove, int n_views, int rows, int cols,
+                          const int *rects, int n_rects, int *left, int *right,
+                          ct_stream_t stream);
+/* Mean bilinear grey value of a strip parallel to each view's projected axis
+ * (axes[v] = u_top, v_top, u_bottom, v_bottom, |bottom - top|), signed offset / width in
+ * pixels (cyltomo/imgproc.py:152-180); out[v] = NaN if the strip is off-frame. */
+int ct_strip_profiles(const float *images, int n_views, int rows, int cols, const double *axes,
+                      double offset, double width, double *out, ct_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -20,7 +20,7 @@ LIB_NAME = "libcyltomo_b200.so"
 LIB_PATH = Path(os.environ.get("CT_LIBRARY") or Path(__file__).resolve().parent / LIB_NAME)
 
 CT_OK = 0
-CT_ABI_VERSION = 3
+CT_ABI_VERSION = 4
 
 
 class CylGridC(C.Structure):
@@ -96,6 +96,14 @@ _SIGNATURES = {
     "ct_cyl_trig": (C.c_int, [C.POINTER(CylGridC), P, P]),
     "ct_sart_update": (C.c_int, [P, P, C.c_int64, C.c_int64, C.POINTER(UpdateC), P]),
     "ct_line_integrals": (C.c_int, [P, C.c_int64, C.c_int64, P, C.c_double, P, P, P]),
+    "ct_image_minmax": (C.c_int, [P, C.c_int, C.c_int64, P, P, P]),
+    "ct_image_histogram": (C.c_int, [P, C.c_int, C.c_int64, P, P, C.c_int, P, P]),
+    "ct_threshold_dilate": (C.c_int, [P, C.c_int, C.c_int, C.c_int, P, C.c_int, P, P]),
+    "ct_row_extents": (C.c_int, [P, P, C.c_int, C.c_int, C.c_int, P, C.c_int, P, P, P]),
+    "ct_row_extents_levels": (C.c_int, [P, P, C.c_int, P, C.c_int, C.c_int, C.c_int, P,
+                                        C.c_int, P, P, P]),
+    "ct_strip_profiles": (C.c_int, [P, C.c_int, C.c_int, C.c_int, P, C.c_double, C.c_double,
+                                    P, P]),
     "ct_sample_cyl": (C.c_int, [P, C.POINTER(CylGridC), P, P, P, C.c_int64, C.c_int, P, P]),
     "ct_sample_cart": (C.c_int, [P, C.POINTER(CartGridC), P, P, P, C.c_int64, C.c_int,
                                  P, P]),

@@ -5,12 +5,14 @@ Mirrors the reference's ``cyltomo simulate | reconstruct | batch``
 (deep-merged on defaults, jsonschema-validated), same artifacts
 (``projections.json/.raw``, ``volume.json/.raw``, ``report.json``,
 ``residuals.csv``, ``batch_results.csv``, ``batch_summary.csv``) and the same
-exit codes (0 ok, 2 config, 3 io, 4 domain).  Differences: pose *estimation*
-(``fit_pose``) is not on the B200 path -- ``reconstruct`` takes a pose dict or
-pose file and ``batch`` runs with ``pose_source = "true"``; ``sart`` accepts
-``subsets`` (OS-SART) and ``residuals``; ``batch`` shards objects over ranks
-when launched with torchrun.
+exit codes (0 ok, 2 config, 3 io, 4 domain).  ``pose`` (``cyltomo/cli.py:286-313``)
+estimates the pose with the GPU-batched segmentation of :mod:`posefit`, and
+``reconstruct`` / ``batch`` use it for ``pose = "estimate"`` /
+``pose_source = "estimated"``.  Additions: ``sart`` accepts ``subsets``
+(OS-SART) and ``residuals``; ``batch`` shards objects over ranks when
+launched with torchrun.
 
+    python -m paper_2005_11976_b200.cli pose --config pose.json --out out/
     python -m paper_2005_11976_b200.cli reconstruct --config recon.json --out out/
 """
 
@@ -30,6 +32,7 @@ from . import errors, io
 from .geometry import Pose, ScanGeometry, full_turn_angles, make_circular_trajectory
 from .grid import CartGrid, CylGrid, CylVolume
 from .phantom import ComponentSpec, make_assembly_phantom, make_weight_map
+from .posefit import LmConfig, PoseFitParams, fit_pose
 from .projector import RaySamplingConfig, simulate_scan
 from .recon import SartConfig, presence_metric, sart_run
 
@@ -157,6 +160,99 @@ RECON_SCHEMA = {
 }
 
 
+def pose_params_from_config(d: dict) -> PoseFitParams:
+    """(cyltomo/cli.py:143-158)"""
+    lm = LmConfig(**d.get("lm", {})) if d.get("lm") else LmConfig()
+    return PoseFitParams(
+        threshold_level=d.get("threshold_level", "auto"),
+        threshold_levels=int(d.get("threshold_levels", 1)),
+        threshold_span=float(d.get("threshold_span", 0.0)),
+        dilation_radius=int(d.get("dilation_radius", 0)),
+        band=int(d.get("band", 1)),
+        nuisance_level=d.get("nuisance_level"),
+        nuisance_dilation=int(d.get("nuisance_dilation", 2)),
+        exclude_rects=tuple(tuple(r) for r in d.get("exclude_rects", [])),
+        estimate_gamma=bool(d.get("estimate_gamma", False)),
+        strip_offset=float(d.get("strip_offset", 0.0)),
+        strip_width=float(d.get("strip_width", 1.0)),
+        lm=lm)
+
+
+# the reference DeviceSpec's pose parameters (cyltomo/experiments.py:219-223):
+# the threshold isolates the dense core, the 9-level ladder recovers sub-pixel
+# corner positions
+DEVICE_POSE_PARAMS = dict(threshold_level=1.8, threshold_levels=9, threshold_span=1.0, band=1)
+
+POSE_SCHEMA = {
+    "type": "object",
+    "properties": {
+        "projections": {"type": "string"},
+        "params": {"type": "object"},
+        "study": {
+            "type": "object",
+            "properties": {
+                "centers_px": {"type": "array", "minItems": 2},
+                "noise_sigma": {"type": "number", "minimum": 0},
+                "geometry": GEOMETRY_SCHEMA,
+                "sim_shape": {"type": "array"},
+            },
+            "required": ["centers_px"],
+        },
+    },
+}
+
+
+def pose_precision_study(centers_px, geom: ScanGeometry, sim_shape=(60, 16, 32),
+                         noise_sigma: float = 0.01, seed: int = 0, pose: Pose | None = None):
+    """Repeated scans with shifted rotation-center column u0; spread of the
+    estimates per pose component (cyltomo/experiments.py:342-372)."""
+    import warnings
+    rng = np.random.default_rng(seed)
+    pose = pose or Pose(alpha=0.4, beta=math.radians(1.0), t=[1.0, -1.0, 0.5])
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        vol = make_assembly_phantom(_device_components(True),
+                                    CylGrid(*sim_shape, 8.0, 60.0, pose))
+    estimates = []
+    for u0 in centers_px:
+        g = ScanGeometry(geom.sdd, geom.sod, geom.det_cols, geom.det_rows, geom.pixel_pitch,
+                         (float(u0), geom.principal_point[1]), geom.stage_angles)
+        ps = simulate_scan(vol, g, noise_sigma=noise_sigma, rng=rng)
+        estimates.append(fit_pose(ps, PoseFitParams(**DEVICE_POSE_PARAMS)).pose)
+    comps = {"x_mm": [e.t[0] for e in estimates], "y_mm": [e.t[1] for e in estimates],
+             "z_mm": [e.t[2] for e in estimates], "alpha_rad": [e.alpha for e in estimates],
+             "beta_rad": [e.beta for e in estimates]}
+    sigma = {k: float(np.std(v, ddof=1)) for k, v in comps.items()}
+    return {"estimates": estimates, "components": comps, "sigma": sigma}
+
+
+def cmd_pose(args) -> int:
+    """(cyltomo/cli.py:286-313)"""
+    cfg = load_config(args, {"params": {}}, POSE_SCHEMA)
+    out = Path(args.out)
+    out.mkdir(parents=True, exist_ok=True)
+    if cfg.get("study"):
+        study = cfg["study"]
+        geom = geometry_from_config(study.get("geometry", {}))
+        result = pose_precision_study(study["centers_px"], geom,
+                                      sim_shape=tuple(study.get("sim_shape", (60, 16, 32))),
+                                      noise_sigma=study.get("noise_sigma", 0.01), seed=args.seed)
+        rows = [(k, *[fmt(v) for v in vals], fmt(result["sigma"][k]))
+                for k, vals in result["components"].items()]
+        n = len(study["centers_px"])
+        write_csv_rows(out / "pose_precision.csv",
+                       ["component", *[f"scan_{i}" for i in range(n)], "sigma"], rows)
+        print(f"wrote {out / 'pose_precision.csv'}")
+        return EXIT_OK
+    if "projections" not in cfg:
+        raise errors.ConfigError("pose needs \"projections\" (or a \"study\")")
+    ps = io.read_projections(cfg["projections"], device=True)
+    result = fit_pose(ps, pose_params_from_config(cfg["params"]))
+    io.write_pose(result.to_dict(), out / "pose.json")
+    print(f"wrote {out / 'pose.json'}")
+    return EXIT_OK
+
+
 def sart_config_from(cfg: dict, seed: int) -> SartConfig:
     sart = dict(cfg.get("sart", {}))
     subsets = sart.get("subsets")
@@ -180,14 +276,13 @@ def cmd_reconstruct(args) -> int:
         cfg["initial"] = None if args.init == "none" else args.init
     if args.weights is not None:
         cfg["weights"] = None if args.weights == "none" else args.weights
+    ps = io.read_projections(cfg["projections"], device=True)
     if isinstance(cfg["pose"], dict):
         pose = Pose.from_dict(cfg["pose"])
     elif cfg["pose"] == "estimate":
-        raise errors.ConfigError("pose estimation (fit_pose) is not part of the B200 path; "
-                                 "give \"pose\" as a pose dict or a pose file")
+        pose = fit_pose(ps, pose_params_from_config(cfg["pose_params"])).pose
     else:
         pose = io.read_pose(cfg["pose"])
-    ps = io.read_projections(cfg["projections"], device=True)
     if cfg["cartesian"]:
         c = cfg["cartesian"]
         grid = CartGrid.centered(*(int(v) for v in c["shape"]), float(c["voxel_size_mm"]),
@@ -255,11 +350,8 @@ def cmd_batch(args) -> int:
     import warnings
     defaults = {"n_samples": 50, "missing_fraction": 0.4, "strategies": ["a", "c"],
                 "recon_shape": [240, 40, 60], "sim_shape": [240, 16, 60], "passes": 1,
-                "noise_sigma": 0.02, "pose_source": "true", "geometry": {}}
+                "noise_sigma": 0.02, "pose_source": "estimated", "geometry": {}}
     cfg = load_config(args, defaults, BATCH_SCHEMA)
-    if cfg["pose_source"] != "true":
-        raise errors.ConfigError("pose_source 'estimated' needs fit_pose, which is not part "
-                                 "of the B200 path; use 'true'")
     strategies = sorted(set(args.strategies)) if args.strategies else list(cfg["strategies"])
     geom = geometry_from_config(cfg["geometry"])
     radius, height = 8.0, 60.0
@@ -279,15 +371,19 @@ def cmd_batch(args) -> int:
     rows = []
     for s in range(n):
         present = s not in missing
-        pose = _random_pose(rng)
+        true_pose = _random_pose(rng)
         with warnings.catch_warnings():
             warnings.simplefilter("ignore")
             vol = make_assembly_phantom(_device_components(present),
-                                        CylGrid(*sshape, radius, height, pose))
+                                        CylGrid(*sshape, radius, height, true_pose))
         # the noise draw advances the shared stream on every rank
         ps = simulate_scan(vol, geom, RaySamplingConfig(), cfg["noise_sigma"], rng)
         if s % world != rank:
             continue
+        if cfg["pose_source"] == "estimated":
+            pose = fit_pose(ps, PoseFitParams(**DEVICE_POSE_PARAMS)).pose
+        else:
+            pose = true_pose
         grid = CylGrid(*rshape, radius, height, pose=pose)
         row = {"sample": s, "present": present}
         for st in strategies:
@@ -343,6 +439,8 @@ def build_parser() -> argparse.ArgumentParser:
     p = sub.add_parser("simulate", parents=[common], help="forward-project a volume")
     p.add_argument("--views", type=int, help="override projection count")
     p.set_defaults(func=cmd_simulate)
+    p = sub.add_parser("pose", parents=[common], help="estimate the object pose")
+    p.set_defaults(func=cmd_pose)
     p = sub.add_parser("reconstruct", parents=[common], help="(OS-)SART reconstruction")
     p.add_argument("--init", metavar="none|PATH", help="initial volume")
     p.add_argument("--weights", metavar="none|PATH", help="back-projection weight map")

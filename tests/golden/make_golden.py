@@ -257,11 +257,118 @@ def io_cases():
             "io_proj_sum": np.asarray([imgs.sum()])}
 
 
+def pose_cases():
+    """The pose step (cyltomo/imgproc.py, posefit.py) on the reference's own
+    desk-scale test setup (tests/test_posefit.py:176-196): fp32-rounded
+    projections of a tilted device phantom, fit_pose under several parameter
+    sets, per-image functions, and LM triangulations."""
+    import warnings as _w
+    from cyltomo import imgproc as rip
+    from cyltomo import posefit as rpf
+    geom = ref.ScanGeometry(791.0, 679.0, 128, 256, 0.52, (63.5, 127.5),
+                            ref.make_circular_trajectory(21, math.radians(200.0)))
+
+    def phantom(pose, insert):
+        grid = ref.CylGrid(60, 96 if insert else 48, 32, radius=8.0, height=60.0, pose=pose)
+        comps = [ref.ComponentSpec("body", mu=0.04),
+                 ref.ComponentSpec("core", mu=1.0, r_range=(0.0, 1.5), h_range=(-28.0, 28.0))]
+        if insert:
+            comps.append(ref.ComponentSpec("insert", mu=0.8, r_range=(4.0, 6.0),
+                                           theta_range=(-0.35, 0.35), h_range=(-12.0, 12.0)))
+        with _w.catch_warnings():
+            _w.simplefilter("ignore")
+            return ref.make_assembly_phantom(comps, grid)
+
+    def images(pose, insert):
+        ps = ref.forward_project_all(phantom(pose, insert), geom,
+                                     ref.RaySamplingConfig(supersample=2))
+        return f32(ps.images)
+
+    g = {"pose_geom": np.array([geom.sdd, geom.sod, geom.det_cols, geom.det_rows,
+                                geom.pixel_pitch, *geom.principal_point])}
+    img_a = images(ref.Pose(alpha=0.6, beta=math.radians(5.0), t=[2.0, -3.0, 1.0]), False)
+    img_b = images(ref.Pose(alpha=0.9, beta=math.radians(4.0), gamma=0.7, t=[1.0, 0.5, -2.0]),
+                   True)
+    g["pose_img_a"] = img_a.astype(np.float32)
+    g["pose_img_b"] = img_b.astype(np.float32)
+    cases = {
+        "core": dict(threshold_level=1.8, threshold_levels=9, threshold_span=1.0, band=1),
+        "auto": dict(threshold_level="auto", dilation_radius=1, band=2),
+        "nuis": dict(threshold_level=0.3, threshold_levels=3, threshold_span=0.1,
+                     nuisance_level=2.5, nuisance_dilation=2,
+                     exclude_rects=((180, 256, 0, 64), (0, 5, 0, 128))),
+        "dil": dict(threshold_level=1.0, threshold_levels=4, threshold_span=0.5,
+                    dilation_radius=2, band=3),
+    }
+    for name, kw in cases.items():
+        res = rpf.fit_pose(ref.ProjectionSet(geom, img_a), rpf.PoseFitParams(**kw))
+        g[f"pose_{name}_axes"] = np.array([[a.top.u, a.top.v, a.bottom.u, a.bottom.v]
+                                           for a in res.axes])
+        g[f"pose_{name}_pose"] = np.array([res.pose.alpha, res.pose.beta, res.pose.gamma,
+                                           *res.pose.t])
+        g[f"pose_{name}_pts"] = np.concatenate([res.top.solution, res.bottom.solution])
+        g[f"pose_{name}_rms"] = np.array([res.top.residual_rms, res.bottom.residual_rms,
+                                          float(res.top.converged and res.bottom.converged)])
+    # gamma from the strip signal on the object with an off-axis insert
+    # (the reference finds a fundamental at offset 10 px and raises FlatSignal
+    # at 14 px on this object -- tests/test_pose.py checks both outcomes)
+    gkw = dict(threshold_level=1.8, threshold_levels=9, threshold_span=1.0, band=1,
+               estimate_gamma=True, strip_offset=10.0, strip_width=8.0)
+    res = rpf.fit_pose(ref.ProjectionSet(geom, img_b), rpf.PoseFitParams(**gkw))
+    g["pose_gamma_pose"] = np.array([res.pose.alpha, res.pose.beta, res.pose.gamma,
+                                     *res.pose.t])
+    g["pose_gamma_signal"] = np.array([rip.strip_profile(img_b[i], res.axes[i], 10.0, 8.0)
+                                       for i in range(geom.n_proj)])
+    try:
+        rpf.fit_pose(ref.ProjectionSet(geom, img_b),
+                     rpf.PoseFitParams(**dict(gkw, strip_offset=14.0)))
+        g["pose_gamma_flat14"] = np.array([0.0])
+    except ref.errors.FlatSignal:
+        g["pose_gamma_flat14"] = np.array([1.0])
+    g["pose_gamma_axes"] = np.array([[a.top.u, a.top.v, a.bottom.u, a.bottom.v]
+                                     for a in res.axes])
+    # per-image functions
+    g["pose_otsu"] = np.array([rip.otsu_level(img_a[i]) for i in range(geom.n_proj)]
+                              + [rip.otsu_level(img_b[i]) for i in range(geom.n_proj)])
+    strips = []
+    for off, wd in ((-6.0, 1.0), (0.0, 3.0), (14.0, 8.0), (-40.5, 2.4), (70.0, 1.0)):
+        for i in (0, 5, 13):
+            ax = rip.AxisObservation(ref.DetectorPoint(60.25, 70.5), ref.DetectorPoint(66.0, 190.0))
+            try:
+                strips.append(rip.strip_profile(img_b[i], ax, off, wd))
+            except Exception:  # off-frame strip
+                strips.append(np.nan)
+    g["pose_strips"] = np.array(strips)
+    ends = []
+    for seed in range(12):
+        m = np.random.default_rng(seed).random((40, 30)) > 0.7
+        m[:seed % 4] = False
+        ob = rip.axis_endpoints(m, band=1 + seed % 3)
+        ends.append([ob.top.u, ob.top.v, ob.bottom.u, ob.bottom.v])
+    g["pose_ends"] = np.array(ends)
+    # LM triangulation on noisy observations (tests/test_posefit.py:45-54 setup)
+    desk = ref.ScanGeometry(791.0, 679.0, 256, 128, 0.748, (127.5, 63.5),
+                            ref.make_circular_trajectory(21, math.radians(200.0)))
+    rng = np.random.default_rng(31)
+    obs_all, sol_all = [], []
+    for _ in range(6):
+        x = rng.uniform(-15, 15, size=3)
+        obs = [(i, ref.project_point(desk, i, x)) for i in range(0, 21, 2)]
+        noisy = [(i, ref.DetectorPoint(p.u + rng.normal(0, 0.3), p.v + rng.normal(0, 0.3)))
+                 for i, p in obs]
+        tp = rpf.track_point(noisy, desk)
+        obs_all.append([[i, p.u, p.v] for i, p in noisy])
+        sol_all.append([*tp.solution, tp.residual_rms])
+    g["pose_lm_obs"] = np.array(obs_all)
+    g["pose_lm_sol"] = np.array(sol_all)
+    return g
+
+
 def main():
     t = time.time()
     groups = {"golden_small.npz": small_cases, "golden_sart.npz": sart_cases,
               "golden_c1.npz": c1_cases, "golden_c2.npz": c2_cases,
-              "golden_io.npz": io_cases}
+              "golden_io.npz": io_cases, "golden_pose.npz": pose_cases}
     only = set(sys.argv[1:])
     for fname, fn in groups.items():
         if only and fname not in only:

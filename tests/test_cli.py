@@ -3,6 +3,7 @@ and exit codes, running on the B200 engine."""
 
 import csv
 import json
+import warnings
 from pathlib import Path
 
 import numpy as np
@@ -30,17 +31,29 @@ def test_config_errors_map_to_exit_codes(tmp_path, capsys):
                                                                  "radius_mm": 1.0,
                                                                  "height_mm": 1.0}})
     assert cli.main(["reconstruct", "--config", c, "--out", str(tmp_path)]) == 2
-    # pose estimation is not on the B200 path -> config error, before any I/O
-    c = _cfg(tmp_path, "c2.json", {"projections": "x", "grid": {"shape": [2, 4, 2],
-                                                                 "radius_mm": 1.0,
-                                                                 "height_mm": 1.0}})
-    assert cli.main(["reconstruct", "--config", c, "--out", str(tmp_path)]) == 2
+    # default pose = "estimate": projections are read first (reference order) -> io error
+    c = _cfg(tmp_path, "c2.json", {"projections": str(tmp_path / "x"),
+                                   "grid": {"shape": [2, 4, 2], "radius_mm": 1.0,
+                                            "height_mm": 1.0}})
+    assert cli.main(["reconstruct", "--config", c, "--out", str(tmp_path)]) == 3
+    # pose schema: study needs centers_px
+    c = _cfg(tmp_path, "p.json", {"study": {"noise_sigma": 0.1}})
+    assert cli.main(["pose", "--config", c, "--out", str(tmp_path)]) == 2
     # missing projections file -> io error
     c = _cfg(tmp_path, "c3.json", {"projections": str(tmp_path / "nope"), "pose": {
         "alpha_rad": 0, "beta_rad": 0, "gamma_rad": 0, "t_mm": [0, 0, 0]},
         "grid": {"shape": [2, 4, 2], "radius_mm": 1.0, "height_mm": 1.0}})
     assert cli.main(["reconstruct", "--config", c, "--out", str(tmp_path)]) == 3
     assert "io error" in capsys.readouterr().err
+
+
+def test_pose_params_from_config():
+    p = cli.pose_params_from_config({"threshold_level": 1.8, "threshold_levels": 9,
+                                     "threshold_span": 1.0, "exclude_rects": [[0, 5, 0, 9]],
+                                     "lm": {"max_iterations": 7}})
+    assert p.levels()[0] == pytest.approx(0.8) and p.exclude_rects == ((0, 5, 0, 9),)
+    assert p.lm.max_iterations == 7 and p.band == 1 and p.nuisance_level is None
+    assert cli.pose_params_from_config({}).threshold_level == "auto"
 
 
 def test_geometry_from_config_matches_reference_defaults():
@@ -81,8 +94,61 @@ def test_simulate_then_reconstruct(tmp_path):
 def test_batch_study_small(tmp_path):
     c = _cfg(tmp_path, "b.json", {"n_samples": 4, "recon_shape": [24, 8, 12],
                                   "sim_shape": [24, 8, 12], "strategies": ["a", "c"],
+                                  "pose_source": "true",
                                   "geometry": {"det_cols": 48, "det_rows": 96}})
     assert cli.main(["batch", "--config", c, "--out", str(tmp_path)]) == 0
     rows = list(csv.reader(open(tmp_path / "batch_results.csv")))
     assert rows[0] == ["sample", "present", "presence_a", "presence_c"] and len(rows) == 5
     assert (tmp_path / "batch_summary.csv").exists()
+
+
+@pytest.mark.gpu
+def test_pose_then_reconstruct_with_estimated_pose(tmp_path):
+    """cyltomo pose -> pose.json; reconstruct with pose = "estimate" uses the
+    same fit (cyltomo/cli.py:286-313, 351-355)."""
+    import math
+    true = P.Pose(alpha=0.6, beta=math.radians(3.0), t=[1.0, -1.5, 0.5])
+    geom = cli.geometry_from_config({})
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        vol = P.make_assembly_phantom(cli._device_components(True),
+                                      P.CylGrid(60, 16, 32, 8.0, 60.0, true))
+    ps = P.simulate_scan(vol, geom, P.RaySamplingConfig())
+    pio.write_projections(ps, tmp_path / "proj")
+    params = cli.DEVICE_POSE_PARAMS
+    c = _cfg(tmp_path, "pose.json", {"projections": str(tmp_path / "proj.json"),
+                                     "params": params})
+    assert cli.main(["pose", "--config", c, "--out", str(tmp_path / "p")]) == 0
+    doc = json.loads((tmp_path / "p" / "pose.json").read_text())
+    assert abs(doc["beta_rad"] - true.beta) < math.radians(0.2)
+    assert np.abs(np.array(doc["t_mm"]) - true.t).max() < 0.2
+    direct = P.fit_pose(pio.read_projections(tmp_path / "proj"), P.PoseFitParams(**params))
+    assert doc["alpha_rad"] == direct.pose.alpha and doc["t_mm"] == list(direct.pose.t)
+    rec = _cfg(tmp_path, "rec.json", {
+        "projections": str(tmp_path / "proj.json"), "pose": "estimate", "pose_params": params,
+        "grid": {"shape": [24, 8, 12], "radius_mm": 8.0, "height_mm": 60.0},
+        "sart": {"passes": 1}})
+    assert cli.main(["reconstruct", "--config", rec, "--out", str(tmp_path / "r")]) == 0
+    report = json.loads((tmp_path / "r" / "report.json").read_text())
+    assert report["pose"]["alpha_rad"] == direct.pose.alpha
+
+
+@pytest.mark.gpu
+def test_pose_precision_study(tmp_path):
+    c = _cfg(tmp_path, "s.json", {"study": {"centers_px": [45.5, 47.5, 49.5],
+                                            "noise_sigma": 0.01}})
+    assert cli.main(["pose", "--config", c, "--out", str(tmp_path)]) == 0
+    rows = list(csv.reader(open(tmp_path / "pose_precision.csv")))
+    assert rows[0] == ["component", "scan_0", "scan_1", "scan_2", "sigma"]
+    assert [r[0] for r in rows[1:]] == ["x_mm", "y_mm", "z_mm", "alpha_rad", "beta_rad"]
+    assert float(rows[1][-1]) < 0.1                       # x spread well under a voxel
+
+
+@pytest.mark.gpu
+def test_batch_with_estimated_poses(tmp_path):
+    c = _cfg(tmp_path, "b.json", {"n_samples": 4, "recon_shape": [48, 8, 12],
+                                  "sim_shape": [60, 16, 32], "strategies": ["a"],
+                                  "pose_source": "estimated"})
+    assert cli.main(["batch", "--config", c, "--out", str(tmp_path)]) == 0
+    rows = list(csv.reader(open(tmp_path / "batch_results.csv")))
+    assert len(rows) == 5
