@@ -260,6 +260,12 @@ int ct_row_extents_levels(const float *images, const double *levels, int n_level
                           const unsigned char *remove, int n_views, int rows, int cols,
                           const int *rects, int n_rects, int *left, int *right,
                           ct_stream_t stream);
+/* Axis endpoints (cyltomo/imgproc.py:97-131 band-corner rule) of n_tables
+ * extent tables left/right[n_tables][rows] (as ct_row_extents writes them):
+ * out[t] = (top_u, top_v, bottom_u, bottom_v) with top above bottom,
+ * status[t] = 0 ok, 1 empty mask, 2 fewer than two rows. */
+int ct_axis_endpoints(const int *left, const int *right, int n_tables, int rows, int band,
+                      double *out, int *status, ct_stream_t stream);
 /* Mean bilinear grey value of a strip parallel to each view's projected axis
  * (axes[v] = u_top, v_top, u_bottom, v_bottom, |bottom - top|), signed offset / width in
  * pixels (cyltomo/imgproc.py:152-180); out[v] = NaN if the strip is off-frame. */

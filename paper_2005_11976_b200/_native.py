@@ -102,6 +102,7 @@ _SIGNATURES = {
     "ct_row_extents": (C.c_int, [P, P, C.c_int, C.c_int, C.c_int, P, C.c_int, P, P, P]),
     "ct_row_extents_levels": (C.c_int, [P, P, C.c_int, P, C.c_int, C.c_int, C.c_int, P,
                                         C.c_int, P, P, P]),
+    "ct_axis_endpoints": (C.c_int, [P, P, C.c_int, C.c_int, C.c_int, P, P, P]),
     "ct_strip_profiles": (C.c_int, [P, C.c_int, C.c_int, C.c_int, P, C.c_double, C.c_double,
                                     P, P]),
     "ct_sample_cyl": (C.c_int, [P, C.POINTER(CylGridC), P, P, P, C.c_int64, C.c_int, P, P]),

@@ -1385,7 +1385,7 @@ __global__ void threshold_dilate_kernel(const float* __restrict__ img, int rows,
   const int r = blockIdx.y * blockDim.y + threadIdx.y;
   if (r >= rows || c >= cols) return;
   const float* p = img + (int64_t)v * rows * cols;
-  const double lv = level[v];
+  const float lv = __double2float_rd(level[v]);     // fp32 x > L  <=>  x > rd_f32(L)
   unsigned char on = 0;
   for (int dr = -radius; dr <= radius && !on; ++dr) {
     const int rr = r + dr;
@@ -1393,7 +1393,7 @@ __global__ void threshold_dilate_kernel(const float* __restrict__ img, int rows,
     for (int dc = -radius; dc <= radius; ++dc) {
       const int cc = c + dc;
       if (cc < 0 || cc >= cols) continue;
-      if ((double)p[(int64_t)rr * cols + cc] > lv) { on = 1; break; }
+      if (p[(int64_t)rr * cols + cc] > lv) { on = 1; break; }
     }
   }
   mask[((int64_t)v * rows + r) * cols + c] = on;
@@ -1415,11 +1415,13 @@ __global__ void __launch_bounds__(256) row_extents_kernel(
   const int v = blockIdx.y, r = blockIdx.x, nv = gridDim.y;
   const int64_t base = ((int64_t)v * rows + r) * cols;
   const int nl = FROM_IMAGE ? n_levels : 1;
-  double lv[CT_MAX_LEVELS];
+  // for fp32 x and fp64 L:  x > L  <=>  x > rd_f32(L)  (NaN stays NaN -> false),
+  // so the ladder compares run in fp32 with the reference's fp64 result
+  float lv[CT_MAX_LEVELS];
   int lo[CT_MAX_LEVELS], hi[CT_MAX_LEVELS];
 #pragma unroll
   for (int l = 0; l < CT_MAX_LEVELS; ++l) {
-    lv[l] = (FROM_IMAGE && l < nl) ? levels[(int64_t)v * n_levels + l] : 0.0;
+    lv[l] = (FROM_IMAGE && l < nl) ? __double2float_rd(levels[(int64_t)v * n_levels + l]) : 0.f;
     lo[l] = INT_MAX;
     hi[l] = -1;
   }
@@ -1431,7 +1433,7 @@ __global__ void __launch_bounds__(256) row_extents_kernel(
         keep = false;
     if (!keep) continue;
     if (FROM_IMAGE) {
-      const double x = (double)img[base + c];
+      const float x = img[base + c];
 #pragma unroll
       for (int l = 0; l < CT_MAX_LEVELS; ++l)
         if (l < nl && x > lv[l]) {
@@ -1464,6 +1466,59 @@ __global__ void __launch_bounds__(256) row_extents_kernel(
     left[o] = (a == INT_MAX) ? -1 : a;
     right[o] = b;
   }
+}
+
+// axis endpoints from per-row extents (cyltomo/imgproc.py:97-131), one block per
+// (level, view) table: first/last foreground rows, then the band corners --
+// extreme columns within the band rows, ties on an extreme column resolved to
+// the outermost row.  Integer work plus exact halves, so the fp64 outputs equal
+// the host rule bit for bit.  out[t] = (top_u, top_v, bottom_u, bottom_v),
+// status[t] = 0 ok, 1 empty, 2 fewer than two rows.
+__device__ void band_corners(const int* __restrict__ L, const int* __restrict__ R, int lo, int hi,
+                             int outward, double* u, double* v) {
+  int cl = INT_MAX, cr = -1;
+  for (int r = lo; r <= hi; ++r)
+    if (L[r] >= 0) { cl = min(cl, L[r]); cr = max(cr, R[r]); }
+  int vl = -1, vr = -1;
+  for (int r = lo; r <= hi; ++r) {
+    if (L[r] < 0) continue;
+    if (L[r] == cl && (vl < 0 || outward > 0)) vl = r;   // first (top) or last (bottom)
+    if (R[r] == cr && (vr < 0 || outward > 0)) vr = r;
+  }
+  *u = 0.5 * (double)(cl + cr);
+  *v = (double)lo + 0.5 * (double)((vl - lo) + (vr - lo));
+}
+
+__global__ void axis_endpoints_kernel(const int* __restrict__ left, const int* __restrict__ right,
+                                      int rows, int band, double* __restrict__ out,
+                                      int* __restrict__ status) {
+  const int t = blockIdx.x;
+  const int* L = left + (int64_t)t * rows;
+  const int* R = right + (int64_t)t * rows;
+  int rmin = INT_MAX, rmax = -1;
+  for (int r = threadIdx.x; r < rows; r += blockDim.x)
+    if (L[r] >= 0) { rmin = min(rmin, r); rmax = max(rmax, r); }
+  for (int o = 16; o > 0; o >>= 1) {
+    rmin = min(rmin, __shfl_xor_sync(0xffffffffu, rmin, o));
+    rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+  }
+  __shared__ int smin[32], smax[32];
+  if ((threadIdx.x & 31) == 0) { smin[threadIdx.x >> 5] = rmin; smax[threadIdx.x >> 5] = rmax; }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { rmin = min(rmin, smin[w]); rmax = max(rmax, smax[w]); }
+  double* o = out + 4 * (int64_t)t;
+  if (rmax < 0 || rmax - rmin < 1) {
+    status[t] = rmax < 0 ? 1 : 2;
+    o[0] = o[1] = o[2] = o[3] = 0.0;
+    return;
+  }
+  double tu, tv, bu, bv;
+  band_corners(L, R, rmin, min(rmin + band, rmax), -1, &tu, &tv);
+  band_corners(L, R, max(rmax - band, rmin), rmax, +1, &bu, &bv);
+  if (tv > bv) { double a = tu; tu = bu; bu = a; a = tv; tv = bv; bv = a; }
+  o[0] = tu; o[1] = tv; o[2] = bu; o[3] = bv;
+  status[t] = 0;
 }
 
 // mean bilinear grey value of a strip parallel to the projected axis
@@ -1862,6 +1917,15 @@ int ct_row_extents_levels(const float* images, const double* levels, int n_level
   row_extents_kernel<true><<<dim3(rows, n_views), 256, 0, CT_STREAM(stream)>>>(
       nullptr, images, levels, n_levels, remove, rows, cols, rects, n_rects, left, right);
   return check_launch("row_extents_kernel");
+}
+
+int ct_axis_endpoints(const int* left, const int* right, int n_tables, int rows, int band,
+                      double* out, int* status, ct_stream_t stream) {
+  if (!left || !right || !out || !status || n_tables < 1 || rows < 1 || band < 0)
+    return set_err(CT_ERR_ARG, "bad axis-endpoint arguments");
+  axis_endpoints_kernel<<<n_tables, 256, 0, CT_STREAM(stream)>>>(left, right, rows, band, out,
+                                                                status);
+  return check_launch("axis_endpoints_kernel");
 }
 
 int ct_strip_profiles(const float* images, int n_views, int rows, int cols, const double* axes,

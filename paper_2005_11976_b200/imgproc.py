@@ -16,8 +16,9 @@ per-pixel pass is a ``ct_*`` kernel:
 The axis endpoints need only those row extents: the band-corner rule of
 ``cyltomo/imgproc.py:97-131`` (extreme columns within the band rows, ties on
 an extreme column resolved to the outermost row) is a function of each row's
-leftmost and rightmost foreground column, so a (rows x 2) int table per view
-is all that crosses PCIe (:func:`endpoints_from_extents`).
+leftmost and rightmost foreground column.  ``ct_axis_endpoints`` applies it
+to the resident extent tables, so four fp64 numbers and a status per
+(view, level) are all that cross PCIe.
 
 Images are float32 (the framework's projection storage); the
 comparisons run in fp64 on the fp32 values exactly as the reference's
@@ -38,6 +39,7 @@ from .errors import DegenerateHistogram, DegenerateMask, EmptyResult, OutOfFrame
 from .geometry import DetectorPoint
 
 HIST_BINS = 256
+OK, EMPTY, ONE_ROW = 0, 1, 2          # ct_axis_endpoints status codes
 
 
 @dataclass
@@ -72,37 +74,6 @@ def otsu_from_histogram(counts, lo: float, hi: float) -> float:
     between = w0 * w1 * (mu0 - mu1) ** 2
     best = np.flatnonzero(between == between.max())
     return float(centers[best[best.size // 2]])
-
-
-def _band_center(left, right, row_lo: int, row_hi: int, outward: int) -> DetectorPoint:
-    lb, rb = left[row_lo:row_hi + 1], right[row_lo:row_hi + 1]
-    has = lb >= 0
-    if not has.any():
-        raise DegenerateMask(f"no foreground pixels in rows {row_lo}..{row_hi}")
-    c_left, c_right = int(lb[has].min()), int(rb[has].max())
-    # a band row touches column c_left iff its leftmost pixel is c_left (c_left
-    # is the band minimum); ties resolve to the outermost row
-    pick = min if outward < 0 else max
-    v_left = pick(np.flatnonzero(has & (lb == c_left)))
-    v_right = pick(np.flatnonzero(has & (rb == c_right)))
-    return DetectorPoint(float(0.5 * (c_left + c_right)),
-                         float(row_lo + 0.5 * float(v_left + v_right)))
-
-
-def endpoints_from_extents(left, right, band: int = 1, view: int = -1) -> AxisObservation:
-    """Axis endpoints (cyltomo/imgproc.py:114-131) from per-row extents:
-    left[r] / right[r] = leftmost / rightmost foreground column, -1 if none."""
-    left = np.asarray(left)
-    right = np.asarray(right)
-    rows = np.flatnonzero(left >= 0)
-    if rows.size == 0:
-        raise DegenerateMask("mask is empty")
-    r_min, r_max = int(rows[0]), int(rows[-1])
-    if r_max - r_min < 1:
-        raise DegenerateMask("mask spans fewer than two rows")
-    top = _band_center(left, right, r_min, min(r_min + band, r_max), outward=-1)
-    bottom = _band_center(left, right, max(r_max - band, r_min), r_max, outward=+1)
-    return AxisObservation(top=top, bottom=bottom, view=view)
 
 
 def bilinear_sample(image, u, v):
@@ -213,12 +184,12 @@ class ViewStack:
         return self._torch.as_tensor(np.array(fixed, dtype=np.int32).ravel(),
                                      device=self.device), len(fixed)
 
-    def extents(self, levels=None, mask=None, remove=None, exclude_rects=()):
-        """Per-row foreground extents -> (left, right) int32 host arrays [L, n, rows].
+    def _extents_dev(self, levels=None, mask=None, remove=None, exclude_rects=()):
+        """Per-row foreground extents on the device -> (left, right) int32 [L, n, rows].
 
-        Foreground is image > levels[v, l] (levels: [n, L]) or the given
-        device mask (L = 1); pixels of `remove` and inside exclude_rects are
-        background.
+        Foreground is image > levels[v, l] (levels: [n, L], one fused pass per
+        16 levels) or the given device mask (L = 1); pixels of `remove` and
+        inside exclude_rects are background.
         """
         torch = self._torch
         rt, nr = self._rects(exclude_rects)
@@ -229,7 +200,7 @@ class ViewStack:
             right = self._buf((1, self.n, self.rows), torch.int32)
             N.call("ct_row_extents", D.ptr(mask), mptr, self.n, self.rows, self.cols, rptr, nr,
                    D.ptr(left), D.ptr(right), D.stream_handle())
-            return left.cpu().numpy(), right.cpu().numpy()
+            return left, right
         lv = np.asarray(levels, dtype=np.float64).reshape(self.n, -1)
         nl = lv.shape[1]
         left = self._buf((nl, self.n, self.rows), torch.int32)
@@ -240,7 +211,26 @@ class ViewStack:
             N.call("ct_row_extents_levels", D.ptr(self.images), D.ptr(lv_t), b - a, mptr,
                    self.n, self.rows, self.cols, rptr, nr, D.ptr(left[a:b]), D.ptr(right[a:b]),
                    D.stream_handle())
+        return left, right
+
+    def extents(self, levels=None, mask=None, remove=None, exclude_rects=()):
+        """:meth:`_extents_dev` copied to the host (numpy int32 [L, n, rows])."""
+        left, right = self._extents_dev(levels, mask, remove, exclude_rects)
         return left.cpu().numpy(), right.cpu().numpy()
+
+    def axis_table(self, left, right, band: int):
+        """Band-corner axis endpoints of device extent tables [L, n, rows]
+        (``ct_axis_endpoints``) -> host (top_u, top_v, bottom_u, bottom_v,
+        status), each [L, n]; status 0 ok, 1 empty, 2 fewer than two rows."""
+        torch = self._torch
+        nt = left.shape[0] * left.shape[1]
+        out = self._buf((nt, 4), torch.float64)
+        st = self._buf(nt, torch.int32)
+        N.call("ct_axis_endpoints", D.ptr(left), D.ptr(right), nt, self.rows, int(band),
+               D.ptr(out), D.ptr(st), D.stream_handle())
+        o = D.to_host(out, pinned=True).reshape(left.shape[0], left.shape[1], 4)
+        s = D.to_host(st, pinned=True).reshape(left.shape[0], left.shape[1])
+        return o[..., 0], o[..., 1], o[..., 2], o[..., 3], s
 
     def strip_profiles(self, axes, offset: float, width: float = 1.0) -> np.ndarray:
         """Mean strip value per view (cyltomo/imgproc.py:156-180); raises in
@@ -314,9 +304,14 @@ def remove_features(mask, nuisance_masks=(), exclude_rects=()) -> np.ndarray:
 def axis_endpoints(mask, band: int = 1, view: int = -1) -> AxisObservation:
     """Axis endpoints of a foreground mask (cyltomo/imgproc.py:114-131)."""
     vs = ViewStack(np.asarray(mask, dtype=np.float32))
-    m = vs.images.to(vs._torch.uint8)
-    left, right = vs.extents(mask=m)
-    return endpoints_from_extents(left[0, 0], right[0, 0], band, view)
+    left, right = vs._extents_dev(mask=vs.images.to(vs._torch.uint8))
+    tu, tv, bu, bv, st = vs.axis_table(left, right, band)
+    if st[0, 0] == EMPTY:
+        raise DegenerateMask("mask is empty")
+    if st[0, 0] == ONE_ROW:
+        raise DegenerateMask("mask spans fewer than two rows")
+    return AxisObservation(DetectorPoint(float(tu[0, 0]), float(tv[0, 0])),
+                           DetectorPoint(float(bu[0, 0]), float(bv[0, 0])), view)
 
 
 def strip_profile(image, axis: AxisObservation, offset: float, width: float = 1.0) -> float:

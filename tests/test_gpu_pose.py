@@ -94,6 +94,32 @@ def test_fused_ladder_extents_equal_mask_extents():
         assert np.array_equal(left[k], lm[0]) and np.array_equal(right[k], rm[0])
 
 
+def test_axis_endpoint_kernel_equals_full_mask_rule(rng):
+    """ct_axis_endpoints on row extents == the reference's np.nonzero band rule
+    (oracle) on random blobs of every band width, incl. the degenerate masks."""
+    masks, bands = [], []
+    for _ in range(300):
+        m = np.zeros((32, 24), dtype=bool)
+        h, w = rng.integers(1, 32), rng.integers(1, 24)
+        m[:h, :w] = rng.random((h, w)) > rng.uniform(0.3, 0.995)
+        masks.append(m)
+        bands.append(int(rng.integers(0, 5)))
+    vs = IP.ViewStack(np.stack(masks).astype(np.float32))
+    left, right = vs._extents_dev(mask=vs.images.to(__import__("torch").uint8))
+    for band in range(5):
+        tu, tv, bu, bv, st = vs.axis_table(left, right, band)
+        for i, m in enumerate(masks):
+            if bands[i] != band:
+                continue
+            try:
+                want = O.axis_endpoints(m, band)
+            except O.OracleError:
+                assert st[0, i] != IP.OK
+                continue
+            assert st[0, i] == IP.OK
+            assert (tu[0, i], tv[0, i], bu[0, i], bv[0, i]) == want
+
+
 @pytest.mark.parametrize("case", ["core", "auto", "nuis", "dil"])
 def test_fit_pose_matches_reference(case):
     with warnings.catch_warnings():

@@ -1,8 +1,8 @@
 """Pose step, host side: the oracle pinned to the
 reference's outputs (tests/golden/golden_pose.npz, written by the unmodified
 reference), and the host logic of paper_2005_11976_b200.imgproc / posefit
-(extent -> endpoint rule, Otsu from counts, LM triangulation, axis_to_pose,
-phase fit) against both.  Behavioural cases follow the reference's
+(Otsu from counts, LM triangulation, axis_to_pose, phase fit) against both;
+the kernels are in tests/test_gpu_pose.py.  Behavioural cases follow the reference's
 tests/test_posefit.py and tests/test_imgproc.py."""
 
 import math
@@ -20,12 +20,11 @@ import pose_oracle as O  # noqa: E402
 from paper_2005_11976_b200 import (DetectorPoint, LmConfig, Pose, PoseFitParams,  # noqa: E402
                                    ScanGeometry, axis_to_pose, euler_to_matrix,
                                    make_circular_trajectory, project_point, track_point)
-from paper_2005_11976_b200.errors import (DegenerateAxis, DegenerateMask, FlatSignal,  # noqa: E402
+from paper_2005_11976_b200.errors import (DegenerateAxis, FlatSignal,  # noqa: E402
                                           IllPosed, NoConvergenceWarning)
 from paper_2005_11976_b200.geometry import (detector_point_world, project_point_jacobian,  # noqa: E402
                                             view_basis, wrap_angle)
-from paper_2005_11976_b200.imgproc import (AxisObservation, endpoints_from_extents,  # noqa: E402
-                                           otsu_from_histogram)
+from paper_2005_11976_b200.imgproc import AxisObservation, otsu_from_histogram  # noqa: E402
 from paper_2005_11976_b200.posefit import (_midpoint_init, _residuals_jacobian,  # noqa: E402
                                            phase_from_signal)
 
@@ -96,39 +95,6 @@ def test_otsu_from_counts_matches_reference():
         counts, _ = np.histogram(x, bins=256, range=(lo, hi))
         got.append(otsu_from_histogram(counts, lo, hi))
     assert np.array_equal(got, G["pose_otsu"])
-
-
-def test_endpoints_from_extents_equal_full_mask_rule(rng):
-    for seed in range(12):
-        m = np.random.default_rng(seed).random((40, 30)) > 0.7
-        m[:seed % 4] = False
-        ob = endpoints_from_extents(*extents(m), band=1 + seed % 3)
-        assert [ob.top.u, ob.top.v, ob.bottom.u, ob.bottom.v] == list(G["pose_ends"][seed])
-    for _ in range(200):   # random blobs, bands, mirrored
-        h, w = rng.integers(3, 30, size=2)
-        m = rng.random((h, w)) > rng.uniform(0.3, 0.97)
-        band = int(rng.integers(0, 5))
-        try:
-            want = O.axis_endpoints(m, band)
-        except O.OracleError:
-            with pytest.raises(DegenerateMask):
-                endpoints_from_extents(*extents(m), band)
-            continue
-        ob = endpoints_from_extents(*extents(m), band)
-        assert (ob.top.u, ob.top.v, ob.bottom.u, ob.bottom.v) == want
-
-
-def test_axis_endpoints_rectangle_and_degenerate():
-    m = np.zeros((60, 40), dtype=bool)
-    m[5:51, 10:21] = True
-    ob = endpoints_from_extents(*extents(m))
-    assert (ob.top.u, ob.top.v, ob.bottom.u, ob.bottom.v) == (15.0, 5.0, 15.0, 50.0)
-    with pytest.raises(DegenerateMask):
-        endpoints_from_extents(*extents(np.zeros((5, 5), dtype=bool)))
-    flat = np.zeros((5, 5), dtype=bool)
-    flat[2] = True
-    with pytest.raises(DegenerateMask):
-        endpoints_from_extents(*extents(flat))
 
 
 def test_axis_observation_swap():
