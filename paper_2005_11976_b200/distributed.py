@@ -6,11 +6,14 @@ north_star and SURVEY.md §8e:
 
 * **angle sharding** -- within OS-SART subset s, rank r projects and
   back-projects the views subset[r::G] on the same mu (views of a subset are
-  independent given mu), writes its partial (num, den) sums, and the one real
-  exchange step runs: reduce-scatter(num), reduce-scatter(den) -> the fused
-  update on the rank's voxel shard -> all-gather(mu).  Every rank ends the
-  subset with the same mu (the gather broadcasts one owner's values).  The
-  residual is an all-reduce of one fp64 per pass.
+  independent given mu) and writes its partial num; the one real exchange
+  step runs: reduce-scatter(num) -> the fused update on the rank's voxel
+  shard -> all-gather(mu).  den is mu-independent -- the BP weights of the
+  in-bounds taps are pure geometry (cyltomo/_kernels.py:365-376) -- so each
+  subset's den shard is computed and reduce-scattered ONCE at setup
+   and only num moves per subset.  Every rank ends the subset
+  with the same mu (the gather broadcasts one owner's values).  The residual
+  is an all-reduce of one fp64 per pass.
 * **object sharding** -- independent objects (config C5 batches) are
   assigned round-robin, no collective on the data path
   (:func:`reconstruct_batch`).
@@ -175,12 +178,29 @@ class ShardedSartRun:
         nmax = max(1, max(len(v) for v in self.local))
         self.corr = self.e.tensor((nmax, ps.geom.det_rows, ps.geom.det_cols))
         self.num = self.e.tensor(pad)
-        self.den = self.e.tensor(pad)
         self.num_c = self.e.tensor(self.chunk)
-        self.den_c = self.e.tensor(self.chunk)
+        self.den_c = self._subset_den(pad)
         self.resid = self.e.tensor(cfg.n_iterations, "float64")
         self.passes_done = 0
         self.launch_log = None
+
+    def _subset_den(self, pad):
+        """Per-subset den shards [n_subsets][chunk]: one partial BP (den only;
+        the correction values do not enter den) and one reduce-scatter per
+        subset, at setup."""
+        den = self.e.tensor(pad)
+        dv = den[:self.nvox].view(self.grid.shape)
+        nv = self.num[:self.nvox].view(self.grid.shape)
+        out = []
+        for views, slots in zip(self.local, self.local_slots):
+            if len(views):
+                self.e.bp_partial(self.corr, slots, len(views), nv, dv)
+            else:
+                den.zero_()
+            chunk = self.e.tensor(self.chunk)
+            _reduce_scatter(den, chunk, self.group)
+            out.append(chunk)
+        return out
 
     def _timed(self, kind, s, fn, *args):
         """Run fn; with launch_log set (GPU engine), bracket it with CUDA events."""
@@ -198,20 +218,16 @@ class ShardedSartRun:
     def run_subset(self, s: int) -> None:
         views, slots = self.local[s], self.local_slots[s]
         nv = self.num[:self.nvox].view(self.grid.shape)
-        dv = self.den[:self.nvox].view(self.grid.shape)
         if len(views):
             self._timed("fp_correction", s, self.e.correction, self.mu, slots, len(views),
                         self.corr)
-            self._timed("bp_partial", s, self.e.bp_partial, self.corr, slots, len(views), nv, dv)
+            self._timed("bp_partial", s, self.e.bp_partial, self.corr, slots, len(views), nv,
+                        None)
         else:
             self.num.zero_()
-            self.den.zero_()
-        def exchange():
-            _reduce_scatter(self.num, self.num_c, self.group)
-            _reduce_scatter(self.den, self.den_c, self.group)
-        self._timed("reduce_scatter", s, exchange)
+        self._timed("reduce_scatter", s, _reduce_scatter, self.num, self.num_c, self.group)
         if self.count:
-            self._timed("update", s, self.e.update, self.num_c, self.den_c, self.offset,
+            self._timed("update", s, self.e.update, self.num_c, self.den_c[s], self.offset,
                         self.count, self.mu)
         self._timed("all_gather", s, _all_gather, self.mu_flat,
                     self.mu_flat[self.rank * self.chunk:(self.rank + 1) * self.chunk],

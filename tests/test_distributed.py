@@ -56,6 +56,8 @@ class OracleEngine:
 
     def bp_partial(self, corr, slots, n, num, den):
         num.zero_()
+        if den is None:               # num-only partial (den precomputed per subset)
+            den = self.torch.zeros_like(num)
         den.zero_()
         out = (num.numpy(), den.numpy())
         for b, i in enumerate(slots[:n]):
