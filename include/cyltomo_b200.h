@@ -114,9 +114,9 @@ const char *ct_arch(void);
  *      :296-343 forward_cart) ---------------------------------------------- */
 
 /* `gather` (optional, may be NULL): the gather layout of the same mu built by
- * ct_pack_gather_* (8 floats per voxel: its 2x2x2 trilinear neighbourhood,
- * one 32-byte sector).  With it every FP sample is two 16-byte loads from one
- * sector instead of eight scattered 4-byte loads; results are identical.
+ * ct_pack_gather_* (8 floats per cell: the trilinear polynomial of its 2x2x2
+ * neighbourhood, one 32-byte sector).  With it every FP sample is one 32-byte
+ * load instead of eight scattered 4-byte loads; results are identical.
  * It must be rebuilt after mu changes. */
 
 /* forward_cyl over a batch of views: out_p / out_w are [n_batch][rows][cols]
@@ -205,10 +205,12 @@ int64_t ct_gather_floats_cyl(const ct_cyl_grid *grid);
 int64_t ct_gather_floats_cart(const ct_cart_grid *grid);
 /* Cell (kc, j, ic) holds the trilinear corner (k, j, i) = (kc-1, j, ic-1) with a
  * one-cell halo at index -1 (r/h: a copy of index 0; theta: the wrapped row
- * n_theta-1): v00, d00, v01, d01, then the
- * same at k+1, where vXY = mu(k+X, j+Y, i) and dXY = mu(k+X, j+Y, i+1) - vXY
- * (r/h clamp to the grid, theta wraps; Cartesian: y plays theta's role and all
- * three axes clamp).  16-byte aligned. */
+ * n_theta-1) as the coefficients of
+ *   f(wr, wt, wh) = c0 + cr wr + ct wt + crt wr wt + ch wh + crh wr wh + cth wt wh
+ *                   + crth wr wt wh,
+ * stored (c0, cr, ct, crt, ch, crh, cth, crth), of the 8 corner values
+ * mu(k+X, j+Y, i+Z) (r/h clamp to the grid, theta wraps; Cartesian: y plays
+ * theta's role and all three axes clamp).  16-byte aligned. */
 int ct_pack_gather_cyl(const float *mu, const ct_cyl_grid *grid, float *gather,
                        ct_stream_t stream);
 int ct_pack_gather_cart(const float *mu, const ct_cart_grid *grid, float *gather,

@@ -122,18 +122,25 @@ __device__ __forceinline__ float theta_2pi(float y, float x) {
   return (y < 0.0f) ? (kTwoPiF - t) : t;
 }
 
-// trilinear value from a gather cell: a = (v00, d00, v01, d01) at k0, b = the
-// same at k1, vXY = mu at (j0+Y, i0), dXY = mu(j0+Y, i0+1) - vXY.  The
-// differences are the ones lerp8 computes in-kernel (same fp32 op), so both
-// paths give identical bits.
-__device__ __forceinline__ float lerp8d(float4 a, float4 b, float wr, float wt, float wh) {
-  const float c00 = fmaf(a.y, wr, a.x);
-  const float c01 = fmaf(a.w, wr, a.z);
-  const float c10 = fmaf(b.y, wr, b.x);
-  const float c11 = fmaf(b.w, wr, b.z);
-  const float q0 = fmaf(c01 - c00, wt, c00);
-  const float q1 = fmaf(c11 - c10, wt, c10);
-  return fmaf(q1 - q0, wh, q0);
+// Trilinear interpolation as a polynomial in the cell weights:
+//   f = c0 + cr wr + ct wt + ch wh + crt wr wt + crh wr wh + cth wt wh + crth wr wt wh
+// from the 8 corner values a = (k0,j0,i0) (k0,j0,i1) (k0,j1,i0) (k0,j1,i1), b = the
+// same at k1.  The gather layout stores the coefficients (same 32 bytes as the
+// values), so a sample is 7 dependent-depth-3 FFMAs and no FADD; the plain
+// path derives them in-kernel with the same fp32 ops, so both paths give
+// identical bits.
+__device__ __forceinline__ void trilinear_coeffs(float4 a, float4 b, float4& ca, float4& cb) {
+  const float dr0 = a.y - a.x, dr1 = a.w - a.z, dr2 = b.y - b.x, dr3 = b.w - b.z;
+  const float dt0 = a.z - a.x, dt1 = b.z - b.x;
+  ca = make_float4(a.x, dr0, dt0, dr1 - dr0);                        // c0, cr, ct, crt
+  cb = make_float4(b.x - a.x, dr2 - dr0, dt1 - dt0, (dr3 - dr2) - (dr1 - dr0));  // ch, crh, cth, crth
+}
+__device__ __forceinline__ float trilinear_eval(float4 ca, float4 cb, float wr, float wt, float wh) {
+  const float e1 = fmaf(cb.w, wh, ca.w);   // crt + crth wh
+  const float e0 = fmaf(cb.y, wh, ca.y);   // cr + crh wh
+  const float f1 = fmaf(cb.z, wh, ca.z);   // ct + cth wh
+  const float f0 = fmaf(cb.x, wh, ca.x);   // c0 + ch wh
+  return fmaf(fmaf(e1, wt, e0), wr, fmaf(f1, wt, f0));
 }
 
 // one 32-byte cell of the gather layout with a single 256-bit load
@@ -150,16 +157,6 @@ __device__ __forceinline__ void ld_cell(const float4* p, float4& a, float4& b) {
 #endif
 }
 
-__device__ __forceinline__ float lerp8(float4 a, float4 b, float wr, float wt, float wh) {
-  // a = (k0,j0,i0) (k0,j0,i1) (k0,j1,i0) (k0,j1,i1); b = same at k1
-  const float c00 = fmaf(a.y - a.x, wr, a.x);
-  const float c01 = fmaf(a.w - a.z, wr, a.z);
-  const float c10 = fmaf(b.y - b.x, wr, b.x);
-  const float c11 = fmaf(b.w - b.z, wr, b.z);
-  const float q0 = fmaf(c01 - c00, wt, c00);
-  const float q1 = fmaf(c11 - c10, wt, c10);
-  return fmaf(q1 - q0, wh, q0);
-}
 
 // ---------------------------------------------------------------------------
 // packed fp32x2 arithmetic (sm_100 FFMA2 / FADD2 / FMUL2): two samples per
@@ -641,11 +638,12 @@ __device__ __forceinline__ int march(const Geo& geo, const ct_ray_view& v, doubl
         ld_cell(geo.oct + 2 * (size_t)(unsigned)idx, pa, pb);
         prev = idx;
       }
-      return lerp8d(pa, pb, c.w0, c.w1, c.w2);
+      return trilinear_eval(pa, pb, c.w0, c.w1, c.w2);
     }
-    float4 a, b;
+    float4 a, b, ca, cb;
     geo.fetch_plain(c, a, b);
-    return lerp8(a, b, c.w0, c.w1, c.w2);
+    trilinear_coeffs(a, b, ca, cb);
+    return trilinear_eval(ca, cb, c.w0, c.w1, c.w2);
   };
   ry.EX = dup2(ry.ex); ry.EY = dup2(ry.ey); ry.EZ = dup2(ry.ez);
   ry.IX = dup2(ry.ix); ry.IY = dup2(ry.iy); ry.IZ = dup2(ry.iz);
@@ -1239,9 +1237,10 @@ __global__ void resample_cyl_kernel(const float* __restrict__ src_mu, ct_cyl_gri
 
 
 // ---------------------------------------------------------------------------
-// gather layout: voxel index m holds its 2x2x2 trilinear neighbourhood
-// (r/h or x/y/z clamp, theta wrap) as two float4 = one 32-byte sector, so one
-// FP sample is 2 x LDG.128 from a single sector instead of 8 scattered loads.
+// gather layout: cell m holds the trilinear polynomial coefficients of its
+// 2x2x2 neighbourhood (r/h or x/y/z clamp, theta wrap) as two float4 = one
+// 32-byte sector, so one FP sample is one 256-bit load instead of 8 scattered
+// loads.
 // ---------------------------------------------------------------------------
 __global__ void pack_gather_cyl_kernel(const float* __restrict__ mu, int nh, int nt, int nr,
                                        float4* __restrict__ oct) {
@@ -1256,9 +1255,11 @@ __global__ void pack_gather_cyl_kernel(const float* __restrict__ mu, int nh, int
   const int k = max(kc - 1, 0), k1 = min(kc, nh - 1);
   const int j = (jc == 0) ? nt - 1 : jc - 1, j1 = (jc == nt) ? 0 : jc;
   auto M = [&](int kk, int jj, int ii) { return __ldg(mu + ((int64_t)kk * nt + jj) * nr + ii); };
-  const float v00 = M(k, j, i), v01 = M(k, j1, i), v10 = M(k1, j, i), v11 = M(k1, j1, i);
-  oct[2 * m] = make_float4(v00, M(k, j, i1) - v00, v01, M(k, j1, i1) - v01);
-  oct[2 * m + 1] = make_float4(v10, M(k1, j, i1) - v10, v11, M(k1, j1, i1) - v11);
+  float4 ca, cb;
+  trilinear_coeffs(make_float4(M(k, j, i), M(k, j, i1), M(k, j1, i), M(k, j1, i1)),
+                   make_float4(M(k1, j, i), M(k1, j, i1), M(k1, j1, i), M(k1, j1, i1)), ca, cb);
+  oct[2 * m] = ca;
+  oct[2 * m + 1] = cb;
 }
 
 __global__ void pack_gather_cart_kernel(const float* __restrict__ mu, int nz, int ny, int nx,
@@ -1273,9 +1274,11 @@ __global__ void pack_gather_cart_kernel(const float* __restrict__ mu, int nz, in
   const int j = max(jc - 1, 0), j1 = min(jc, ny - 1);
   const int k = max(kc - 1, 0), k1 = min(kc, nz - 1);
   auto M = [&](int kk, int jj, int ii) { return __ldg(mu + ((int64_t)kk * ny + jj) * nx + ii); };
-  const float v00 = M(k, j, i), v01 = M(k, j1, i), v10 = M(k1, j, i), v11 = M(k1, j1, i);
-  oct[2 * m] = make_float4(v00, M(k, j, i1) - v00, v01, M(k, j1, i1) - v01);
-  oct[2 * m + 1] = make_float4(v10, M(k1, j, i1) - v10, v11, M(k1, j1, i1) - v11);
+  float4 ca, cb;
+  trilinear_coeffs(make_float4(M(k, j, i), M(k, j, i1), M(k, j1, i), M(k, j1, i1)),
+                   make_float4(M(k1, j, i), M(k1, j, i1), M(k1, j1, i), M(k1, j1, i1)), ca, cb);
+  oct[2 * m] = ca;
+  oct[2 * m + 1] = cb;
 }
 
 int64_t gather_cells_cyl(const ct_cyl_grid& g) {
