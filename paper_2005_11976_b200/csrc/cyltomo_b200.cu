@@ -32,7 +32,11 @@
 
 namespace {
 
-constexpr double kTwoPi = 2.0 * 3.141592653589793;
+#ifndef CT_GATHER_HFAST
+#define CT_GATHER_HFAST 0
+#endif
+constexpr double kPi = 3.141592653589793;
+constexpr double kTwoPi = 2.0 * kPi;
 constexpr float kTwoPiF = 6.28318530717958647692f;
 
 thread_local char g_err[512] = "";
@@ -144,13 +148,17 @@ __device__ __forceinline__ float trilinear_eval(float4 ca, float4 cb, float wr, 
 }
 
 // one 32-byte cell of the gather layout with a single 256-bit load
-// (sm_100 LDG.E.ENL2.256; read-only path)
+// (sm_100 LDG.E.NA.ENL2.256; read-only path).  L1::no_allocate: the cells of
+// one ray are reused in registers and neighbouring rays rarely meet in L1, so
+// allocating L1 lines only costs data-pipe fill wavefronts (A/B: -5.5% FP time)
 __device__ __forceinline__ void ld_cell(const float4* p, float4& a, float4& b) {
-#if defined(CT_CELL_LOAD_128)
-  a = __ldg(p);
-  b = __ldg(p + 1);
-#else
+#if defined(CT_CELL_LOAD_ALLOC)
   asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z),
+                 "=f"(b.w)
+               : "l"(p));
+#else
+  asm("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z),
                  "=f"(b.w)
                : "l"(p));
@@ -196,11 +204,62 @@ __device__ __forceinline__ f32x2 add2_rd(f32x2 a, f32x2 b) {
   return d;
 }
 __device__ __forceinline__ f32x2 dup2(float a) { return pk(a, a); }
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 
-// Per-ray march constants, splatted for the paired path
+// 2 atan(q) / q as a polynomial in q^2 on q in [-1, 1]: degree-15 odd minimax
+// fit of 2 atan (max error 5.7e-8 rad; tools/fit_atan.py)
+#define CT_ATAN2X_C7 -0.008428506553173065f
+#define CT_ATAN2X_C6 0.044908907264471054f
+#define CT_ATAN2X_C5 -0.1135723665356636f
+#define CT_ATAN2X_C4 0.1941567361354828f
+#define CT_ATAN2X_C3 -0.2787010073661804f
+#define CT_ATAN2X_C2 0.3990408182144165f
+#define CT_ATAN2X_C1 -0.6666072607040405f
+#define CT_ATAN2X_C0 1.999998927116394f
+__device__ __forceinline__ float atan2x_poly(float s) {
+  float p = fmaf(CT_ATAN2X_C7, s, CT_ATAN2X_C6);
+  p = fmaf(p, s, CT_ATAN2X_C5);
+  p = fmaf(p, s, CT_ATAN2X_C4);
+  p = fmaf(p, s, CT_ATAN2X_C3);
+  p = fmaf(p, s, CT_ATAN2X_C2);
+  p = fmaf(p, s, CT_ATAN2X_C1);
+  return fmaf(p, s, CT_ATAN2X_C0);
+}
+__device__ __forceinline__ f32x2 atan2x_poly2(f32x2 s) {
+  f32x2 p = fma2(dup2(CT_ATAN2X_C7), s, dup2(CT_ATAN2X_C6));
+  p = fma2(p, s, dup2(CT_ATAN2X_C5));
+  p = fma2(p, s, dup2(CT_ATAN2X_C4));
+  p = fma2(p, s, dup2(CT_ATAN2X_C3));
+  p = fma2(p, s, dup2(CT_ATAN2X_C2));
+  p = fma2(p, s, dup2(CT_ATAN2X_C1));
+  return fma2(p, s, dup2(CT_ATAN2X_C0));
+}
+
+// Per-ray march constants.  Sample k of a ray sits at e + k*i (grid frame).
+//  * Cartesian: (ex, ey, ez) + k*(ix, iy, iz), in index units folded by locate.
+//  * Cylindrical: the ray's trace in the (x, y) plane is a line at distance
+//    d0 from the axis; with s the signed distance along it from the foot of
+//    the perpendicular, oriented so that theta increases with s,
+//        r = sqrt(s^2 + d0^2),   theta = phi + 2 atan(s / (r + d0))
+//    (half-angle form: |s / (r + d0)| <= 1, so no octant reduction), where
+//    phi is the foot's angle, shifted by 2 pi so the ray's smallest theta lies
+//    in [0, 2 pi).  s and d0 are in r-index units, the h index is linear in k:
+//        s = es + k*is,   h index + 1 = eh + k*ih,
+//    and ct = phi / dtheta + 0.5 folds the theta index offset (+1 halo, -0.5
+//    cell centre).  A ray spans < pi in theta, so indices stay below 1.5 n_theta
+//    + 1: the gather layout carries those rows (CylGeo::gather_rows).
 struct RayF {
-  float ex, ey, ez, ix, iy, iz;
-  f32x2 EX, EY, EZ, IX, IY, IZ;
+  float ex, ey, ez, ix, iy, iz;   // Cartesian, and the cylindrical nearest mode
+  float es, is, eh, ih, d0, d2, ct;
 };
 
 // One sample's trilinear cell: bit patterns of floor(index + 1) (+0x4B000000,
@@ -211,13 +270,6 @@ struct Cell {
 };
 
 constexpr unsigned kMagicBits = 0x4B000000u;   // bits of 2^23
-
-// octant fixups of theta_2pi, shared by the scalar and the paired code
-__device__ __forceinline__ float theta_fix(float t, float x, float y, bool y_major) {
-  t = y_major ? (1.57079632679489662f - t) : t;
-  t = (x < 0.0f) ? (3.14159265358979324f - t) : t;
-  return (y < 0.0f) ? (kTwoPiF - t) : t;
-}
 
 // ---------------------------------------------------------------------------
 // grid policies: support interval (fp64), last-sample test (fp64) and the
@@ -230,7 +282,9 @@ struct CylGeo {
   double radius, half_h;
   // fp32 sampling constants
   float inv_dr, inv_dth, inv_dh, h_off, h_off1, nr_m1, nh_m1;
-  unsigned cell_kstride, cell_jstride, idx_bias;   // gather layout (nh+1, nt+1, nr+1)
+  // gather layout: cells (nh+1, T, nr+1); CT_GATHER_HFAST stores them
+  // (T, nr+1, nh+1), h fastest
+  unsigned cell_kstride, cell_jstride, cell_istride, idx_bias;
 
   __host__ void init(const float* m, const float* gather, const ct_cyl_grid& g) {
     mu = m;
@@ -246,10 +300,19 @@ struct CylGeo {
     nh_m1 = (float)(g.n_h - 1);
     h_off1 = h_off + 1.0f;
     const unsigned B = kMagicBits;
+#if CT_GATHER_HFAST
+    cell_kstride = 1u;
+    cell_istride = (unsigned)g.n_h + 1u;
+    cell_jstride = ((unsigned)g.n_r + 1u) * cell_istride;
+#else
+    cell_istride = 1u;
     cell_jstride = (unsigned)g.n_r + 1u;
-    cell_kstride = ((unsigned)g.n_theta + 1u) * cell_jstride;
-    idx_bias = 0u - B * (cell_kstride + cell_jstride + 1u);            // mod 2^32
+    cell_kstride = (unsigned)gather_rows(g.n_theta) * cell_jstride;
+#endif
+    idx_bias = 0u - B * (cell_kstride + cell_jstride + cell_istride);  // mod 2^32
   }
+  // theta rows of the gather layout: indices -1 .. 1.5 n_theta + 1 (see RayF)
+  __host__ __device__ static int gather_rows(int n_theta) { return n_theta + (n_theta + 1) / 2 + 2; }
 
   // _kernels.py:170-204 (same operation order)
   __device__ __forceinline__ bool interval(const double s[3], const double d[3], double& t0,
@@ -295,58 +358,80 @@ struct CylGeo {
     return true;
   }
 
-  // Trilinear cell of a point.  The gather layout has a one-cell halo at
-  // r/h/theta index -1, so no clamps are needed: where the reference clamps,
-  // the halo's r/h difference is an exact 0 (theta: the wrapped row).
+  // Per-ray constants (RayF) from the first sample position e and the step
+  // vector inc (grid frame, fp64); samples 0..n-1.
+  __device__ __forceinline__ void setup_ray(const double e[3], const double inc[3], int n,
+                                            RayF& ry) const {
+    ry.ex = (float)e[0]; ry.ey = (float)e[1]; ry.ez = (float)e[2];
+    ry.ix = (float)inc[0]; ry.iy = (float)inc[1]; ry.iz = (float)inc[2];
+    const double l2 = inc[0] * inc[0] + inc[1] * inc[1];
+    double es, is, d0, phi;
+    if (l2 > 0.0) {
+      const double l = sqrt(l2), ux = inc[0] / l, uy = inc[1] / l;
+      const double c = e[0] * uy - e[1] * ux;        // > 0: theta increases along the ray
+      const double sg = c >= 0.0 ? 1.0 : -1.0;
+      d0 = fabs(c);
+      es = sg * (e[0] * ux + e[1] * uy);
+      is = sg * l;
+      phi = atan2(uy, ux) - sg * (0.5 * kPi);         // angle of the foot point
+    } else {                                          // parallel to the axis
+      es = 0.0; is = 0.0;
+      d0 = sqrt(e[0] * e[0] + e[1] * e[1]);
+      phi = atan2(e[1], e[0]);
+    }
+    // shift phi by 2 pi so the smallest theta of samples 0..n-1 is in [0, 2 pi)
+    const double th_min = phi + atan2(fmin(es, es + (n - 1) * is), d0);
+    phi -= kTwoPi * floor(th_min / kTwoPi);
+    const double idr = (double)nr / radius, d0i = fmax(d0 * idr, 1e-30);
+    ry.es = (float)(es * idr);
+    ry.is = (float)(is * idr);
+    ry.d0 = (float)d0i;
+    ry.d2 = (float)(d0i * d0i);
+    ry.ct = (float)(phi * ((double)nt / kTwoPi) + 0.5);
+    ry.eh = (float)(e[2] * ((double)nh / (2.0 * half_h)) + (0.5 * nh + 0.5));
+    ry.ih = (float)(inc[2] * ((double)nh / (2.0 * half_h)));
+  }
+
+  // Trilinear cell of sample k (see RayF): r = sqrt(s^2 + d0^2) and
+  // theta = phi + 2 atan(s / (r + d0)) with 2 atan from a degree-15 odd
+  // minimax polynomial on [-1, 1] (5.7e-8 rad; 2.8e-7 evaluated in fp32).
   // floor() via x + 2^23 rounded toward -inf (bits = floor(x) + 0x4B000000).
-  __device__ __forceinline__ Cell locate(float x, float y, float z) const {
-    const float r = sqrt_approx(fmaf(x, x, y * y));
-    const float th = theta_2pi(y, x);
-    const float fr1 = fmaf(r, inv_dr, 0.5f);      // r index + 1 (halo), >= 0.5
-    const float fh1 = fmaf(z, inv_dh, h_off1);    // h index + 1 (halo), >= 0.5
-    const float ft1 = fmaf(th, inv_dth, 0.5f);    // theta index + 1, in [0.5, nt + 0.5]
+  // The indices carry the gather layout's +1 halo offset.
+  __device__ __forceinline__ Cell locate1(float k, const RayF& ry) const {
+    const float s = fmaf(k, ry.is, ry.es);
+    const float fh1 = fmaf(k, ry.ih, ry.eh);
+    const float r = sqrt_approx(fmaf(s, s, ry.d2));
+    const float q = __fmul_rn(s, rcp_approx(__fadd_rn(r, ry.d0)));
+    const float ft1 = fmaf(__fmul_rn(q, atan2x_poly(__fmul_rn(q, q))), inv_dth, ry.ct);
+    const float fr1 = __fadd_rn(r, 0.5f);
     const float tr = __fadd_rd(fr1, 8388608.0f);
     const float th_ = __fadd_rd(fh1, 8388608.0f);
     const float tt = __fadd_rd(ft1, 8388608.0f);
     Cell c;
-    c.w0 = fr1 - (tr - 8388608.0f);
-    c.w1 = ft1 - (tt - 8388608.0f);
-    c.w2 = fh1 - (th_ - 8388608.0f);
+    c.w0 = __fsub_rn(fr1, __fsub_rn(tr, 8388608.0f));
+    c.w1 = __fsub_rn(ft1, __fsub_rn(tt, 8388608.0f));
+    c.w2 = __fsub_rn(fh1, __fsub_rn(th_, 8388608.0f));
     c.ib = __float_as_uint(tr);
     c.jb = __float_as_uint(tt);
     c.kb = __float_as_uint(th_);
     return c;
   }
 
-  // the same for samples k0, k0+1 of a ray, two per f32x2 instruction
-  __device__ __forceinline__ void locate2(float k0, const RayF& ry, Cell& ca, Cell& cb) const {
-    const f32x2 K = pk(k0, k0 + 1.0f);
-    const f32x2 X = fma2(K, ry.IX, ry.EX), Y = fma2(K, ry.IY, ry.EY), Z = fma2(K, ry.IZ, ry.EZ);
-    const f32x2 R2 = fma2(X, X, mul2(Y, Y));
-    float xa, xb, ya, yb, r2a, r2b;
-    upk(X, xa, xb);
-    upk(Y, ya, yb);
-    upk(R2, r2a, r2b);
-    const float mxa = fmaxf(fabsf(xa), fabsf(ya)), mna = fminf(fabsf(xa), fabsf(ya));
-    const float mxb = fmaxf(fabsf(xb), fabsf(yb)), mnb = fminf(fabsf(xb), fabsf(yb));
-    float rca, rcb;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rca) : "f"(fmaxf(mxa, 1e-30f)));
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rcb) : "f"(fmaxf(mxb, 1e-30f)));
-    const f32x2 A = mul2(pk(mna, mnb), pk(rca, rcb));
-    const f32x2 S = mul2(A, A);
-    f32x2 P = fma2(dup2(0.0068140108452664225f), S, dup2(-0.033610868703448114f));
-    P = fma2(P, S, dup2(0.07963126616806604f));
-    P = fma2(P, S, dup2(-0.13233753525313302f));
-    P = fma2(P, S, dup2(0.19807922265216282f));
-    P = fma2(P, S, dup2(-0.3331737967047227f));
-    P = fma2(P, S, dup2(0.999996115058577f));
-    float ta, tb;
-    upk(mul2(A, P), ta, tb);
-    ta = theta_fix(ta, xa, ya, fabsf(ya) > fabsf(xa));
-    tb = theta_fix(tb, xb, yb, fabsf(yb) > fabsf(xb));
-    const f32x2 FT1 = fma2(pk(ta, tb), dup2(inv_dth), dup2(0.5f));
-    const f32x2 FR1 = fma2(pk(sqrt_approx(r2a), sqrt_approx(r2b)), dup2(inv_dr), dup2(0.5f));
-    const f32x2 FH1 = fma2(Z, dup2(inv_dh), dup2(h_off1));
+  // the same for samples ka, kb, two per f32x2 instruction (lane-for-lane
+  // the ops of locate1, so both give identical bits)
+  __device__ __forceinline__ void locate2(float ka, float kb, const RayF& ry, Cell& ca,
+                                          Cell& cb) const {
+    const f32x2 K = pk(ka, kb);
+    const f32x2 S = fma2(K, dup2(ry.is), dup2(ry.es));
+    const f32x2 FH1 = fma2(K, dup2(ry.ih), dup2(ry.eh));
+    float r2a, r2b;
+    upk(fma2(S, S, dup2(ry.d2)), r2a, r2b);
+    const f32x2 R = pk(sqrt_approx(r2a), sqrt_approx(r2b));
+    float rda, rdb;
+    upk(add2(R, dup2(ry.d0)), rda, rdb);
+    const f32x2 Q = mul2(S, pk(rcp_approx(rda), rcp_approx(rdb)));
+    const f32x2 FT1 = fma2(mul2(Q, atan2x_poly2(mul2(Q, Q))), dup2(inv_dth), dup2(ry.ct));
+    const f32x2 FR1 = add2(R, dup2(0.5f));
     const f32x2 BIG = dup2(8388608.0f);
     const f32x2 TR = add2_rd(FR1, BIG), TT = add2_rd(FT1, BIG), TH = add2_rd(FH1, BIG);
     const f32x2 WR = sub2(FR1, sub2(TR, BIG)), WT = sub2(FT1, sub2(TT, BIG));
@@ -365,16 +450,20 @@ struct CylGeo {
 
   // gather-layout cell index (modular uint32; one constant for all offsets)
   __device__ __forceinline__ int gather_index(const Cell& c) const {
+#if CT_GATHER_HFAST
+    return (int)(c.ib * cell_istride + c.jb * cell_jstride + c.kb + idx_bias);
+#else
     return (int)(c.kb * cell_kstride + c.jb * cell_jstride + c.ib + idx_bias);
+#endif
   }
 
-  // the same 8 values from the plain mu layout (r/h clamp, theta wrap)
+  // the same 8 values from the plain mu layout (r/h clamp, theta modulo n_theta)
   __device__ __forceinline__ void fetch_plain(const Cell& c, float4& a, float4& b) const {
     const int i0 = (int)(c.ib - kMagicBits) - 1, g = (int)(c.jb - kMagicBits);
     const int k0 = (int)(c.kb - kMagicBits) - 1;
     const int ia = max(i0, 0), ib1 = min(i0 + 1, nr - 1);
     const int ka = max(k0, 0), kb1 = min(k0 + 1, nh - 1);
-    const int ja = (g == 0) ? nt - 1 : g - 1, jb1 = (g == nt) ? 0 : g;
+    const int ja = (g + nt - 1) % nt, jb1 = g % nt;
     const float* p0 = mu + ((size_t)ka * nt + ja) * nr;
     const float* p1 = mu + ((size_t)ka * nt + jb1) * nr;
     const float* p2 = mu + ((size_t)kb1 * nt + ja) * nr;
@@ -483,9 +572,20 @@ struct CartGeo {
     return c;
   }
 
-  __device__ __forceinline__ void locate2(float k0, const RayF& ry, Cell& ca, Cell& cb) const {
-    const f32x2 K = pk(k0, k0 + 1.0f);
-    const f32x2 X = fma2(K, ry.IX, ry.EX), Y = fma2(K, ry.IY, ry.EY), Z = fma2(K, ry.IZ, ry.EZ);
+  __device__ __forceinline__ void setup_ray(const double e[3], const double inc[3], int,
+                                            RayF& ry) const {
+    ry.ex = (float)e[0]; ry.ey = (float)e[1]; ry.ez = (float)e[2];
+    ry.ix = (float)inc[0]; ry.iy = (float)inc[1]; ry.iz = (float)inc[2];
+  }
+  __device__ __forceinline__ Cell locate1(float k, const RayF& ry) const {
+    return locate(fmaf(k, ry.ix, ry.ex), fmaf(k, ry.iy, ry.ey), fmaf(k, ry.iz, ry.ez));
+  }
+
+  __device__ __forceinline__ void locate2(float ka, float kb, const RayF& ry, Cell& ca,
+                                          Cell& cb) const {
+    const f32x2 K = pk(ka, kb);
+    const f32x2 X = fma2(K, dup2(ry.ix), dup2(ry.ex)), Y = fma2(K, dup2(ry.iy), dup2(ry.ey));
+    const f32x2 Z = fma2(K, dup2(ry.iz), dup2(ry.ez));
     const f32x2 IV = dup2(inv_vs);
     const f32x2 FX = fma2(X, IV, dup2(off1[0])), FY = fma2(Y, IV, dup2(off1[1]));
     const f32x2 FZ = fma2(Z, IV, dup2(off1[2]));
@@ -534,11 +634,25 @@ struct CartGeo {
 // ---------------------------------------------------------------------------
 enum FpEpi { EPI_PROJECT = 0, EPI_CORR = 1, EPI_RESID = 2, EPI_ROWMAX = 3 };
 
-constexpr int FP_THREADS = 128;
-#ifndef CT_FP_MIN_BLOCKS
-#define CT_FP_MIN_BLOCKS 9
+// block = FP_WX x FP_WY warps, each warp a pixel patch (tile_ww x tile_wh rays)
+#ifndef CT_FP_WX
+#define CT_FP_WX 4
 #endif
-constexpr int FP_MIN_BLOCKS = CT_FP_MIN_BLOCKS;   // 9: <= 56 registers, 36 warps/SM
+#ifndef CT_FP_WY
+#define CT_FP_WY 1
+#endif
+#ifndef CT_FP_CHAINS
+#define CT_FP_CHAINS 2           // independent gather chains per ray chunk (2 or 4)
+#endif
+#ifndef CT_FP_MAXREG
+#define CT_FP_MAXREG 64          // 32 warps/SM
+#endif
+#ifndef CT_FP_WW1
+#define CT_FP_WW1 4              // warp patch width at one lane per ray
+#endif
+constexpr int FP_WX = CT_FP_WX, FP_WY = CT_FP_WY, FP_CHAINS = CT_FP_CHAINS;
+static_assert(FP_CHAINS == 2 || FP_CHAINS == 4, "FP_CHAINS");
+constexpr int FP_THREADS = 32 * FP_WX * FP_WY;
 
 template <class Geo>
 struct FpArgs {
@@ -567,8 +681,8 @@ __host__ __device__ inline int lanes_for(int rows, int cols) {
   const long long px = (long long)rows * cols;
   return px >= 131072 ? 1 : px >= 65536 ? 2 : px >= 32768 ? 4 : 8;
 }
-// warp pixel patch: K=1 8x4, K=2 4x4, K=4 4x2, K=8 2x2; block = 2x2 warps
-__host__ __device__ inline int tile_ww(int K) { return K == 1 ? 8 : (K == 8 ? 2 : 4); }
+// warp pixel patch: K=1 8x4, K=2 4x4, K=4 4x2, K=8 2x2; block = FP_WX x FP_WY warps
+__host__ __device__ inline int tile_ww(int K) { return K == 1 ? CT_FP_WW1 : (K == 8 ? 2 : 4); }
 __host__ __device__ inline int tile_wh(int K) { return (32 / K) / tile_ww(K); }
 
 // One sub-ray, chunk `chunk` of `K`: returns this chunk's in-support sample
@@ -589,12 +703,15 @@ __device__ __forceinline__ int march(const Geo& geo, const ct_ray_view& v, doubl
   // fp32 march relative to the first sample position
   const double ts = dadd(t0, dmul(0.5, step));
   RayF ry;
-  ry.ex = (float)(v.src[0] + ts * d[0]);
-  ry.ey = (float)(v.src[1] + ts * d[1]);
-  ry.ez = (float)(v.src[2] + ts * d[2]);
-  ry.ix = (float)(step * d[0]);
-  ry.iy = (float)(step * d[1]);
-  ry.iz = (float)(step * d[2]);
+  {
+    double e[3], inc[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      e[a] = v.src[a] + ts * d[a];
+      inc[a] = step * d[a];
+    }
+    geo.setup_ray(e, inc, n, ry);
+  }
   const int n_int = n - 1;
   // interior samples [k, k_end) of this chunk; the last sample goes to chunk K-1
   int k = (chunk * n_int) / K;
@@ -627,45 +744,79 @@ __device__ __forceinline__ int march(const Geo& geo, const ct_ray_view& v, doubl
   }
   // Linear interpolation.  OCT: consecutive samples are half a voxel apart, so
   // a sample in the same cell as its predecessor skips its (predicated-off)
-  // 32-byte load and reuses the live cell (pa, pb).  Plain: the same 8 values
-  // from mu.  Same cells, weights and summation grouping either way.
-  int prev = -1;
-  float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pb = pa;
-  auto value = [&](const Cell& c) -> float {
+  // 32-byte load and reuses the live cell.  Plain: the same 8 values from mu.
+  // Same cells, weights and summation grouping either way.
+  //
+  // The chunk is marched as FP_CHAINS independent chains over consecutive
+  // sub-ranges, each with its own live cell: the chains' gathers are in
+  // flight together (a single chain serialises load -> evaluate -> next load
+  // through its cell registers), and one f32x2 locate serves two chains.
+  struct Chain {
+    int prev = -1;
+    float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pb = make_float4(0.f, 0.f, 0.f, 0.f);
+    float sum = 0.0f;
+  };
+  auto value = [&](Chain& ch, const Cell& c) -> float {
     if (OCT) {
       const int idx = geo.gather_index(c);
-      if (idx != prev) {
-        ld_cell(geo.oct + 2 * (size_t)(unsigned)idx, pa, pb);
-        prev = idx;
+      if (idx != ch.prev) {
+        ld_cell(geo.oct + 2 * (size_t)(unsigned)idx, ch.pa, ch.pb);
+        ch.prev = idx;
       }
-      return trilinear_eval(pa, pb, c.w0, c.w1, c.w2);
+      return trilinear_eval(ch.pa, ch.pb, c.w0, c.w1, c.w2);
     }
     float4 a, b, ca, cb;
     geo.fetch_plain(c, a, b);
     trilinear_coeffs(a, b, ca, cb);
     return trilinear_eval(ca, cb, c.w0, c.w1, c.w2);
   };
-  ry.EX = dup2(ry.ex); ry.EY = dup2(ry.ey); ry.EZ = dup2(ry.ez);
-  ry.IX = dup2(ry.ix); ry.IY = dup2(ry.iy); ry.IZ = dup2(ry.iz);
+  constexpr int NC = FP_CHAINS;
+  Chain ch[NC];
+  int kc[NC], ke[NC];
+  {
+    const int len = k_end - k;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      kc[c] = k + (c * len) / NC;
+      ke[c] = k + ((c + 1) * len) / NC;
+    }
+  }
+  // every chain has >= len/NC - 1 samples; 4 samples per iteration
+  const int iters = ((k_end - k) / NC) / (4 / NC);
 #pragma unroll 1
-  for (; k + 4 <= k_end; k += 4) {
-    const float k0 = (float)k;
+  for (int it = 0; it < iters; ++it) {
     Cell c0, c1, c2, c3;
-    geo.locate2(k0, ry, c0, c1);
-    geo.locate2(k0 + 2.0f, ry, c2, c3);
-    const float s0 = value(c0);
-    const float s1 = value(c1);
-    const float s2 = value(c2);
-    const float s3 = value(c3);
-    sum += (s0 + s1) + (s2 + s3);
+    if (NC == 2) {
+      geo.locate2((float)kc[0], (float)kc[1], ry, c0, c1);
+      geo.locate2((float)(kc[0] + 1), (float)(kc[1] + 1), ry, c2, c3);
+      const float a0 = value(ch[0], c0);
+      const float b0 = value(ch[1], c1);
+      const float a1 = value(ch[0], c2);
+      const float b1 = value(ch[1], c3);
+      ch[0].sum += a0 + a1;
+      ch[1].sum += b0 + b1;
+      kc[0] += 2; kc[1] += 2;
+    } else {
+      geo.locate2((float)kc[0], (float)kc[1], ry, c0, c1);
+      geo.locate2((float)kc[NC - 2], (float)kc[NC - 1], ry, c2, c3);
+      ch[0].sum += value(ch[0], c0);
+      ch[1].sum += value(ch[1], c1);
+      ch[NC - 2].sum += value(ch[NC - 2], c2);
+      ch[NC - 1].sum += value(ch[NC - 1], c3);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) ++kc[c];
+    }
   }
-  for (; k < k_end; ++k) {
-    const float kf = (float)k;
-    sum += value(geo.locate(fmaf(kf, ry.ix, ry.ex), fmaf(kf, ry.iy, ry.ey), fmaf(kf, ry.iz, ry.ez)));
-  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+    for (; kc[c] < ke[c]; ++kc[c]) ch[c].sum += value(ch[c], geo.locate1((float)kc[c], ry));
+  sum = ch[0].sum;
+#pragma unroll
+  for (int c = 1; c < NC; ++c) sum += ch[c].sum;
+  Chain& B = ch[NC - 1];
   if (own_last && last_in && geo.interp_nonzero(v.src, d, t_last)) {
     const float kf = (float)n_int;
-    sum += value(geo.locate(fmaf(kf, ry.ix, ry.ex), fmaf(kf, ry.iy, ry.ey), fmaf(kf, ry.iz, ry.ez)));
+    sum += value(B, geo.locate1(kf, ry));
   }
   acc += sum;
   return (k_end - (chunk * n_int) / K) + ((own_last && last_in) ? 1 : 0);
@@ -683,15 +834,15 @@ __device__ __forceinline__ double warp_max(double x) {
 }
 
 template <class Geo, int EPI, bool NEAREST, bool OCT>
-__global__ void __launch_bounds__(FP_THREADS, FP_MIN_BLOCKS) fp_kernel(const FpArgs<Geo> a) {
+__global__ void __maxnreg__(CT_FP_MAXREG) fp_kernel(const FpArgs<Geo> a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int K = a.lanes;
   const int ww = tile_ww(K), wh = tile_wh(K);
   const int chunk = lane & (K - 1);
   const int rslot = lane / K;
-  // each warp covers a ww x wh pixel patch, the block 2x2 warps
-  const int col = blockIdx.x * (2 * ww) + (warp & 1) * ww + rslot % ww;
-  const int row = blockIdx.z * (2 * wh) + (warp >> 1) * wh + rslot / ww;
+  // each warp covers a ww x wh pixel patch, the block FP_WX x FP_WY warps
+  const int col = blockIdx.x * (FP_WX * ww) + (warp % FP_WX) * ww + rslot % ww;
+  const int row = blockIdx.z * (FP_WY * wh) + (warp / FP_WX) * wh + rslot / ww;
   const int b = blockIdx.y;
   const int vid = a.view_ids ? a.view_ids[b] : b;
   const bool active = row < a.rows && col < a.cols;
@@ -795,7 +946,7 @@ __global__ void __launch_bounds__(1024) sum_partials_kernel(const double* __rest
 
 dim3 fp_grid(const ct_batch& b) {
   const int K = lanes_for(b.det_rows, b.det_cols);
-  const int tw = 2 * tile_ww(K), th = 2 * tile_wh(K);
+  const int tw = FP_WX * tile_ww(K), th = FP_WY * tile_wh(K);
   return dim3((b.det_cols + tw - 1) / tw, b.n_batch, (b.det_rows + th - 1) / th);
 }
 
@@ -1244,16 +1395,22 @@ __global__ void resample_cyl_kernel(const float* __restrict__ src_mu, ct_cyl_gri
 // ---------------------------------------------------------------------------
 __global__ void pack_gather_cyl_kernel(const float* __restrict__ mu, int nh, int nt, int nr,
                                        float4* __restrict__ oct) {
-  // cells (kc, jc, ic), kc in [0, nh], jc in [0, nt], ic in [0, nr]: corner
-  // (kc-1, jc-1, ic-1); index -1 is a halo (r/h: copy of 0; theta: row nt-1)
-  const int64_t n = (int64_t)(nh + 1) * (nt + 1) * (nr + 1);
+  // cells (kc, jc, ic), kc in [0, nh], jc in [0, T), ic in [0, nr]: corner
+  // (kc-1, jc-1, ic-1); index -1 is a halo (r/h: copy of 0), theta modulo nt
+  const int T = CylGeo::gather_rows(nt);
+  const int64_t n = (int64_t)(nh + 1) * T * (nr + 1);
   const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= n) return;
-  const int ic = (int)(m % (nr + 1)), jc = (int)((m / (nr + 1)) % (nt + 1));
-  const int kc = (int)(m / ((int64_t)(nr + 1) * (nt + 1)));
+#if CT_GATHER_HFAST
+  const int kc = (int)(m % (nh + 1)), ic = (int)((m / (nh + 1)) % (nr + 1));
+  const int jc = (int)(m / ((int64_t)(nh + 1) * (nr + 1)));
+#else
+  const int ic = (int)(m % (nr + 1)), jc = (int)((m / (nr + 1)) % T);
+  const int kc = (int)(m / ((int64_t)(nr + 1) * T));
+#endif
   const int i = max(ic - 1, 0), i1 = min(ic, nr - 1);
   const int k = max(kc - 1, 0), k1 = min(kc, nh - 1);
-  const int j = (jc == 0) ? nt - 1 : jc - 1, j1 = (jc == nt) ? 0 : jc;
+  const int j = (jc + nt - 1) % nt, j1 = jc % nt;
   auto M = [&](int kk, int jj, int ii) { return __ldg(mu + ((int64_t)kk * nt + jj) * nr + ii); };
   float4 ca, cb;
   trilinear_coeffs(make_float4(M(k, j, i), M(k, j, i1), M(k, j1, i), M(k, j1, i1)),
@@ -1282,7 +1439,7 @@ __global__ void pack_gather_cart_kernel(const float* __restrict__ mu, int nz, in
 }
 
 int64_t gather_cells_cyl(const ct_cyl_grid& g) {
-  return (int64_t)(g.n_h + 1) * (g.n_theta + 1) * (g.n_r + 1);
+  return (int64_t)(g.n_h + 1) * CylGeo::gather_rows(g.n_theta) * (g.n_r + 1);
 }
 int64_t gather_cells_cart(const ct_cart_grid& g) {
   return (int64_t)(g.n_z + 1) * (g.n_y + 1) * (g.n_x + 1);
