@@ -419,9 +419,7 @@ struct CylGeo {
 
   // the same for samples ka, kb, two per f32x2 instruction (lane-for-lane
   // the ops of locate1, so both give identical bits)
-  __device__ __forceinline__ void locate2(float ka, float kb, const RayF& ry, Cell& ca,
-                                          Cell& cb) const {
-    const f32x2 K = pk(ka, kb);
+  __device__ __forceinline__ void locate2(f32x2 K, const RayF& ry, Cell& ca, Cell& cb) const {
     const f32x2 S = fma2(K, dup2(ry.is), dup2(ry.es));
     const f32x2 FH1 = fma2(K, dup2(ry.ih), dup2(ry.eh));
     float r2a, r2b;
@@ -581,9 +579,7 @@ struct CartGeo {
     return locate(fmaf(k, ry.ix, ry.ex), fmaf(k, ry.iy, ry.ey), fmaf(k, ry.iz, ry.ez));
   }
 
-  __device__ __forceinline__ void locate2(float ka, float kb, const RayF& ry, Cell& ca,
-                                          Cell& cb) const {
-    const f32x2 K = pk(ka, kb);
+  __device__ __forceinline__ void locate2(f32x2 K, const RayF& ry, Cell& ca, Cell& cb) const {
     const f32x2 X = fma2(K, dup2(ry.ix), dup2(ry.ex)), Y = fma2(K, dup2(ry.iy), dup2(ry.ey));
     const f32x2 Z = fma2(K, dup2(ry.iz), dup2(ry.ez));
     const f32x2 IV = dup2(inv_vs);
@@ -644,13 +640,16 @@ enum FpEpi { EPI_PROJECT = 0, EPI_CORR = 1, EPI_RESID = 2, EPI_ROWMAX = 3 };
 #ifndef CT_FP_CHAINS
 #define CT_FP_CHAINS 2           // independent gather chains per ray chunk (2 or 4)
 #endif
+#ifndef CT_FP_UNROLL
+#define CT_FP_UNROLL 2           // main march loop unroll
+#endif
 #ifndef CT_FP_MAXREG
 #define CT_FP_MAXREG 64          // 32 warps/SM
 #endif
 #ifndef CT_FP_WW1
 #define CT_FP_WW1 4              // warp patch width at one lane per ray
 #endif
-constexpr int FP_WX = CT_FP_WX, FP_WY = CT_FP_WY, FP_CHAINS = CT_FP_CHAINS;
+constexpr int FP_WX = CT_FP_WX, FP_WY = CT_FP_WY, FP_CHAINS = CT_FP_CHAINS, FP_UNROLL = CT_FP_UNROLL;
 static_assert(FP_CHAINS == 2 || FP_CHAINS == 4, "FP_CHAINS");
 constexpr int FP_THREADS = 32 * FP_WX * FP_WY;
 
@@ -759,10 +758,8 @@ __device__ __forceinline__ int march(const Geo& geo, const ct_ray_view& v, doubl
   auto value = [&](Chain& ch, const Cell& c) -> float {
     if (OCT) {
       const int idx = geo.gather_index(c);
-      if (idx != ch.prev) {
-        ld_cell(geo.oct + 2 * (size_t)(unsigned)idx, ch.pa, ch.pb);
-        ch.prev = idx;
-      }
+      if (idx != ch.prev) ld_cell(geo.oct + 2 * (size_t)(unsigned)idx, ch.pa, ch.pb);
+      ch.prev = idx;   // (unconditional: equal when not reloaded; no predicated move)
       return trilinear_eval(ch.pa, ch.pb, c.w0, c.w1, c.w2);
     }
     float4 a, b, ca, cb;
@@ -783,22 +780,24 @@ __device__ __forceinline__ int march(const Geo& geo, const ct_ray_view& v, doubl
   }
   // every chain has >= len/NC - 1 samples; 4 samples per iteration
   const int iters = ((k_end - k) / NC) / (4 / NC);
-#pragma unroll 1
+  f32x2 kf01 = pk((float)kc[0], (float)kc[1]);
+#pragma unroll FP_UNROLL
   for (int it = 0; it < iters; ++it) {
     Cell c0, c1, c2, c3;
     if (NC == 2) {
-      geo.locate2((float)kc[0], (float)kc[1], ry, c0, c1);
-      geo.locate2((float)(kc[0] + 1), (float)(kc[1] + 1), ry, c2, c3);
+      // float sample counters (exact below 2^24): no int->float conversions
+      geo.locate2(kf01, ry, c0, c1);
+      geo.locate2(add2(kf01, dup2(1.0f)), ry, c2, c3);
+      kf01 = add2(kf01, dup2(2.0f));
       const float a0 = value(ch[0], c0);
       const float b0 = value(ch[1], c1);
       const float a1 = value(ch[0], c2);
       const float b1 = value(ch[1], c3);
       ch[0].sum += a0 + a1;
       ch[1].sum += b0 + b1;
-      kc[0] += 2; kc[1] += 2;
     } else {
-      geo.locate2((float)kc[0], (float)kc[1], ry, c0, c1);
-      geo.locate2((float)kc[NC - 2], (float)kc[NC - 1], ry, c2, c3);
+      geo.locate2(pk((float)kc[0], (float)kc[1]), ry, c0, c1);
+      geo.locate2(pk((float)kc[NC - 2], (float)kc[NC - 1]), ry, c2, c3);
       ch[0].sum += value(ch[0], c0);
       ch[1].sum += value(ch[1], c1);
       ch[NC - 2].sum += value(ch[NC - 2], c2);
@@ -806,6 +805,10 @@ __device__ __forceinline__ int march(const Geo& geo, const ct_ray_view& v, doubl
 #pragma unroll
       for (int c = 0; c < NC; ++c) ++kc[c];
     }
+  }
+  if (NC == 2) {
+    kc[0] += 2 * iters;
+    kc[1] += 2 * iters;
   }
 #pragma unroll
   for (int c = 0; c < NC; ++c)
