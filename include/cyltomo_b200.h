@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define CT_ABI_VERSION 4
+#define CT_ABI_VERSION 5
 
 #define CT_OK 0
 #define CT_ERR_ARG (-1)   /* invalid argument (null pointer, bad size) */
@@ -174,21 +174,34 @@ int ct_rowsum_max_cart(const ct_cart_grid *grid, const ct_ray_view *views,
 /* Sum over the batch of backproject_*(corr[b], view_ids[b]).  accumulate != 0
  * adds into num/den (the reference's semantics); 0 overwrites.  den may be
  * NULL.  trig (device, float64, [2*n_theta]) holds cos(theta_j), sin(theta_j)
- * of the voxel centres (see ct_cyl_trig). */
-int ct_bp_cyl(const float *corr, const ct_det_view *dets, const ct_batch *batch,
-              const ct_cyl_grid *grid, const double *trig, float *num, float *den,
-              int accumulate, ct_stream_t stream);
-int ct_bp_cart(const float *corr, const ct_det_view *dets, const ct_batch *batch,
-               const ct_cart_grid *grid, float *num, float *den, int accumulate,
-               ct_stream_t stream);
+ * of the voxel centres (see ct_cyl_trig).
+ * `quads` (optional, may be NULL): the bilinear footprints of the same corr
+ * stack built by ct_pack_quads; with it an interior voxel-view reads one
+ * 16-byte footprint instead of four scattered taps.  Results are identical
+ * to within fp32 rounding of the bilinear form (same taps, same weights).
+ * n_batch * det_rows * det_cols must be < 2^32. */
+int ct_bp_cyl(const float *corr, const float *quads, const ct_det_view *dets,
+              const ct_batch *batch, const ct_cyl_grid *grid, const double *trig, float *num,
+              float *den, int accumulate, ct_stream_t stream);
+int ct_bp_cart(const float *corr, const float *quads, const ct_det_view *dets,
+               const ct_batch *batch, const ct_cart_grid *grid, float *num, float *den,
+               int accumulate, ct_stream_t stream);
 
 /* BP of the batch followed by the fused SART / OS-SART update of
  * cyltomo/recon.py:105-119 with num/den = the batch sums (kept in registers). */
-int ct_bp_cyl_update(const float *corr, const ct_det_view *dets, const ct_batch *batch,
-                     const ct_cyl_grid *grid, const double *trig, const ct_update *upd,
-                     ct_stream_t stream);
-int ct_bp_cart_update(const float *corr, const ct_det_view *dets, const ct_batch *batch,
-                      const ct_cart_grid *grid, const ct_update *upd, ct_stream_t stream);
+int ct_bp_cyl_update(const float *corr, const float *quads, const ct_det_view *dets,
+                     const ct_batch *batch, const ct_cyl_grid *grid, const double *trig,
+                     const ct_update *upd, ct_stream_t stream);
+int ct_bp_cart_update(const float *corr, const float *quads, const ct_det_view *dets,
+                      const ct_batch *batch, const ct_cart_grid *grid, const ct_update *upd,
+                      ct_stream_t stream);
+
+/* Bilinear footprints of a correction stack [n_batch][rows][cols]: quad
+ * (b, v, u) = (c[v][u], c[v][u+1], c[v+1][u], c[v+1][u+1]) of image b (0 past
+ * the last row / column), 4 floats per pixel, 16-byte aligned.
+ * ct_quads_floats gives the buffer length in floats. */
+int64_t ct_quads_floats(const ct_batch *batch);
+int ct_pack_quads(const float *corr, const ct_batch *batch, float *quads, ct_stream_t stream);
 
 /* Fill trig[0:n] = cos((j+.5)dtheta), trig[n:2n] = sin(...) (fp64). */
 int ct_cyl_trig(const ct_cyl_grid *grid, double *trig, ct_stream_t stream);

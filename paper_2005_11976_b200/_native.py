@@ -20,7 +20,7 @@ LIB_NAME = "libcyltomo_b200.so"
 LIB_PATH = Path(os.environ.get("CT_LIBRARY") or Path(__file__).resolve().parent / LIB_NAME)
 
 CT_OK = 0
-CT_ABI_VERSION = 4
+CT_ABI_VERSION = 5
 
 
 class CylGridC(C.Structure):
@@ -85,14 +85,16 @@ _SIGNATURES = {
                                     C.POINTER(SamplingC), P, P]),
     "ct_rowsum_max_cart": (C.c_int, [C.POINTER(CartGridC), P, C.POINTER(BatchC),
                                      C.POINTER(SamplingC), P, P]),
-    "ct_bp_cyl": (C.c_int, [P, P, C.POINTER(BatchC), C.POINTER(CylGridC), P, P, P,
+    "ct_bp_cyl": (C.c_int, [P, P, P, C.POINTER(BatchC), C.POINTER(CylGridC), P, P, P,
                             C.c_int, P]),
-    "ct_bp_cart": (C.c_int, [P, P, C.POINTER(BatchC), C.POINTER(CartGridC), P, P,
+    "ct_bp_cart": (C.c_int, [P, P, P, C.POINTER(BatchC), C.POINTER(CartGridC), P, P,
                              C.c_int, P]),
-    "ct_bp_cyl_update": (C.c_int, [P, P, C.POINTER(BatchC), C.POINTER(CylGridC), P,
+    "ct_bp_cyl_update": (C.c_int, [P, P, P, C.POINTER(BatchC), C.POINTER(CylGridC), P,
                                    C.POINTER(UpdateC), P]),
-    "ct_bp_cart_update": (C.c_int, [P, P, C.POINTER(BatchC), C.POINTER(CartGridC),
+    "ct_bp_cart_update": (C.c_int, [P, P, P, C.POINTER(BatchC), C.POINTER(CartGridC),
                                     C.POINTER(UpdateC), P]),
+    "ct_quads_floats": (C.c_int64, [C.POINTER(BatchC)]),
+    "ct_pack_quads": (C.c_int, [P, C.POINTER(BatchC), P, P]),
     "ct_cyl_trig": (C.c_int, [C.POINTER(CylGridC), P, P]),
     "ct_sart_update": (C.c_int, [P, P, C.c_int64, C.c_int64, C.POINTER(UpdateC), P]),
     "ct_line_integrals": (C.c_int, [P, C.c_int64, C.c_int64, P, C.c_double, P, P, P]),

@@ -89,12 +89,6 @@ __device__ __forceinline__ float floor_pos(float x, int& i) {
   return t - 8388608.0f;
 }
 
-// 1/x from the MUFU approximation + one Newton step (~1 ulp)
-__device__ __forceinline__ float rcp_nr(float x) {
-  float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return fmaf(r, fmaf(-x, r, 1.0f), r);
-}
 
 __device__ __forceinline__ float sqrt_approx(float x) {
   float r;
@@ -145,6 +139,14 @@ __device__ __forceinline__ float trilinear_eval(float4 ca, float4 cb, float wr, 
   const float f1 = fmaf(cb.z, wh, ca.z);   // ct + cth wh
   const float f0 = fmaf(cb.x, wh, ca.x);   // c0 + ch wh
   return fmaf(fmaf(e1, wt, e0), wr, fmaf(f1, wt, f0));
+}
+
+// one bilinear footprint (ct_pack_quads) with a single 128-bit load
+__device__ __forceinline__ float4 ld_quad(const float4* p) {
+  float4 q;
+  asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+      : "=f"(q.x), "=f"(q.y), "=f"(q.z), "=f"(q.w) : "l"(p));
+  return q;
 }
 
 // one 32-byte cell of the gather layout with a single 256-bit load
@@ -204,6 +206,11 @@ __device__ __forceinline__ f32x2 add2_rd(f32x2 a, f32x2 b) {
   return d;
 }
 __device__ __forceinline__ f32x2 dup2(float a) { return pk(a, a); }
+__device__ __forceinline__ uint2 bits2(f32x2 v) {
+  uint2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(r.x), "=r"(r.y) : "l"(v));
+  return r;
+}
 __device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
   f32x2 d;
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
@@ -1017,12 +1024,17 @@ constexpr int BP_THREADS = CT_BP_THREADS;
 #define CT_BP_UNROLL 2
 #endif
 constexpr int BP_UNROLL = CT_BP_UNROLL;
+#ifndef CT_BP_MIN_BLOCKS
+#define CT_BP_MIN_BLOCKS 6       // <= 40 registers at 256 threads (A/B: 4-6)
+#endif
+constexpr int BP_MIN_BLOCKS = CT_BP_MIN_BLOCKS;
 constexpr int BP_CHUNK = 64;   // views staged in shared memory per pass
 constexpr float BP_EDGE_EPS = 1e-3f;  // px band around the frame edge refined in fp64
 
-struct BpViewF {
-  float cphi, sphi, sod, sdd_p;  // sdd / pitch
-  float u0, v0, depth_floor, _pad;
+// a pair of views (batch slots 2i, 2i+1), lane-interleaved for f32x2
+struct __align__(16) BpPairF {
+  f32x2 cphi, sphi, sod, sdd_p;   // sdd / pitch
+  f32x2 u0, v0, dfloor, coff;     // u0 + 1, v0 + 1, refine floor, tap offset (u32)
 };
 
 struct CylVox {
@@ -1081,6 +1093,7 @@ template <class Vox>
 struct BpArgs {
   Vox vox;
   const float* __restrict__ corr;
+  const float4* __restrict__ quads;   // bilinear footprints of corr (ct_pack_quads) or null
   const ct_det_view* __restrict__ dets;
   const int32_t* __restrict__ view_ids;
   int n_batch, rows, cols;
@@ -1127,9 +1140,54 @@ __device__ __noinline__ float2 bp_refine(const Vox& vox, int m, const ct_det_vie
   return acc;
 }
 
-template <class Vox, int MODE>
-__global__ void __launch_bounds__(BP_THREADS) bp_kernel(const __grid_constant__ BpArgs<Vox> a) {
-  __shared__ BpViewF sv[BP_CHUNK];
+// One voxel-view off the interior fast path (frame edge, fp64 refine band,
+// near the source plane): returns its (num, den) contribution.  u1 = u + 1,
+// v1 = v + 1 in pixels; img is the view's correction image.
+template <class Vox>
+__device__ __forceinline__ float2 bp_view_slow(const BpArgs<Vox>& a, int m, int slot, float u1,
+                                               float v1, float depth, float depth_floor,
+                                               const float* __restrict__ img) {
+  const float W1 = (float)a.cols + 1.0f, H1 = (float)a.rows + 1.0f;
+  // signed distance (px) of the footprint to the boundary of the set where
+  // den > 0, i.e. (-1, W) x (-1, H); near it, redo in fp64.
+  const float edge_d = fminf(fminf(u1, W1 - u1), fminf(v1, H1 - v1));
+  if (edge_d < BP_EDGE_EPS || depth <= depth_floor) {
+    if (edge_d > -BP_EDGE_EPS || depth <= depth_floor) {
+      const int vid = a.view_ids ? a.view_ids[slot] : slot;
+      return bp_refine(a.vox, m, a.dets[vid], img, a.rows, a.cols);
+    }
+    return make_float2(0.0f, 0.0f);
+  }
+  int iu, iv;                                       // floor(u), floor(v) >= -1
+  const float fu = u1 - floor_pos(u1, iu);
+  const float fv = v1 - floor_pos(v1, iv);
+  iu -= 1;
+  iv -= 1;
+  const float wu0 = 1.0f - fu, wv0 = 1.0f - fv;
+  // frame edge: only in-bounds taps count (_kernels.py:365-376)
+  const bool cu0 = iu >= 0, cu1 = iu + 1 < a.cols;
+  const bool rv0 = iv >= 0, rv1 = iv + 1 < a.rows;
+  const float* r0 = img + (iv * a.cols + iu);
+  const float t00 = (rv0 && cu0) ? __ldg(r0) : 0.0f;
+  const float t01 = (rv0 && cu1) ? __ldg(r0 + 1) : 0.0f;
+  const float t10 = (rv1 && cu0) ? __ldg(r0 + a.cols) : 0.0f;
+  const float t11 = (rv1 && cu1) ? __ldg(r0 + a.cols + 1) : 0.0f;
+  float2 r;
+  r.x = wv0 * fmaf(wu0, t00, fu * t01) + fv * fmaf(wu0, t10, fu * t11);
+  r.y = ((cu0 ? wu0 : 0.0f) + (cu1 ? fu : 0.0f)) * ((rv0 ? wv0 : 0.0f) + (rv1 ? fv : 0.0f));
+  return r;
+}
+
+// Voxel-driven BP (_kernels.py:380-417): one thread per voxel, the views of
+// the batch staged in shared memory in pairs and projected two per f32x2
+// instruction.  Interior footprints (all four taps on the detector, clear of
+// the source plane) take the fast path: one 32-bit tap offset per view from
+// the floor bit patterns, lerp-form bilinear in f32x2, den += 1 (the four
+// weights sum to 1); everything else goes through bp_view_slow.  num / den
+// accumulate per pair lane (even / odd batch slots) and are summed at the end.
+template <class Vox, int MODE, bool QUADS>
+__global__ void __launch_bounds__(BP_THREADS, BP_MIN_BLOCKS) bp_kernel(const __grid_constant__ BpArgs<Vox> a) {
+  __shared__ BpPairF sv[BP_CHUNK / 2];
   const int64_t nvox = a.vox.count();
   const int m = blockIdx.x * BP_THREADS + threadIdx.x;
   const bool active = m < nvox;
@@ -1142,74 +1200,118 @@ __global__ void __launch_bounds__(BP_THREADS) bp_kernel(const __grid_constant__ 
     zw = (float)w64[2];
   }
   const float W1 = (float)a.cols + 1.0f, H1 = (float)a.rows + 1.0f;
-  const size_t npix = (size_t)a.rows * a.cols;
-  float num = 0.0f, den = 0.0f;
+  const int npix = a.rows * a.cols;
+  const f32x2 XW = dup2(xw), NYW = dup2(-yw), YW = dup2(yw), ZW = dup2(zw);
+  const f32x2 BIG = dup2(8388608.0f);
+  f32x2 NUM = dup2(0.0f), DEN = dup2(0.0f);
+  int nfast = 0;   // interior voxel-views: den += 1 each
 
   for (int c0 = 0; c0 < a.n_batch; c0 += BP_CHUNK) {
     const int nc = min(BP_CHUNK, a.n_batch - c0);
     __syncthreads();
     if (threadIdx.x < nc) {
-      const int vid = a.view_ids ? a.view_ids[c0 + threadIdx.x] : c0 + threadIdx.x;
+      const int slot = c0 + threadIdx.x;
+      const int vid = a.view_ids ? a.view_ids[slot] : slot;
       const ct_det_view& d = a.dets[vid];
-      BpViewF f;
-      f.cphi = (float)d.cphi; f.sphi = (float)d.sphi; f.sod = (float)d.sod;
-      f.sdd_p = (float)(d.sdd / d.pitch);
-      f.u0 = (float)(d.u0 + 1.0); f.v0 = (float)(d.v0 + 1.0);   // stores u0 + 1, v0 + 1
-      f.depth_floor = (float)(2e-6 * d.sod);  // refine band: 2x the reference floor
-      f._pad = 0.0f;
-      sv[threadIdx.x] = f;
+      float* f = reinterpret_cast<float*>(&sv[threadIdx.x >> 1]) + (threadIdx.x & 1);
+      f[0] = (float)d.cphi;
+      f[2] = (float)d.sphi;
+      f[4] = (float)d.sod;
+      f[6] = (float)(d.sdd / d.pitch);
+      f[8] = (float)(d.u0 + 1.0);                      // u0 + 1, v0 + 1
+      f[10] = (float)(d.v0 + 1.0);
+      f[12] = (float)(2e-6 * d.sod);                   // refine band: 2x the reference floor
+      // tap offset constant: element (iv, iu) of the slot's image from the
+      // floor bit patterns ivb = B + iv + 1, iub = B + iu + 1 (mod 2^32)
+      reinterpret_cast<unsigned*>(f)[14] =
+          (unsigned)slot * (unsigned)npix - kMagicBits * ((unsigned)a.cols + 1u) -
+          (unsigned)a.cols - 1u;
     }
     __syncthreads();
     if (!active) continue;
-    const float* __restrict__ img = a.corr + (size_t)c0 * npix;
+    const float* __restrict__ img0 = a.corr + (size_t)c0 * npix;
+    const int np = nc >> 1;
 #pragma unroll BP_UNROLL
-    for (int i = 0; i < nc; ++i, img += npix) {
-      const BpViewF f = sv[i];
-      const float xi = fmaf(f.cphi, xw, -f.sphi * yw);
-      const float yi = fmaf(f.sphi, xw, f.cphi * yw);
-      const float depth = f.sod + yi;
-      const float scale = f.sdd_p * rcp_nr(depth);
-      const float u1 = fmaf(xi, scale, f.u0);   // u + 1
-      const float v1 = fmaf(zw, scale, f.v0);   // v + 1
-      // signed distance (px) of the footprint to the boundary of the set
-      // where den > 0, i.e. (-1, W) x (-1, H); near it, redo in fp64.
-      const float edge_d = fminf(fminf(u1, W1 - u1), fminf(v1, H1 - v1));
-      if (edge_d < BP_EDGE_EPS || depth <= f.depth_floor) {
-        if (edge_d > -BP_EDGE_EPS || depth <= f.depth_floor) {
-          const int vid = a.view_ids ? a.view_ids[c0 + i] : c0 + i;
-          const float2 nd = bp_refine(a.vox, m, a.dets[vid], img, a.rows, a.cols);
-          num += nd.x;
-          den += nd.y;
+    for (int i = 0; i < np; ++i) {
+      const BpPairF f = sv[i];
+      const f32x2 XI = fma2(f.cphi, XW, mul2(f.sphi, NYW));
+      const f32x2 YI = fma2(f.sphi, XW, mul2(f.cphi, YW));
+      const f32x2 DEPTH = add2(f.sod, YI);
+      float da, db;
+      upk(DEPTH, da, db);
+      const f32x2 R = pk(rcp_approx(da), rcp_approx(db));
+      const f32x2 RC = fma2(R, fma2(sub2(dup2(0.0f), DEPTH), R, dup2(1.0f)), R);
+      const f32x2 SC = mul2(f.sdd_p, RC);
+      const f32x2 U1 = fma2(XI, SC, f.u0);
+      const f32x2 V1 = fma2(ZW, SC, f.v0);
+      const f32x2 WU = sub2(dup2(W1), U1), HV = sub2(dup2(H1), V1);
+      float u1a, u1b, v1a, v1b, wua, wub, hva, hvb, dfa, dfb;
+      upk(U1, u1a, u1b);
+      upk(V1, v1a, v1b);
+      upk(WU, wua, wub);
+      upk(HV, hva, hvb);
+      upk(f.dfloor, dfa, dfb);
+      // edge_d > 1 <=> all four taps in bounds (then also clear of the band)
+      const bool fast_a = fminf(fminf(u1a, wua), fminf(v1a, hva)) > 1.0f && da > dfa;
+      const bool fast_b = fminf(fminf(u1b, wub), fminf(v1b, hvb)) > 1.0f && db > dfb;
+      if (fast_a && fast_b) {
+        const f32x2 TU = add2_rd(U1, BIG), TV = add2_rd(V1, BIG);
+        const f32x2 FU = sub2(U1, sub2(TU, BIG)), FV = sub2(V1, sub2(TV, BIG));
+        const uint2 tu = bits2(TU), tv = bits2(TV), co = bits2(f.coff);
+        const unsigned oa = tv.x * (unsigned)a.cols + tu.x + co.x;
+        const unsigned ob = tv.y * (unsigned)a.cols + tu.y + co.y;
+        if (QUADS) {
+          // one 16-byte footprint per view; lerp-form bilinear per lane
+          const float4 qa = ld_quad(a.quads + oa), qb = ld_quad(a.quads + ob);
+          float fua, fub, fva, fvb;
+          upk(FU, fua, fub);
+          upk(FV, fva, fvb);
+          const float aa = fmaf(fua, qa.y - qa.x, qa.x), ba = fmaf(fua, qa.w - qa.z, qa.z);
+          const float ab = fmaf(fub, qb.y - qb.x, qb.x), bb = fmaf(fub, qb.w - qb.z, qb.z);
+          NUM = add2(NUM, pk(fmaf(fva, ba - aa, aa), fmaf(fvb, bb - ab, ab)));
+        } else {
+          const float* qa = a.corr + oa;
+          const float* qb = a.corr + ob;
+          const f32x2 T00 = pk(__ldg(qa), __ldg(qb));
+          const f32x2 T01 = pk(__ldg(qa + 1), __ldg(qb + 1));
+          const f32x2 T10 = pk(__ldg(qa + a.cols), __ldg(qb + a.cols));
+          const f32x2 T11 = pk(__ldg(qa + a.cols + 1), __ldg(qb + a.cols + 1));
+          const f32x2 A = fma2(FU, sub2(T01, T00), T00);
+          const f32x2 B = fma2(FU, sub2(T11, T10), T10);
+          NUM = add2(NUM, fma2(FV, sub2(B, A), A));
         }
-        continue;
-      }
-      int iu, iv;                                       // floor(u), floor(v) >= -1
-      const float fu = u1 - floor_pos(u1, iu);
-      const float fv = v1 - floor_pos(v1, iv);
-      iu -= 1;
-      iv -= 1;
-      const float wu0 = 1.0f - fu, wv0 = 1.0f - fv;
-      // edge_d > 1 <=> 0 <= floor(u), floor(u)+1 < W (same for v): all 4 taps in bounds
-      if (edge_d > 1.0f) {
-        // whole footprint on the detector: the four weights sum to 1
-        const float* r0 = img + (iv * a.cols + iu);
-        const float t00 = __ldg(r0), t01 = __ldg(r0 + 1);
-        const float t10 = __ldg(r0 + a.cols), t11 = __ldg(r0 + a.cols + 1);
-        num += wv0 * fmaf(wu0, t00, fu * t01) + fv * fmaf(wu0, t10, fu * t11);
-        den += 1.0f;
+        nfast += 2;
       } else {
-        // frame edge: only in-bounds taps count (_kernels.py:365-376)
-        const bool cu0 = iu >= 0, cu1 = iu + 1 < a.cols;
-        const bool rv0 = iv >= 0, rv1 = iv + 1 < a.rows;
-        const float* r0 = img + (iv * a.cols + iu);
-        const float t00 = (rv0 && cu0) ? __ldg(r0) : 0.0f;
-        const float t01 = (rv0 && cu1) ? __ldg(r0 + 1) : 0.0f;
-        const float t10 = (rv1 && cu0) ? __ldg(r0 + a.cols) : 0.0f;
-        const float t11 = (rv1 && cu1) ? __ldg(r0 + a.cols + 1) : 0.0f;
-        num += wv0 * fmaf(wu0, t00, fu * t01) + fv * fmaf(wu0, t10, fu * t11);
-        den += ((cu0 ? wu0 : 0.0f) + (cu1 ? fu : 0.0f)) * ((rv0 ? wv0 : 0.0f) + (rv1 ? fv : 0.0f));
+        const float* ia = img0 + (size_t)(2 * i) * npix;
+        const float2 ra = bp_view_slow(a, m, c0 + 2 * i, u1a, v1a, da, dfa, ia);
+        const float2 rb = bp_view_slow(a, m, c0 + 2 * i + 1, u1b, v1b, db, dfb, ia + npix);
+        NUM = add2(NUM, pk(ra.x, rb.x));
+        DEN = add2(DEN, pk(ra.y, rb.y));
       }
     }
+    if (nc & 1) {   // odd view of the chunk: scalar, into the even lane
+      const int i = nc - 1;
+      const float* fp = reinterpret_cast<const float*>(&sv[i >> 1]);
+      const float cphi = fp[0], sphi = fp[2], sod = fp[4], sdd_p = fp[6];
+      const float u0 = fp[8], v0 = fp[10], dfl = fp[12];
+      const float xi = fmaf(cphi, xw, sphi * -yw);
+      const float yi = fmaf(sphi, xw, cphi * yw);
+      const float depth = sod + yi;
+      const float r = rcp_approx(depth);
+      const float scale = sdd_p * fmaf(r, fmaf(-depth, r, 1.0f), r);
+      const float2 rr = bp_view_slow(a, m, c0 + i, fmaf(xi, scale, u0), fmaf(zw, scale, v0), depth,
+                                     dfl, img0 + (size_t)i * npix);
+      NUM = add2(NUM, pk(rr.x, 0.0f));
+      DEN = add2(DEN, pk(rr.y, 0.0f));
+    }
+  }
+  float num, den;
+  {
+    float n0, n1, d0, d1;
+    upk(NUM, n0, n1);
+    upk(DEN, d0, d1);
+    num = n0 + n1;
+    den = (d0 + d1) + (float)nfast;
   }
   if (!active) return;
   if (MODE == BP_ACC) {
@@ -1237,11 +1339,12 @@ __global__ void __launch_bounds__(BP_THREADS) bp_kernel(const __grid_constant__ 
 }
 
 template <class Vox, int MODE>
-int launch_bp(const Vox& vox, const float* corr, const ct_det_view* dets, const ct_batch& b,
-              float* num, float* den, const ct_update* upd, cudaStream_t st) {
+int launch_bp(const Vox& vox, const float* corr, const float* quads, const ct_det_view* dets,
+              const ct_batch& b, float* num, float* den, const ct_update* upd, cudaStream_t st) {
   BpArgs<Vox> a;
   a.vox = vox;
   a.corr = corr;
+  a.quads = reinterpret_cast<const float4*>(quads);
   a.dets = dets;
   a.view_ids = b.view_ids;
   a.n_batch = b.n_batch;
@@ -1252,7 +1355,10 @@ int launch_bp(const Vox& vox, const float* corr, const ct_det_view* dets, const 
   if (upd) a.upd = *upd; else memset(&a.upd, 0, sizeof a.upd);
   const int64_t nvox = vox.count();
   const unsigned blocks = (unsigned)((nvox + BP_THREADS - 1) / BP_THREADS);
-  bp_kernel<Vox, MODE><<<blocks, BP_THREADS, 0, st>>>(a);
+  if (quads)
+    bp_kernel<Vox, MODE, true><<<blocks, BP_THREADS, 0, st>>>(a);
+  else
+    bp_kernel<Vox, MODE, false><<<blocks, BP_THREADS, 0, st>>>(a);
   return check_launch("bp_kernel");
 }
 
@@ -1439,6 +1545,20 @@ __global__ void pack_gather_cart_kernel(const float* __restrict__ mu, int nz, in
                    make_float4(M(k1, j, i), M(k1, j, i1), M(k1, j1, i), M(k1, j1, i1)), ca, cb);
   oct[2 * m] = ca;
   oct[2 * m + 1] = cb;
+}
+
+// bilinear footprints of a correction stack: quad (v, u) = (c[v][u], c[v][u+1],
+// c[v+1][u], c[v+1][u+1]) of the same image, 0 past the last row / column
+// (never read: the BP's fast path only takes footprints inside the frame)
+__global__ void pack_quads_kernel(const float* __restrict__ corr, int64_t n, int rows, int cols,
+                                  float4* __restrict__ quads) {
+  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n) return;
+  const int u = (int)(m % cols), v = (int)((m / cols) % rows);
+  const bool ru = u + 1 < cols, rv = v + 1 < rows;
+  const float* p = corr + m;
+  quads[m] = make_float4(__ldg(p), ru ? __ldg(p + 1) : 0.0f, rv ? __ldg(p + cols) : 0.0f,
+                         (ru && rv) ? __ldg(p + cols + 1) : 0.0f);
 }
 
 int64_t gather_cells_cyl(const ct_cyl_grid& g) {
@@ -1868,10 +1988,13 @@ static int check_bp(const float* corr, const ct_det_view* dets, const ct_batch* 
   if (!corr || !dets || !b) return set_err(CT_ERR_ARG, "null corr/dets/batch");
   if (b->n_batch < 1 || b->det_rows < 1 || b->det_cols < 1)
     return set_err(CT_ERR_ARG, "bad batch dimensions");
+  // the BP addresses the correction stack with 32-bit element offsets
+  if ((int64_t)b->n_batch * b->det_rows * b->det_cols > (int64_t)0xFFFFFFFFu)
+    return set_err(CT_ERR_ARG, "BP batch too large (n_batch*rows*cols must be < 2^32)");
   return CT_OK;
 }
 
-int ct_bp_cyl(const float* corr, const ct_det_view* dets, const ct_batch* batch,
+int ct_bp_cyl(const float* corr, const float* quads, const ct_det_view* dets, const ct_batch* batch,
               const ct_cyl_grid* grid, const double* trig, float* num, float* den,
               int accumulate, ct_stream_t stream) {
   int rc = check_bp(corr, dets, batch);
@@ -1880,11 +2003,11 @@ int ct_bp_cyl(const float* corr, const ct_det_view* dets, const ct_batch* batch,
   CylVox vox;
   vox.init(*grid, trig);
   if (accumulate)
-    return launch_bp<CylVox, BP_ACC>(vox, corr, dets, *batch, num, den, nullptr, CT_STREAM(stream));
-  return launch_bp<CylVox, BP_WRITE>(vox, corr, dets, *batch, num, den, nullptr, CT_STREAM(stream));
+    return launch_bp<CylVox, BP_ACC>(vox, corr, quads, dets, *batch, num, den, nullptr, CT_STREAM(stream));
+  return launch_bp<CylVox, BP_WRITE>(vox, corr, quads, dets, *batch, num, den, nullptr, CT_STREAM(stream));
 }
 
-int ct_bp_cart(const float* corr, const ct_det_view* dets, const ct_batch* batch,
+int ct_bp_cart(const float* corr, const float* quads, const ct_det_view* dets, const ct_batch* batch,
                const ct_cart_grid* grid, float* num, float* den, int accumulate,
                ct_stream_t stream) {
   int rc = check_bp(corr, dets, batch);
@@ -1893,11 +2016,11 @@ int ct_bp_cart(const float* corr, const ct_det_view* dets, const ct_batch* batch
   CartVox vox;
   vox.init(*grid);
   if (accumulate)
-    return launch_bp<CartVox, BP_ACC>(vox, corr, dets, *batch, num, den, nullptr, CT_STREAM(stream));
-  return launch_bp<CartVox, BP_WRITE>(vox, corr, dets, *batch, num, den, nullptr, CT_STREAM(stream));
+    return launch_bp<CartVox, BP_ACC>(vox, corr, quads, dets, *batch, num, den, nullptr, CT_STREAM(stream));
+  return launch_bp<CartVox, BP_WRITE>(vox, corr, quads, dets, *batch, num, den, nullptr, CT_STREAM(stream));
 }
 
-int ct_bp_cyl_update(const float* corr, const ct_det_view* dets, const ct_batch* batch,
+int ct_bp_cyl_update(const float* corr, const float* quads, const ct_det_view* dets, const ct_batch* batch,
                      const ct_cyl_grid* grid, const double* trig, const ct_update* upd,
                      ct_stream_t stream) {
   int rc = check_bp(corr, dets, batch);
@@ -1905,18 +2028,18 @@ int ct_bp_cyl_update(const float* corr, const ct_det_view* dets, const ct_batch*
   if (!trig || !upd || !upd->mu) return set_err(CT_ERR_ARG, "null trig/update/mu");
   CylVox vox;
   vox.init(*grid, trig);
-  return launch_bp<CylVox, BP_UPDATE>(vox, corr, dets, *batch, nullptr, nullptr, upd,
+  return launch_bp<CylVox, BP_UPDATE>(vox, corr, quads, dets, *batch, nullptr, nullptr, upd,
                                       CT_STREAM(stream));
 }
 
-int ct_bp_cart_update(const float* corr, const ct_det_view* dets, const ct_batch* batch,
+int ct_bp_cart_update(const float* corr, const float* quads, const ct_det_view* dets, const ct_batch* batch,
                       const ct_cart_grid* grid, const ct_update* upd, ct_stream_t stream) {
   int rc = check_bp(corr, dets, batch);
   if (rc || (rc = check_cart(grid))) return rc;
   if (!upd || !upd->mu) return set_err(CT_ERR_ARG, "null update/mu");
   CartVox vox;
   vox.init(*grid);
-  return launch_bp<CartVox, BP_UPDATE>(vox, corr, dets, *batch, nullptr, nullptr, upd,
+  return launch_bp<CartVox, BP_UPDATE>(vox, corr, quads, dets, *batch, nullptr, nullptr, upd,
                                        CT_STREAM(stream));
 }
 
@@ -2010,6 +2133,21 @@ int ct_pack_gather_cart(const float* mu, const ct_cart_grid* grid, float* gather
   pack_gather_cart_kernel<<<blocks_for(n, 256), 256, 0, CT_STREAM(stream)>>>(
       mu, grid->n_z, grid->n_y, grid->n_x, reinterpret_cast<float4*>(gather));
   return check_launch("pack_gather_cart_kernel");
+}
+
+int64_t ct_quads_floats(const ct_batch* batch) {
+  if (!batch || batch->n_batch < 1 || batch->det_rows < 1 || batch->det_cols < 1) return 0;
+  return 4 * (int64_t)batch->n_batch * batch->det_rows * batch->det_cols;
+}
+
+int ct_pack_quads(const float* corr, const ct_batch* batch, float* quads, ct_stream_t stream) {
+  if (!corr || !quads || !batch) return set_err(CT_ERR_ARG, "null corr/quads/batch");
+  if (batch->n_batch < 1 || batch->det_rows < 1 || batch->det_cols < 1)
+    return set_err(CT_ERR_ARG, "bad batch dimensions");
+  const int64_t n = (int64_t)batch->n_batch * batch->det_rows * batch->det_cols;
+  pack_quads_kernel<<<blocks_for(n, 256), 256, 0, CT_STREAM(stream)>>>(
+      corr, n, batch->det_rows, batch->det_cols, reinterpret_cast<float4*>(quads));
+  return check_launch("pack_quads_kernel");
 }
 
 // ---- projection-image statistics for the pose step --------------------------

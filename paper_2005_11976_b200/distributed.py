@@ -108,6 +108,7 @@ class GpuEngine:
         self.weights = _device_weights(cfg, grid.shape, self.device)
         self.cfg = cfg
         self.gather = None
+        self.quads = None
 
     def tensor(self, shape, dtype="float32"):
         torch = self.D.torch_mod()
@@ -126,7 +127,10 @@ class GpuEngine:
         self.eng.correction(mu, self.p_meas, slots, n, corr, self.gather)
 
     def bp_partial(self, corr, slots, n, num, den):
-        self.eng.bp_partial(corr, slots, n, num, den)
+        if self.quads is None:
+            self.quads = self.eng.alloc_quads(corr.shape[0])
+        self.eng.pack_quads(corr, n, self.quads)
+        self.eng.bp_partial(corr, slots, n, num, den, self.quads)
 
     def update(self, num_c, den_c, offset, count, mu):
         from . import _native as N

@@ -175,10 +175,10 @@ def back_project(correction, geom: ScanGeometry, i: int, grid, out=None):
     g = D.grid_c(grid)
     if isinstance(grid, CylGrid):
         trig = D.upload_f64(D.trig_table(grid))
-        N.call("ct_bp_cyl", D.ptr(corr), D.ptr(dets), C.byref(b), C.byref(g), D.ptr(trig),
+        N.call("ct_bp_cyl", D.ptr(corr), None, D.ptr(dets), C.byref(b), C.byref(g), D.ptr(trig),
                D.ptr(num), D.ptr(den), 1, D.stream_handle())
     else:
-        N.call("ct_bp_cart", D.ptr(corr), D.ptr(dets), C.byref(b), C.byref(g), D.ptr(num),
+        N.call("ct_bp_cart", D.ptr(corr), None, D.ptr(dets), C.byref(b), C.byref(g), D.ptr(num),
                D.ptr(den), 1, D.stream_handle())
     if out is not None:
         # write back into the caller's arrays (accumulation semantics)

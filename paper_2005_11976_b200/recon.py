@@ -28,6 +28,8 @@ import math
 import time
 from dataclasses import dataclass, field
 
+import os
+
 import numpy as np
 
 from . import _device as D
@@ -179,23 +181,41 @@ class SartEngine:
                C.byref(b), C.byref(self.samp), D.ptr(p_meas), D.ptr(self.row_thr), D.ptr(corr),
                D.stream_handle())
 
-    def bp_update(self, corr, slots, n: int, upd: N.UpdateC) -> None:
+    def alloc_quads(self, n: int):
+        """Buffer for the bilinear footprints of an n-view correction stack
+        (None with CT_BP_QUADS=0: the BP reads the four taps from corr)."""
+        if os.environ.get("CT_BP_QUADS", "1") == "0":
+            return None
+        torch = D.torch_mod()
+        b = D.batch_c(n, self.rows, self.cols)
+        length = int(N.load_library().ct_quads_floats(C.byref(b)))
+        return torch.empty(length, dtype=torch.float32, device=self.device)
+
+    def pack_quads(self, corr, n: int, quads) -> None:
+        if quads is None:
+            return
+        b = D.batch_c(n, self.rows, self.cols)
+        N.call("ct_pack_quads", D.ptr(corr), C.byref(b), D.ptr(quads), D.stream_handle())
+
+    def bp_update(self, corr, slots, n: int, upd: N.UpdateC, quads=None) -> None:
         b = D.batch_c(n, self.rows, self.cols, slots)
         if self.cyl:
-            N.call("ct_bp_cyl_update", D.ptr(corr), D.ptr(self.bp_dets), C.byref(b),
-                   C.byref(self.gc), D.ptr(self.trig), C.byref(upd), D.stream_handle())
+            N.call("ct_bp_cyl_update", D.ptr(corr), D.ptr(quads), D.ptr(self.bp_dets),
+                   C.byref(b), C.byref(self.gc), D.ptr(self.trig), C.byref(upd),
+                   D.stream_handle())
         else:
-            N.call("ct_bp_cart_update", D.ptr(corr), D.ptr(self.bp_dets), C.byref(b),
-                   C.byref(self.gc), C.byref(upd), D.stream_handle())
+            N.call("ct_bp_cart_update", D.ptr(corr), D.ptr(quads), D.ptr(self.bp_dets),
+                   C.byref(b), C.byref(self.gc), C.byref(upd), D.stream_handle())
 
-    def bp_partial(self, corr, slots, n: int, num, den) -> None:
+    def bp_partial(self, corr, slots, n: int, num, den, quads=None) -> None:
         """num/den = sum over the batch of the BP (overwrites)."""
         b = D.batch_c(n, self.rows, self.cols, slots)
         if self.cyl:
-            N.call("ct_bp_cyl", D.ptr(corr), D.ptr(self.bp_dets), C.byref(b), C.byref(self.gc),
-                   D.ptr(self.trig), D.ptr(num), D.ptr(den), 0, D.stream_handle())
+            N.call("ct_bp_cyl", D.ptr(corr), D.ptr(quads), D.ptr(self.bp_dets), C.byref(b),
+                   C.byref(self.gc), D.ptr(self.trig), D.ptr(num), D.ptr(den), 0,
+                   D.stream_handle())
         else:
-            N.call("ct_bp_cart", D.ptr(corr), D.ptr(self.bp_dets), C.byref(b),
+            N.call("ct_bp_cart", D.ptr(corr), D.ptr(quads), D.ptr(self.bp_dets), C.byref(b),
                    C.byref(self.gc), D.ptr(num), D.ptr(den), 0, D.stream_handle())
 
     def residual_scratch(self, n: int):
@@ -317,6 +337,7 @@ class SartRun:
                                 device=dev)
         self.upd = make_update(self.mu, self.weights, cfg)
         self.gather = self.eng.alloc_gather()
+        self.quads = self.eng.alloc_quads(nmax)
         self.resid = torch.zeros(cfg.n_iterations, dtype=torch.float64, device=dev)
         self.resid_cur = torch.zeros(1, dtype=torch.float64, device=dev)
         self.eng.residual_scratch(ps.geom.n_proj)      # no allocation inside a pass
@@ -344,7 +365,9 @@ class SartRun:
             self._timed("pack_gather", k, e.pack, self.mu, self.gather)
             self._timed("fp_correction", k, e.correction, self.mu, self.p_meas, slots, len(s),
                         self.corr, self.gather)
-            self._timed("bp_update", k, e.bp_update, self.corr, slots, len(s), self.upd)
+            self._timed("pack_quads", k, e.pack_quads, self.corr, len(s), self.quads)
+            self._timed("bp_update", k, e.bp_update, self.corr, slots, len(s), self.upd,
+                        self.quads)
         if residual:
             self.resid_cur.zero_()
             self._timed("pack_gather", -1, e.pack, self.mu, self.gather)

@@ -327,3 +327,44 @@ def test_gather_layout_matches_plain_path(rng, kind):
         outs.append(p)
     assert outs[0].abs().max() > 0
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("kind", ["cyl", "cart"])
+def test_quad_footprints_match_plain_bp(rng, kind):
+    """The BP's 16-byte footprints (ct_pack_quads) read the same taps as the
+    four scattered loads: num / den agree to fp32 rounding of the bilinear form,
+    including frame-edge footprints (a grid wider than the field of view)."""
+    import ctypes as C
+    import torch
+    from paper_2005_11976_b200 import _device as D, _native as N
+    if kind == "cyl":
+        grid = CylGrid(14, 24, 12, 6.0, 10.0, Pose.tilt(0.25, -0.1, [0.4, -0.2, 0.3]))
+    else:
+        grid = CartGrid.centered(13, 11, 15, 0.8, center=(0.3, -0.2, 0.1))
+    geom = ScanGeometry(300.0, 150.0, 30, 26, 0.3, (14.5, 12.5), P.full_turn_angles(7))
+    nv = geom.n_proj
+    corr = torch.as_tensor(rng.standard_normal((nv, geom.det_rows, geom.det_cols),
+                                               dtype=np.float32), device="cuda")
+    dets = D.upload_f64(D.det_view_table(geom, range(nv)))
+    g = D.grid_c(grid)
+    b = D.batch_c(nv, geom.det_rows, geom.det_cols)
+    nq = int(N.load_library().ct_quads_floats(C.byref(b)))
+    quads = torch.empty(nq, device="cuda")
+    N.call("ct_pack_quads", D.ptr(corr), C.byref(b), D.ptr(quads), D.stream_handle())
+    res = []
+    for q in (None, quads):
+        num = torch.empty(grid.shape, device="cuda")
+        den = torch.empty(grid.shape, device="cuda")
+        if kind == "cyl":
+            trig = D.upload_f64(D.trig_table(grid))
+            N.call("ct_bp_cyl", D.ptr(corr), D.ptr(q), D.ptr(dets), C.byref(b), C.byref(g),
+                   D.ptr(trig), D.ptr(num), D.ptr(den), 0, D.stream_handle())
+        else:
+            N.call("ct_bp_cart", D.ptr(corr), D.ptr(q), D.ptr(dets), C.byref(b), C.byref(g),
+                   D.ptr(num), D.ptr(den), 0, D.stream_handle())
+        res.append((num, den))
+    (n0, d0), (n1, d1) = res
+    assert (d0 > 0).any() and (d0 == 0).any()          # touched and untouched voxels
+    assert torch.equal(d0 > 0, d1 > 0)
+    assert torch.allclose(d0, d1, rtol=1e-6, atol=1e-6)
+    assert torch.allclose(n0, n1, rtol=1e-5, atol=1e-5)

@@ -134,7 +134,8 @@ def c4():
             fp_t += t
             num = torch.empty(grid.shape, device="cuda")
             den = torch.empty(grid.shape, device="cuda")
-            t, _ = timed(lambda: e.bp_partial(run.corr, slots, len(s), num, den))
+            t, _ = timed(lambda: (e.pack_quads(run.corr, len(s), run.quads),
+                                  e.bp_partial(run.corr, slots, len(s), num, den, run.quads)))
             bp_t += t
         out[name] = {"fp_all_views_s": fp_t, "bp_all_views_s": bp_t}
     return out
