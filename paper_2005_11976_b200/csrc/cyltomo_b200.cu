@@ -262,11 +262,13 @@ __device__ __forceinline__ f32x2 atan2x_poly2(f32x2 s) {
 //    in [0, 2 pi).  s and d0 are in r-index units, the h index is linear in k:
 //        s = es + k*is,   h index + 1 = eh + k*ih,
 //    and ct = phi / dtheta + 0.5 folds the theta index offset (+1 halo, -0.5
-//    cell centre).  A ray spans < pi in theta, so indices stay below 1.5 n_theta
-//    + 1: the gather layout carries those rows (CylGeo::gather_rows).
+//    cell centre).  A ray spans < pi in theta; one that crosses theta = 2 pi
+//    (wrap) has its rows past n_theta wrapped in the integer cell index
+//    (CylGeo::gather_index<true>), taken warp-uniformly by march().
 struct RayF {
   float ex, ey, ez, ix, iy, iz;   // Cartesian, and the cylindrical nearest mode
   float es, is, eh, ih, d0, d2, ct;
+  bool wrap;                      // cylindrical: the ray's theta index passes n_theta
 };
 
 // One sample's trilinear cell: bit patterns of floor(index + 1) (+0x4B000000,
@@ -291,7 +293,7 @@ struct CylGeo {
   float inv_dr, inv_dth, inv_dh, h_off, h_off1, nr_m1, nh_m1;
   // gather layout: cells (nh+1, T, nr+1); CT_GATHER_HFAST stores them
   // (T, nr+1, nh+1), h fastest
-  unsigned cell_kstride, cell_jstride, cell_istride, idx_bias;
+  unsigned cell_kstride, cell_jstride, cell_istride, idx_bias, jb_wrap;
 
   __host__ void init(const float* m, const float* gather, const ct_cyl_grid& g) {
     mu = m;
@@ -317,9 +319,10 @@ struct CylGeo {
     cell_kstride = (unsigned)gather_rows(g.n_theta) * cell_jstride;
 #endif
     idx_bias = 0u - B * (cell_kstride + cell_jstride + cell_istride);  // mod 2^32
+    jb_wrap = B + (unsigned)g.n_theta;
   }
-  // theta rows of the gather layout: indices -1 .. 1.5 n_theta + 1 (see RayF)
-  __host__ __device__ static int gather_rows(int n_theta) { return n_theta + (n_theta + 1) / 2 + 2; }
+  // theta rows of the gather layout: indices -1 .. n_theta - 1 (see RayF)
+  __host__ __device__ static int gather_rows(int n_theta) { return n_theta + 1; }
 
   // _kernels.py:170-204 (same operation order)
   __device__ __forceinline__ bool interval(const double s[3], const double d[3], double& t0,
@@ -387,8 +390,11 @@ struct CylGeo {
       phi = atan2(e[1], e[0]);
     }
     // shift phi by 2 pi so the smallest theta of samples 0..n-1 is in [0, 2 pi)
-    const double th_min = phi + atan2(fmin(es, es + (n - 1) * is), d0);
+    const double s_last = es + (n - 1) * is;
+    const double th_min = phi + atan2(fmin(es, s_last), d0);
     phi -= kTwoPi * floor(th_min / kTwoPi);
+    // theta index passes n_theta (the fp32 index stays below n_theta + 1 otherwise)
+    ry.wrap = (phi + atan2(fmax(es, s_last), d0)) * ((double)nt / kTwoPi) > nt - 1e-3;
     const double idr = (double)nr / radius, d0i = fmax(d0 * idr, 1e-30);
     ry.es = (float)(es * idr);
     ry.is = (float)(is * idr);
@@ -454,11 +460,15 @@ struct CylGeo {
   }
 
   // gather-layout cell index (modular uint32; one constant for all offsets)
+  template <bool WRAP>
   __device__ __forceinline__ int gather_index(const Cell& c) const {
+    // WRAP (rays crossing theta = 2 pi): rows past n_theta wrap onto the
+    // primary rows (integer ops)
+    const unsigned jb = (WRAP && c.jb > jb_wrap) ? c.jb - (unsigned)nt : c.jb;
 #if CT_GATHER_HFAST
-    return (int)(c.ib * cell_istride + c.jb * cell_jstride + c.kb + idx_bias);
+    return (int)(c.ib * cell_istride + jb * cell_jstride + c.kb + idx_bias);
 #else
-    return (int)(c.kb * cell_kstride + c.jb * cell_jstride + c.ib + idx_bias);
+    return (int)(c.kb * cell_kstride + jb * cell_jstride + c.ib + idx_bias);
 #endif
   }
 
@@ -581,6 +591,7 @@ struct CartGeo {
                                             RayF& ry) const {
     ry.ex = (float)e[0]; ry.ey = (float)e[1]; ry.ez = (float)e[2];
     ry.ix = (float)inc[0]; ry.iy = (float)inc[1]; ry.iz = (float)inc[2];
+    ry.wrap = false;
   }
   __device__ __forceinline__ Cell locate1(float k, const RayF& ry) const {
     return locate(fmaf(k, ry.ix, ry.ex), fmaf(k, ry.iy, ry.ey), fmaf(k, ry.iz, ry.ez));
@@ -606,6 +617,7 @@ struct CartGeo {
     ca.kb = __float_as_uint(t0); cb.kb = __float_as_uint(t1);
   }
 
+  template <bool WRAP>
   __device__ __forceinline__ int gather_index(const Cell& c) const {
     return (int)(c.kb * cell_kstride + c.jb * cell_jstride + c.ib + idx_bias);
   }
@@ -691,6 +703,90 @@ __host__ __device__ inline int lanes_for(int rows, int cols) {
 __host__ __device__ inline int tile_ww(int K) { return K == 1 ? CT_FP_WW1 : (K == 8 ? 2 : 4); }
 __host__ __device__ inline int tile_wh(int K) { return (32 / K) / tile_ww(K); }
 
+// Linear-interpolation march of samples [k, k_end) of one ray (+ the last
+// sample k_last when with_last), returning the fp32 sum of the values.
+template <class Geo, bool OCT, bool WRAP>
+__device__ __forceinline__ float march_linear(const Geo& geo, const RayF& ry, int k, int k_end,
+                                              bool with_last, float k_last) {
+  // Linear interpolation.  OCT: consecutive samples are half a voxel apart, so
+  // a sample in the same cell as its predecessor skips its (predicated-off)
+  // 32-byte load and reuses the live cell.  Plain: the same 8 values from mu.
+  // Same cells, weights and summation grouping either way.
+  //
+  // The chunk is marched as FP_CHAINS independent chains over consecutive
+  // sub-ranges, each with its own live cell: the chains' gathers are in
+  // flight together (a single chain serialises load -> evaluate -> next load
+  // through its cell registers), and one f32x2 locate serves two chains.
+  struct Chain {
+    int prev = -1;
+    float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pb = make_float4(0.f, 0.f, 0.f, 0.f);
+    float sum = 0.0f;
+  };
+  auto value = [&](Chain& ch, const Cell& c) -> float {
+    if (OCT) {
+      const int idx = geo.template gather_index<WRAP>(c);
+      if (idx != ch.prev) ld_cell(geo.oct + 2 * (size_t)(unsigned)idx, ch.pa, ch.pb);
+      ch.prev = idx;   // (unconditional: equal when not reloaded; no predicated move)
+      return trilinear_eval(ch.pa, ch.pb, c.w0, c.w1, c.w2);
+    }
+    float4 a, b, ca, cb;
+    geo.fetch_plain(c, a, b);
+    trilinear_coeffs(a, b, ca, cb);
+    return trilinear_eval(ca, cb, c.w0, c.w1, c.w2);
+  };
+  constexpr int NC = FP_CHAINS;
+  Chain ch[NC];
+  int kc[NC], ke[NC];
+  {
+    const int len = k_end - k;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      kc[c] = k + (c * len) / NC;
+      ke[c] = k + ((c + 1) * len) / NC;
+    }
+  }
+  // every chain has >= len/NC - 1 samples; 4 samples per iteration
+  const int iters = ((k_end - k) / NC) / (4 / NC);
+  f32x2 kf01 = pk((float)kc[0], (float)kc[1]);
+#pragma unroll FP_UNROLL
+  for (int it = 0; it < iters; ++it) {
+    Cell c0, c1, c2, c3;
+    if (NC == 2) {
+      // float sample counters (exact below 2^24): no int->float conversions
+      geo.locate2(kf01, ry, c0, c1);
+      geo.locate2(add2(kf01, dup2(1.0f)), ry, c2, c3);
+      kf01 = add2(kf01, dup2(2.0f));
+      const float a0 = value(ch[0], c0);
+      const float b0 = value(ch[1], c1);
+      const float a1 = value(ch[0], c2);
+      const float b1 = value(ch[1], c3);
+      ch[0].sum += a0 + a1;
+      ch[1].sum += b0 + b1;
+    } else {
+      geo.locate2(pk((float)kc[0], (float)kc[1]), ry, c0, c1);
+      geo.locate2(pk((float)kc[NC - 2], (float)kc[NC - 1]), ry, c2, c3);
+      ch[0].sum += value(ch[0], c0);
+      ch[1].sum += value(ch[1], c1);
+      ch[NC - 2].sum += value(ch[NC - 2], c2);
+      ch[NC - 1].sum += value(ch[NC - 1], c3);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) ++kc[c];
+    }
+  }
+  if (NC == 2) {
+    kc[0] += 2 * iters;
+    kc[1] += 2 * iters;
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+    for (; kc[c] < ke[c]; ++kc[c]) ch[c].sum += value(ch[c], geo.locate1((float)kc[c], ry));
+  float sum = ch[0].sum;
+#pragma unroll
+  for (int c = 1; c < NC; ++c) sum += ch[c].sum;
+  if (with_last) sum += value(ch[NC - 1], geo.locate1(k_last, ry));
+  return sum;
+}
+
 // One sub-ray, chunk `chunk` of `K`: returns this chunk's in-support sample
 // count and adds the fp32 sum of its interpolated values into acc (COUNT_ONLY:
 // chunk 0 returns the whole ray's count, without marching).
@@ -748,86 +844,13 @@ __device__ __forceinline__ int march(const Geo& geo, const ct_ray_view& v, doubl
     acc += sum;
     return (k_end - (chunk * n_int) / K) + ((own_last && last_in) ? 1 : 0);
   }
-  // Linear interpolation.  OCT: consecutive samples are half a voxel apart, so
-  // a sample in the same cell as its predecessor skips its (predicated-off)
-  // 32-byte load and reuses the live cell.  Plain: the same 8 values from mu.
-  // Same cells, weights and summation grouping either way.
-  //
-  // The chunk is marched as FP_CHAINS independent chains over consecutive
-  // sub-ranges, each with its own live cell: the chains' gathers are in
-  // flight together (a single chain serialises load -> evaluate -> next load
-  // through its cell registers), and one f32x2 locate serves two chains.
-  struct Chain {
-    int prev = -1;
-    float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pb = make_float4(0.f, 0.f, 0.f, 0.f);
-    float sum = 0.0f;
-  };
-  auto value = [&](Chain& ch, const Cell& c) -> float {
-    if (OCT) {
-      const int idx = geo.gather_index(c);
-      if (idx != ch.prev) ld_cell(geo.oct + 2 * (size_t)(unsigned)idx, ch.pa, ch.pb);
-      ch.prev = idx;   // (unconditional: equal when not reloaded; no predicated move)
-      return trilinear_eval(ch.pa, ch.pb, c.w0, c.w1, c.w2);
-    }
-    float4 a, b, ca, cb;
-    geo.fetch_plain(c, a, b);
-    trilinear_coeffs(a, b, ca, cb);
-    return trilinear_eval(ca, cb, c.w0, c.w1, c.w2);
-  };
-  constexpr int NC = FP_CHAINS;
-  Chain ch[NC];
-  int kc[NC], ke[NC];
-  {
-    const int len = k_end - k;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      kc[c] = k + (c * len) / NC;
-      ke[c] = k + ((c + 1) * len) / NC;
-    }
-  }
-  // every chain has >= len/NC - 1 samples; 4 samples per iteration
-  const int iters = ((k_end - k) / NC) / (4 / NC);
-  f32x2 kf01 = pk((float)kc[0], (float)kc[1]);
-#pragma unroll FP_UNROLL
-  for (int it = 0; it < iters; ++it) {
-    Cell c0, c1, c2, c3;
-    if (NC == 2) {
-      // float sample counters (exact below 2^24): no int->float conversions
-      geo.locate2(kf01, ry, c0, c1);
-      geo.locate2(add2(kf01, dup2(1.0f)), ry, c2, c3);
-      kf01 = add2(kf01, dup2(2.0f));
-      const float a0 = value(ch[0], c0);
-      const float b0 = value(ch[1], c1);
-      const float a1 = value(ch[0], c2);
-      const float b1 = value(ch[1], c3);
-      ch[0].sum += a0 + a1;
-      ch[1].sum += b0 + b1;
-    } else {
-      geo.locate2(pk((float)kc[0], (float)kc[1]), ry, c0, c1);
-      geo.locate2(pk((float)kc[NC - 2], (float)kc[NC - 1]), ry, c2, c3);
-      ch[0].sum += value(ch[0], c0);
-      ch[1].sum += value(ch[1], c1);
-      ch[NC - 2].sum += value(ch[NC - 2], c2);
-      ch[NC - 1].sum += value(ch[NC - 1], c3);
-#pragma unroll
-      for (int c = 0; c < NC; ++c) ++kc[c];
-    }
-  }
-  if (NC == 2) {
-    kc[0] += 2 * iters;
-    kc[1] += 2 * iters;
-  }
-#pragma unroll
-  for (int c = 0; c < NC; ++c)
-    for (; kc[c] < ke[c]; ++kc[c]) ch[c].sum += value(ch[c], geo.locate1((float)kc[c], ry));
-  sum = ch[0].sum;
-#pragma unroll
-  for (int c = 1; c < NC; ++c) sum += ch[c].sum;
-  Chain& B = ch[NC - 1];
-  if (own_last && last_in && geo.interp_nonzero(v.src, d, t_last)) {
-    const float kf = (float)n_int;
-    sum += value(B, geo.locate1(kf, ry));
-  }
+  const bool with_last = own_last && last_in && geo.interp_nonzero(v.src, d, t_last);
+  // rays crossing theta = 2 pi need the wrapped cell index; the choice is
+  // warp-uniform so the two loop versions never diverge within a warp
+  if (__any_sync(__activemask(), ry.wrap))
+    sum = march_linear<Geo, OCT, true>(geo, ry, k, k_end, with_last, (float)n_int);
+  else
+    sum = march_linear<Geo, OCT, false>(geo, ry, k, k_end, with_last, (float)n_int);
   acc += sum;
   return (k_end - (chunk * n_int) / K) + ((own_last && last_in) ? 1 : 0);
 }

@@ -162,9 +162,9 @@ class SartEngine:
 
     # -- launchers -------------------------------------------------------------
     def alloc_gather(self):
-        """Buffer for the FP gather layout (8 floats per voxel, 16B aligned)."""
-        torch = D.torch_mod()
-        if self.samp.nearest:
+        """Buffer for the FP gather layout (8 floats per voxel, 16B aligned);
+        None (plain-layout FP) in nearest mode or with CT_FP_GATHER=0."""
+        if self.samp.nearest or os.environ.get("CT_FP_GATHER", "1") == "0":
             return None
         return D.alloc_gather(self.grid, self.device)
 

@@ -14,7 +14,8 @@ from pathlib import Path
 KIND = [("fp_kernel<<unnamed>::CylGeo, 1", "fp_correction"),
         ("fp_kernel<<unnamed>::CylGeo, 2", "fp_residual"),
         ("bp_kernel<<unnamed>::CylVox, 2", "bp_update"),
-        ("pack_gather_cyl", "pack_gather")]
+        ("pack_gather_cyl", "pack_gather"),
+        ("pack_quads", "pack_quads")]
 
 FIELDS = {"duration_ms": ("gpu__time_duration.sum", 1.0),
           "dram_read_bytes": ("dram__bytes_read.sum", None),

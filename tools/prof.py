@@ -18,7 +18,8 @@ import paper_2005_11976_b200 as P
 from paper_2005_11976_b200 import workloads as W
 from paper_2005_11976_b200.recon import SartRun
 
-wl = W.c2_medium(n_views=args.views) if args.config == "c2" else W.c1_small()
+wl = (W.c2_medium(n_views=args.views) if args.config == "c2" else
+      W.c5_object(0) if args.config == "c5" else W.c1_small())
 vol = P.CylVolume(wl.grid, torch.as_tensor(wl.mu, device="cuda"))
 ps = P.forward_project_all(vol, wl.geom)
 run = SartRun(P.ProjectionSet(wl.geom, ps.images), wl.grid,
@@ -28,7 +29,8 @@ torch.cuda.synchronize()
 for _ in range(args.reps):
     run.eng.pack(run.mu, run.gather)
     run.eng.correction(run.mu, run.p_meas, slots, len(s), run.corr, run.gather)
-    run.eng.bp_update(run.corr, slots, len(s), run.upd)
+    run.eng.pack_quads(run.corr, len(s), run.quads)
+    run.eng.bp_update(run.corr, slots, len(s), run.upd, run.quads)
 run.eng.pack(run.mu, run.gather)
 run.eng.residual(run.mu, run.p_meas, run.all_slots, wl.geom.n_proj, run.resid_cur, run.gather)
 torch.cuda.synchronize()
