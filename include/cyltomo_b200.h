@@ -212,15 +212,15 @@ int ct_sart_update(const float *num, const float *den, int64_t offset, int64_t c
                    const ct_update *upd, ct_stream_t stream);
 
 /* ---- gather layout for the forward projector ------------------------------ */
-/* Number of floats of the gather buffer: 8 per cell, cells (n_h+1, T, n_r+1)
- * with T = n_theta + (n_theta+1)/2 + 2 for a cylindrical grid (theta rows
- * -1 .. 1.5 n_theta + 1, periodic), (n_z+1, n_y+1, n_x+1) for a Cartesian one. */
+/* Number of floats of the gather buffer: 8 per cell, cells (n_h+1, n_theta+1,
+ * n_r+1) for a cylindrical grid, (n_z+1, n_y+1, n_x+1) for a Cartesian one,
+ * r (x) fastest; each h (z) layer is padded by < 256 cells so that the cell
+ * index needs no bias term. */
 int64_t ct_gather_floats_cyl(const ct_cyl_grid *grid);
 int64_t ct_gather_floats_cart(const ct_cart_grid *grid);
 /* Cell (kc, jc, ic) holds the trilinear corner (k, j, i) = (kc-1, jc-1, ic-1)
- * with a one-cell halo at index -1 (r/h: a copy of index 0; theta: indices are
- * taken modulo n_theta, so a ray's theta range never needs a wrap) as the
- * coefficients of
+ * with a one-cell halo at index -1 (r/h: a copy of index 0; theta: the wrapped
+ * row n_theta-1) as the coefficients of
  *   f(wr, wt, wh) = c0 + cr wr + ct wt + crt wr wt + ch wh + crh wr wh + cth wt wh
  *                   + crth wr wt wh,
  * stored (c0, cr, ct, crt, ch, crh, cth, crth), of the 8 corner values

@@ -32,9 +32,6 @@
 
 namespace {
 
-#ifndef CT_GATHER_HFAST
-#define CT_GATHER_HFAST 0
-#endif
 constexpr double kPi = 3.141592653589793;
 constexpr double kTwoPi = 2.0 * kPi;
 constexpr float kTwoPiF = 6.28318530717958647692f;
@@ -284,6 +281,16 @@ constexpr unsigned kMagicBits = 0x4B000000u;   // bits of 2^23
 // grid policies: support interval (fp64), last-sample test (fp64) and the
 // fp32 trilinear sample
 // ---------------------------------------------------------------------------
+// Gather-layout strides in cells: r (x) fastest, row stride js = n + 1, layer
+// stride ks = rows * js padded so that ks + js + 1 == 0 (mod 256).  The floor
+// bit patterns carry the magic 2^23 = 75 * 2^24 (bits B = 0x4B000000), so
+// B * (ks + js + 1) == 0 (mod 2^32) and kb*ks + jb*js + ib is the cell index
+// itself: no bias term per sample.
+__host__ __device__ inline unsigned gather_layer_stride(unsigned rows, unsigned js) {
+  const unsigned ks = rows * js;
+  return ks + (256u - (ks + js + 1u) % 256u) % 256u;
+}
+
 struct CylGeo {
   const float* __restrict__ mu;
   const float4* __restrict__ oct;  // gather layout (ct_pack_gather_cyl) or null
@@ -291,9 +298,8 @@ struct CylGeo {
   double radius, half_h;
   // fp32 sampling constants
   float inv_dr, inv_dth, inv_dh, h_off, h_off1, nr_m1, nh_m1;
-  // gather layout: cells (nh+1, T, nr+1); CT_GATHER_HFAST stores them
-  // (T, nr+1, nh+1), h fastest
-  unsigned cell_kstride, cell_jstride, cell_istride, idx_bias, jb_wrap;
+  // gather layout: cells (nh+1, nt+1, nr+1), strides (ks, js, 1)
+  unsigned cell_kstride, cell_jstride, jb_wrap;
 
   __host__ void init(const float* m, const float* gather, const ct_cyl_grid& g) {
     mu = m;
@@ -309,16 +315,8 @@ struct CylGeo {
     nh_m1 = (float)(g.n_h - 1);
     h_off1 = h_off + 1.0f;
     const unsigned B = kMagicBits;
-#if CT_GATHER_HFAST
-    cell_kstride = 1u;
-    cell_istride = (unsigned)g.n_h + 1u;
-    cell_jstride = ((unsigned)g.n_r + 1u) * cell_istride;
-#else
-    cell_istride = 1u;
     cell_jstride = (unsigned)g.n_r + 1u;
-    cell_kstride = (unsigned)gather_rows(g.n_theta) * cell_jstride;
-#endif
-    idx_bias = 0u - B * (cell_kstride + cell_jstride + cell_istride);  // mod 2^32
+    cell_kstride = gather_layer_stride((unsigned)gather_rows(g.n_theta), cell_jstride);
     jb_wrap = B + (unsigned)g.n_theta;
   }
   // theta rows of the gather layout: indices -1 .. n_theta - 1 (see RayF)
@@ -465,11 +463,7 @@ struct CylGeo {
     // WRAP (rays crossing theta = 2 pi): rows past n_theta wrap onto the
     // primary rows (integer ops)
     const unsigned jb = (WRAP && c.jb > jb_wrap) ? c.jb - (unsigned)nt : c.jb;
-#if CT_GATHER_HFAST
-    return (int)(c.ib * cell_istride + jb * cell_jstride + c.kb + idx_bias);
-#else
-    return (int)(c.kb * cell_kstride + jb * cell_jstride + c.ib + idx_bias);
-#endif
+    return (int)(c.kb * cell_kstride + jb * cell_jstride + c.ib);
   }
 
   // the same 8 values from the plain mu layout (r/h clamp, theta modulo n_theta)
@@ -506,7 +500,7 @@ struct CartGeo {
   int nz, ny, nx;
   double vs, lo[3], hi[3];
   float inv_vs, off[3], off1[3], nx_m1, ny_m1, nz_m1;
-  unsigned cell_kstride, cell_jstride, idx_bias;   // gather layout (nz+1, ny+1, nx+1)
+  unsigned cell_kstride, cell_jstride;   // gather layout (nz+1, ny+1, nx+1), strides (ks, js, 1)
 
   __host__ void init(const float* m, const float* gather, const ct_cart_grid& g) {
     mu = m;
@@ -523,8 +517,7 @@ struct CartGeo {
     for (int a = 0; a < 3; ++a) off1[a] = off[a] + 1.0f;
     const unsigned B = kMagicBits;
     cell_jstride = (unsigned)nx + 1u;
-    cell_kstride = ((unsigned)ny + 1u) * cell_jstride;
-    idx_bias = 0u - B * (cell_kstride + cell_jstride + 1u);          // mod 2^32
+    cell_kstride = gather_layer_stride((unsigned)ny + 1u, cell_jstride);
   }
 
   // _kernels.py:207-231
@@ -619,7 +612,7 @@ struct CartGeo {
 
   template <bool WRAP>
   __device__ __forceinline__ int gather_index(const Cell& c) const {
-    return (int)(c.kb * cell_kstride + c.jb * cell_jstride + c.ib + idx_bias);
+    return (int)(c.kb * cell_kstride + c.jb * cell_jstride + c.ib);
   }
 
   __device__ __forceinline__ void fetch_plain(const Cell& c, float4& a, float4& b) const {
@@ -1525,24 +1518,25 @@ __global__ void resample_cyl_kernel(const float* __restrict__ src_mu, ct_cyl_gri
 // 32-byte sector, so one FP sample is one 256-bit load instead of 8 scattered
 // loads.
 // ---------------------------------------------------------------------------
+// one h-layer (blockIdx.y = kc) per grid row; cells past the layer's rows are
+// the stride padding (zeroed, never read)
 __global__ void pack_gather_cyl_kernel(const float* __restrict__ mu, int nh, int nt, int nr,
-                                       float4* __restrict__ oct) {
-  // cells (kc, jc, ic), kc in [0, nh], jc in [0, T), ic in [0, nr]: corner
-  // (kc-1, jc-1, ic-1); index -1 is a halo (r/h: copy of 0), theta modulo nt
-  const int T = CylGeo::gather_rows(nt);
-  const int64_t n = (int64_t)(nh + 1) * T * (nr + 1);
-  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= n) return;
-#if CT_GATHER_HFAST
-  const int kc = (int)(m % (nh + 1)), ic = (int)((m / (nh + 1)) % (nr + 1));
-  const int jc = (int)(m / ((int64_t)(nh + 1) * (nr + 1)));
-#else
-  const int ic = (int)(m % (nr + 1)), jc = (int)((m / (nr + 1)) % T);
-  const int kc = (int)(m / ((int64_t)(nr + 1) * T));
-#endif
+                                       unsigned ks, float4* __restrict__ oct) {
+  // cells (kc, jc, ic), kc in [0, nh], jc in [0, nt], ic in [0, nr]: corner
+  // (kc-1, jc-1, ic-1); index -1 is a halo (r/h: copy of 0; theta: row nt-1)
+  const unsigned rem = blockIdx.x * blockDim.x + threadIdx.x;
+  if (rem >= ks) return;
+  const int kc = blockIdx.y;
+  const size_t m = (size_t)kc * ks + rem;
+  const unsigned js = (unsigned)nr + 1u;
+  const int jc = (int)(rem / js), ic = (int)(rem % js);
+  if (jc > nt) {
+    oct[2 * m] = oct[2 * m + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
   const int i = max(ic - 1, 0), i1 = min(ic, nr - 1);
   const int k = max(kc - 1, 0), k1 = min(kc, nh - 1);
-  const int j = (jc + nt - 1) % nt, j1 = jc % nt;
+  const int j = (jc == 0) ? nt - 1 : jc - 1, j1 = (jc == nt) ? 0 : jc;
   auto M = [&](int kk, int jj, int ii) { return __ldg(mu + ((int64_t)kk * nt + jj) * nr + ii); };
   float4 ca, cb;
   trilinear_coeffs(make_float4(M(k, j, i), M(k, j, i1), M(k, j1, i), M(k, j1, i1)),
@@ -1552,13 +1546,18 @@ __global__ void pack_gather_cyl_kernel(const float* __restrict__ mu, int nh, int
 }
 
 __global__ void pack_gather_cart_kernel(const float* __restrict__ mu, int nz, int ny, int nx,
-                                        float4* __restrict__ oct) {
+                                        unsigned ks, float4* __restrict__ oct) {
   // cells (kc, jc, ic) in [0, n] per axis: corner (kc-1, jc-1, ic-1)
-  const int64_t n = (int64_t)(nz + 1) * (ny + 1) * (nx + 1);
-  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= n) return;
-  const int ic = (int)(m % (nx + 1)), jc = (int)((m / (nx + 1)) % (ny + 1));
-  const int kc = (int)(m / ((int64_t)(nx + 1) * (ny + 1)));
+  const unsigned rem = blockIdx.x * blockDim.x + threadIdx.x;
+  if (rem >= ks) return;
+  const int kc = blockIdx.y;
+  const size_t m = (size_t)kc * ks + rem;
+  const unsigned js = (unsigned)nx + 1u;
+  const int jc = (int)(rem / js), ic = (int)(rem % js);
+  if (jc > ny) {
+    oct[2 * m] = oct[2 * m + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
   const int i = max(ic - 1, 0), i1 = min(ic, nx - 1);
   const int j = max(jc - 1, 0), j1 = min(jc, ny - 1);
   const int k = max(kc - 1, 0), k1 = min(kc, nz - 1);
@@ -1584,12 +1583,14 @@ __global__ void pack_quads_kernel(const float* __restrict__ corr, int64_t n, int
                          (ru && rv) ? __ldg(p + cols + 1) : 0.0f);
 }
 
-int64_t gather_cells_cyl(const ct_cyl_grid& g) {
-  return (int64_t)(g.n_h + 1) * CylGeo::gather_rows(g.n_theta) * (g.n_r + 1);
+unsigned gather_ks_cyl(const ct_cyl_grid& g) {
+  return gather_layer_stride((unsigned)CylGeo::gather_rows(g.n_theta), (unsigned)g.n_r + 1u);
 }
-int64_t gather_cells_cart(const ct_cart_grid& g) {
-  return (int64_t)(g.n_z + 1) * (g.n_y + 1) * (g.n_x + 1);
+unsigned gather_ks_cart(const ct_cart_grid& g) {
+  return gather_layer_stride((unsigned)g.n_y + 1u, (unsigned)g.n_x + 1u);
 }
+int64_t gather_cells_cyl(const ct_cyl_grid& g) { return (int64_t)(g.n_h + 1) * gather_ks_cyl(g); }
+int64_t gather_cells_cart(const ct_cart_grid& g) { return (int64_t)(g.n_z + 1) * gather_ks_cart(g); }
 
 // Beer-Lambert p = -ln(I / I0) (cyltomo/projector.py:169-181), fp64 log of the
 // fp32 inputs; flat field is a scalar or one image broadcast over the views.
@@ -2140,9 +2141,10 @@ int ct_pack_gather_cyl(const float* mu, const ct_cyl_grid* grid, float* gather,
   if (rc) return rc;
   if (!mu || !gather) return set_err(CT_ERR_ARG, "null mu/gather");
   if (reinterpret_cast<uintptr_t>(gather) % 16) return set_err(CT_ERR_ARG, "gather not 16B-aligned");
-  const int64_t n = gather_cells_cyl(*grid);
-  pack_gather_cyl_kernel<<<blocks_for(n, 256), 256, 0, CT_STREAM(stream)>>>(
-      mu, grid->n_h, grid->n_theta, grid->n_r, reinterpret_cast<float4*>(gather));
+  if (grid->n_h + 1 > 65535) return set_err(CT_ERR_ARG, "gather layout: n_h + 1 > 65535");
+  const unsigned ks = gather_ks_cyl(*grid);
+  pack_gather_cyl_kernel<<<dim3(blocks_for(ks, 256), grid->n_h + 1), 256, 0, CT_STREAM(stream)>>>(
+      mu, grid->n_h, grid->n_theta, grid->n_r, ks, reinterpret_cast<float4*>(gather));
   return check_launch("pack_gather_cyl_kernel");
 }
 
@@ -2152,9 +2154,10 @@ int ct_pack_gather_cart(const float* mu, const ct_cart_grid* grid, float* gather
   if (rc) return rc;
   if (!mu || !gather) return set_err(CT_ERR_ARG, "null mu/gather");
   if (reinterpret_cast<uintptr_t>(gather) % 16) return set_err(CT_ERR_ARG, "gather not 16B-aligned");
-  const int64_t n = gather_cells_cart(*grid);
-  pack_gather_cart_kernel<<<blocks_for(n, 256), 256, 0, CT_STREAM(stream)>>>(
-      mu, grid->n_z, grid->n_y, grid->n_x, reinterpret_cast<float4*>(gather));
+  if (grid->n_z + 1 > 65535) return set_err(CT_ERR_ARG, "gather layout: n_z + 1 > 65535");
+  const unsigned ks = gather_ks_cart(*grid);
+  pack_gather_cart_kernel<<<dim3(blocks_for(ks, 256), grid->n_z + 1), 256, 0, CT_STREAM(stream)>>>(
+      mu, grid->n_z, grid->n_y, grid->n_x, ks, reinterpret_cast<float4*>(gather));
   return check_launch("pack_gather_cart_kernel");
 }
 
