@@ -132,33 +132,60 @@ def batch_c(n_batch: int, rows: int, cols: int, view_ids=None) -> N.BatchC:
     return b
 
 
+def _view_rotations(geom: ScanGeometry, views) -> np.ndarray:
+    """(n, 3, 3) rot_z(-phi_i) with libm cos/sin, as geometry.rot_z builds it."""
+    ang = [-float(geom.stage_angles[int(i)]) for i in views]
+    c = np.array([math.cos(a) for a in ang])
+    s = np.array([math.sin(a) for a in ang])
+    rz = np.zeros((len(ang), 3, 3))
+    rz[:, 0, 0], rz[:, 0, 1], rz[:, 1, 0], rz[:, 1, 1], rz[:, 2, 2] = c, -s, s, c, 1.0
+    return rz
+
+
+def _matvec(m, v) -> np.ndarray:
+    """Per-item m @ v over a stack (numpy's per-matrix matvec, the same
+    arithmetic as the reference's 3x3 @ 3 products)."""
+    return np.matmul(m, v[..., None])[..., 0]
+
+
 def ray_view_table(grid, geom: ScanGeometry, views) -> np.ndarray:
     """(n, 12) fp64: src, pixel-(0,0) origin, du, dv per view.
 
     Cylindrical grids get the basis mapped into the grid-aligned frame with
     the reference's expressions (cyltomo/projector.py:83-88); Cartesian grids
-    use the world basis (cyltomo/projector.py:110-116).
+    use the world basis (cyltomo/projector.py:110-116).  All views at once,
+    bit-identical to the per-view geometry.view_basis expressions
+    (tests/test_host.py::TestGeometryBitExact).
     """
-    out = np.empty((len(views), 12), dtype=np.float64)
+    views = [int(i) for i in views]
+    if not views:
+        return np.empty((0, 12), dtype=np.float64)
+    rz = _view_rotations(geom, views)
+    u0, v0 = geom.principal_point
+    p = geom.pixel_pitch
+    src = _matvec(rz, np.array([0.0, -geom.sod, 0.0]))
+    origin = _matvec(rz, np.array([-u0 * p, geom.sdd - geom.sod, -v0 * p]))
+    du = _matvec(rz, np.array([p, 0.0, 0.0]))
+    dv = _matvec(rz, np.array([0.0, 0.0, p]))
     if isinstance(grid, CylGrid):
         a = grid.rotation.T
         t = grid.pose.t
-        for n, i in enumerate(views):
-            src, origin, du, dv = view_basis(geom, int(i))
-            out[n] = np.concatenate([a @ (src - t), a @ (origin - t), a @ du, a @ dv])
+        parts = [_matvec(a, src - t), _matvec(a, origin - t), _matvec(a, du), _matvec(a, dv)]
     else:
-        for n, i in enumerate(views):
-            out[n] = np.concatenate(view_basis(geom, int(i)))
-    return out
+        parts = [src, origin, du, dv]
+    return np.ascontiguousarray(np.concatenate(parts, axis=1), dtype=np.float64)
 
 
 def det_view_table(geom: ScanGeometry, views) -> np.ndarray:
     """(n, 8) fp64: u0, v0, pitch, sdd, sod, cos(phi), sin(phi), 0 (projector.py:151-152)."""
-    out = np.zeros((len(views), 8), dtype=np.float64)
+    idx = np.asarray([int(i) for i in views], dtype=np.int64)
+    phi = np.asarray(geom.stage_angles, dtype=np.float64)[idx]
+    out = np.zeros((len(idx), 8), dtype=np.float64)
     u0, v0 = geom.principal_point
-    for n, i in enumerate(views):
-        phi = geom.stage_angles[int(i)]
-        out[n, :7] = (u0, v0, geom.pixel_pitch, geom.sdd, geom.sod, np.cos(phi), np.sin(phi))
+    out[:, 0], out[:, 1], out[:, 2] = u0, v0, geom.pixel_pitch
+    out[:, 3], out[:, 4] = geom.sdd, geom.sod
+    out[:, 5] = [np.cos(x) for x in phi]
+    out[:, 6] = [np.sin(x) for x in phi]
     return out
 
 

@@ -160,6 +160,34 @@ class SartEngine:
         self.row_thr = D.upload_f64(ROW_SUM_SKIP_FRACTION * max_row)
         return max_row
 
+    def prepare_thresholds_async(self):
+        """prepare_thresholds without a host round trip: the skip thresholds
+        are computed on the device, and the row maxima are copied to pinned
+        host memory behind an event.  Returns (max_row_host, event); the
+        caller checks for empty views once the event has completed
+        (check_empty_views) -- the kernels treat an empty view as all-skipped,
+        so work queued before the check is harmless."""
+        torch = D.torch_mod()
+        n = len(self.views)
+        out = torch.zeros(n, dtype=torch.float64, device=self.device)
+        b = D.batch_c(n, self.rows, self.cols)
+        fn = "ct_rowsum_max_cyl" if self.cyl else "ct_rowsum_max_cart"
+        N.call(fn, C.byref(self.gc), D.ptr(self.fp_views), C.byref(b), C.byref(self.samp),
+               D.ptr(out), D.stream_handle())
+        self.row_thr = out * ROW_SUM_SKIP_FRACTION
+        host = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        host.copy_(out, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        return host, ev
+
+    def check_empty_views(self, max_row, order_slots=None) -> None:
+        """EmptyView for the first empty view in processing order."""
+        check = range(len(self.views)) if order_slots is None else order_slots
+        for slot in check:
+            if max_row[slot] <= 0.0:
+                raise EmptyView(f"view {int(self.views[slot])} misses the volume entirely")
+
     # -- launchers -------------------------------------------------------------
     def alloc_gather(self):
         """Buffer for the FP gather layout (8 floats per voxel, 16B aligned);
@@ -308,6 +336,66 @@ def _initial_mu(grid, cfg: SartConfig, device):
     return D.to_device(init.mu, device=device).clone()
 
 
+class _StreamedUpload:
+    """Host projections -> device in subset order on a copy stream, so the
+    upload overlaps the first subsets' compute: subset k's views are copied
+    (one async copy per view from page-locked memory) while subset k-1
+    computes, and the compute stream waits on subset k's event just before
+    its first use.  Only for page-locked host arrays (SartRun uploads pageable
+    ones in one synchronous copy: staging them would cost a host memcpy)."""
+
+    @staticmethod
+    def applies(images) -> bool:
+        torch = D.torch_mod()
+        arr = np.asarray(images)
+        return (arr.dtype == np.float32 and arr.flags.c_contiguous
+                and torch.from_numpy(arr).is_pinned())
+
+    def __init__(self, images, subsets, device):
+        torch = D.torch_mod()
+        host = torch.from_numpy(np.asarray(images))
+        self.host = host
+        self.dev = torch.empty(tuple(host.shape), dtype=torch.float32, device=device)
+        self.subsets = subsets
+        self.stream = torch.cuda.Stream(device)
+        self.stream.wait_stream(torch.cuda.current_stream())
+        self.events = [None] * len(subsets)
+        self.issued = 0
+        self.waited = [False] * len(subsets)
+        self.issue(0)
+
+    def issue(self, k: int) -> None:
+        """Queue the copies of subsets up to k (inclusive)."""
+        torch = D.torch_mod()
+        while self.issued <= min(k, len(self.subsets) - 1):
+            with torch.cuda.stream(self.stream):
+                for v in self.subsets[self.issued]:
+                    self.dev[int(v)].copy_(self.host[int(v)], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.stream)
+            self.events[self.issued] = ev
+            self.issued += 1
+
+    def before_subset(self, k: int) -> None:
+        """Make subset k resident for the compute stream (and queue k+1)."""
+        if all(self.waited):
+            return
+        torch = D.torch_mod()
+        self.issue(k + 1)
+        if not self.waited[k]:
+            torch.cuda.current_stream().wait_event(self.events[k])
+            self.waited[k] = True
+
+    def finish(self) -> None:
+        """Everything resident for the compute stream."""
+        for k in range(len(self.subsets)):
+            self.before_subset(k)
+
+    @property
+    def done(self) -> bool:
+        return all(self.waited)
+
+
 class SartRun:
     """A prepared (OS-)SART reconstruction: tables, thresholds, buffers.
 
@@ -327,9 +415,17 @@ class SartRun:
         self.mu = _initial_mu(grid, cfg, dev)
         self.order = projection_order(cfg, ps.geom.n_proj)
         self.subsets = make_subsets(self.order, cfg.n_subsets)
-        self.eng.prepare_thresholds(order_slots=self.order)
+        # row maxima / thresholds stay on the device; the EmptyView check runs
+        # once their host copy has landed (run(), after the first pass is queued)
+        self._max_row, self._max_row_ev = self.eng.prepare_thresholds_async()
+        self._empty_checked = False
         self.weights = _device_weights(cfg, grid.shape, dev)
-        self.p_meas = D.to_device(ps.images, device=dev)
+        if ps.on_device or not _StreamedUpload.applies(ps.images):
+            self._p_meas = D.to_device(ps.images, device=dev)
+            self._upload = None
+        else:
+            self._upload = _StreamedUpload(ps.images, self.subsets, dev)
+            self._p_meas = self._upload.dev
         self.subset_slots = [D.upload_i32(s) for s in self.subsets]
         self.all_slots = D.upload_i32(np.arange(ps.geom.n_proj))
         nmax = max(len(s) for s in self.subsets)
@@ -359,19 +455,39 @@ class SartRun:
         b.record()
         self.launch_log.append((kind, s, a, b))
 
-    def _pass_body(self, residual: bool) -> None:
+    @property
+    def p_meas(self):
+        """The measured projections on the device (complete: any streamed
+        upload is finished for the current stream first)."""
+        if self._upload is not None:
+            self._upload.finish()
+        return self._p_meas
+
+    def check_empty_views(self) -> None:
+        """Raise EmptyView (reference order) once the row maxima are on the host."""
+        if not self._empty_checked:
+            self._max_row_ev.synchronize()
+            self._empty_checked = True
+            self.eng.check_empty_views(self._max_row.numpy(), order_slots=self.order)
+
+    def _pass_body(self, residual: bool, after_updates=None) -> None:
         e = self.eng
+        up = self._upload if (self._upload is not None and not self._upload.done) else None
         for k, (s, slots) in enumerate(zip(self.subsets, self.subset_slots)):
+            if up is not None:
+                up.before_subset(k)
             self._timed("pack_gather", k, e.pack, self.mu, self.gather)
-            self._timed("fp_correction", k, e.correction, self.mu, self.p_meas, slots, len(s),
+            self._timed("fp_correction", k, e.correction, self.mu, self._p_meas, slots, len(s),
                         self.corr, self.gather)
             self._timed("pack_quads", k, e.pack_quads, self.corr, len(s), self.quads)
             self._timed("bp_update", k, e.bp_update, self.corr, slots, len(s), self.upd,
                         self.quads)
+        if after_updates is not None:
+            after_updates()
         if residual:
             self.resid_cur.zero_()
             self._timed("pack_gather", -1, e.pack, self.mu, self.gather)
-            self._timed("fp_residual", -1, e.residual, self.mu, self.p_meas, self.all_slots,
+            self._timed("fp_residual", -1, e.residual, self.mu, self._p_meas, self.all_slots,
                         self.ps.geom.n_proj, self.resid_cur, self.gather)
 
     def run_pass(self, residual: bool | None = None) -> None:
@@ -385,6 +501,8 @@ class SartRun:
             torch = D.torch_mod()
             g = self._graphs.get(want)
             if g is None:
+                if self._upload is not None:
+                    self._upload.finish()
                 # low-level capture on a side stream: torch.cuda.graph() would
                 # also gc.collect() and empty the caching allocator every time
                 g = torch.cuda.CUDAGraph()
@@ -406,16 +524,47 @@ class SartRun:
             self.resid[k:k + 1].copy_(self.resid_cur)
         self.passes_done += 1
 
+    def _run_pass_hooked(self, after_updates) -> None:
+        """run_pass (eager) with a hook queued after the last subset's update."""
+        want = self.cfg.compute_residuals
+        self._pass_body(want, after_updates)
+        if want:
+            k = min(self.passes_done, self.resid.numel() - 1)
+            self.resid[k:k + 1].copy_(self.resid_cur)
+        self.passes_done += 1
+
     def run(self):
         torch = D.torch_mod()
         t0 = time.perf_counter()
-        for _ in range(self.cfg.n_iterations):
-            self.run_pass()
+        host_mu = None
+        for it in range(self.cfg.n_iterations):
+            last = it == self.cfg.n_iterations - 1
+            if last and not self.ps.on_device and not self.use_graph:
+                # the final volume is complete after the last subset's update:
+                # copy it out on a side stream while the residual FP runs
+                host_mu = torch.empty(tuple(self.mu.shape), dtype=self.mu.dtype,
+                                      pin_memory=True)
+                copy_stream = torch.cuda.Stream(self.eng.device)
+
+                def d2h():
+                    copy_stream.wait_stream(torch.cuda.current_stream())
+                    with torch.cuda.stream(copy_stream):
+                        host_mu.copy_(self.mu, non_blocking=True)
+                    self.mu.record_stream(copy_stream)
+                self._run_pass_hooked(d2h)
+            else:
+                self.run_pass()
+            self.check_empty_views()
         torch.cuda.synchronize(self.eng.device)
         wall = time.perf_counter() - t0
         residuals = ([math.sqrt(float(x)) for x in D.to_host(self.resid)]
                      if self.cfg.compute_residuals else [])
-        mu = self.mu if self.ps.on_device else D.to_host(self.mu, pinned=True)
+        if self.ps.on_device:
+            mu = self.mu
+        elif host_mu is not None:
+            mu = host_mu.numpy()
+        else:
+            mu = D.to_host(self.mu, pinned=True)
         vol = _volume_cls(self.grid)._trusted(self.grid, mu)
         return vol, ReconReport(residuals=residuals, wall_time=wall,
                                 config=_config_echo(self.cfg))

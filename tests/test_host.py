@@ -35,6 +35,28 @@ class TestGeometryBitExact:
         tab = D.ray_view_table(grid, desk(), range(8))
         assert np.array_equal(tab, golden_small["geo_aligned_basis"])
 
+    def test_tables_match_per_view_expressions(self, rng):
+        """The all-views tables equal the per-view reference expressions
+        (view_basis + the aligned-basis products) bit for bit."""
+        for _ in range(20):
+            geom = P.ScanGeometry(float(rng.uniform(300, 600)), float(rng.uniform(100, 250)),
+                                  64, 48, float(rng.uniform(0.05, 0.3)),
+                                  (float(rng.uniform(20, 40)), float(rng.uniform(10, 30))),
+                                  P.full_turn_angles(int(rng.integers(5, 400))))
+            grid = P.CylGrid(4, 8, 4, 6.0, 10.0, P.Pose(*rng.uniform(-3, 3, size=3),
+                                                      t=rng.uniform(-2, 2, size=3)))
+            views = range(geom.n_proj)
+            a, t = grid.rotation.T, grid.pose.t
+            ref = np.stack([np.concatenate([a @ (s - t), a @ (o - t), a @ u, a @ v])
+                            for s, o, u, v in (P.view_basis(geom, i) for i in views)])
+            assert np.array_equal(D.ray_view_table(grid, geom, views), ref)
+            cart = np.stack([np.concatenate(P.view_basis(geom, i)) for i in views])
+            assert np.array_equal(D.ray_view_table(P.CartGrid.centered(3, 3, 3, 1.0), geom, views),
+                                  cart)
+            det = D.det_view_table(geom, views)
+            assert np.array_equal(det[:, 5], [np.cos(x) for x in geom.stage_angles])
+            assert np.array_equal(det[:, 6], [np.sin(x) for x in geom.stage_angles])
+
     def test_det_table(self):
         geom = desk()
         tab = D.det_view_table(geom, range(8))
