@@ -515,7 +515,6 @@ struct CartGeo {
     for (int a = 0; a < 3; ++a) off[a] = (float)(-g.origin[a] / g.voxel_size - 0.5);
     nx_m1 = (float)(nx - 1); ny_m1 = (float)(ny - 1); nz_m1 = (float)(nz - 1);
     for (int a = 0; a < 3; ++a) off1[a] = off[a] + 1.0f;
-    const unsigned B = kMagicBits;
     cell_jstride = (unsigned)nx + 1u;
     cell_kstride = gather_layer_stride((unsigned)ny + 1u, cell_jstride);
   }
