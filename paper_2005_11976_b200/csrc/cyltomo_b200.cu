@@ -141,8 +141,13 @@ __device__ __forceinline__ float trilinear_eval(float4 ca, float4 cb, float wr, 
 // one bilinear footprint (ct_pack_quads) with a single 128-bit load
 __device__ __forceinline__ float4 ld_quad(const float4* p) {
   float4 q;
+#if defined(CT_QUAD_LOAD_NOALLOC)
   asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
       : "=f"(q.x), "=f"(q.y), "=f"(q.z), "=f"(q.w) : "l"(p));
+#else
+  asm("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];"
+      : "=f"(q.x), "=f"(q.y), "=f"(q.z), "=f"(q.w) : "l"(p));
+#endif
   return q;
 }
 
