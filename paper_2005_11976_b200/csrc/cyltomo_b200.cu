@@ -234,23 +234,21 @@ __device__ __forceinline__ float rcp_approx(float x) {
 #define CT_ATAN2X_C2 0.3990408182144165f
 #define CT_ATAN2X_C1 -0.6666072607040405f
 #define CT_ATAN2X_C0 1.999998927116394f
-__device__ __forceinline__ float atan2x_poly(float s) {
-  float p = fmaf(CT_ATAN2X_C7, s, CT_ATAN2X_C6);
-  p = fmaf(p, s, CT_ATAN2X_C5);
-  p = fmaf(p, s, CT_ATAN2X_C4);
-  p = fmaf(p, s, CT_ATAN2X_C3);
-  p = fmaf(p, s, CT_ATAN2X_C2);
-  p = fmaf(p, s, CT_ATAN2X_C1);
-  return fmaf(p, s, CT_ATAN2X_C0);
+constexpr double kAtan2x[8] = {CT_ATAN2X_C0, CT_ATAN2X_C1, CT_ATAN2X_C2, CT_ATAN2X_C3,
+                               CT_ATAN2X_C4, CT_ATAN2X_C5, CT_ATAN2X_C6, CT_ATAN2X_C7};
+// The polynomial with coefficients pre-scaled by 1/dtheta (CylGeo::tc): the
+// theta index is then one FFMA away, fma(q, p(q^2), ct).
+__device__ __forceinline__ float atan2x_poly(const float* c, float s) {
+  float p = fmaf(c[7], s, c[6]);
+#pragma unroll
+  for (int i = 5; i >= 0; --i) p = fmaf(p, s, c[i]);
+  return p;
 }
-__device__ __forceinline__ f32x2 atan2x_poly2(f32x2 s) {
-  f32x2 p = fma2(dup2(CT_ATAN2X_C7), s, dup2(CT_ATAN2X_C6));
-  p = fma2(p, s, dup2(CT_ATAN2X_C5));
-  p = fma2(p, s, dup2(CT_ATAN2X_C4));
-  p = fma2(p, s, dup2(CT_ATAN2X_C3));
-  p = fma2(p, s, dup2(CT_ATAN2X_C2));
-  p = fma2(p, s, dup2(CT_ATAN2X_C1));
-  return fma2(p, s, dup2(CT_ATAN2X_C0));
+__device__ __forceinline__ f32x2 atan2x_poly2(const float* c, f32x2 s) {
+  f32x2 p = fma2(dup2(c[7]), s, dup2(c[6]));
+#pragma unroll
+  for (int i = 5; i >= 0; --i) p = fma2(p, s, dup2(c[i]));
+  return p;
 }
 
 // Per-ray march constants.  Sample k of a ray sits at e + k*i (grid frame).
@@ -303,6 +301,7 @@ struct CylGeo {
   double radius, half_h;
   // fp32 sampling constants
   float inv_dr, inv_dth, inv_dh, h_off, h_off1, nr_m1, nh_m1;
+  float tc[8];   // 2 atan polynomial coefficients times n_theta / (2 pi)
   // gather layout: cells (nh+1, nt+1, nr+1), strides (ks, js, 1)
   unsigned cell_kstride, cell_jstride, jb_wrap;
 
@@ -314,6 +313,7 @@ struct CylGeo {
     half_h = 0.5 * g.height;
     inv_dr = (float)(g.n_r / g.radius);
     inv_dth = (float)(g.n_theta / kTwoPi);
+    for (int i = 0; i < 8; ++i) tc[i] = (float)(kAtan2x[i] * (g.n_theta / kTwoPi));
     inv_dh = (float)(g.n_h / g.height);
     h_off = (float)(0.5 * g.n_h - 0.5);
     nr_m1 = (float)(g.n_r - 1);
@@ -418,7 +418,7 @@ struct CylGeo {
     const float fh1 = fmaf(k, ry.ih, ry.eh);
     const float r = sqrt_approx(fmaf(s, s, ry.d2));
     const float q = __fmul_rn(s, rcp_approx(__fadd_rn(r, ry.d0)));
-    const float ft1 = fmaf(__fmul_rn(q, atan2x_poly(__fmul_rn(q, q))), inv_dth, ry.ct);
+    const float ft1 = fmaf(q, atan2x_poly(tc, __fmul_rn(q, q)), ry.ct);
     const float fr1 = __fadd_rn(r, 0.5f);
     const float tr = __fadd_rd(fr1, 8388608.0f);
     const float th_ = __fadd_rd(fh1, 8388608.0f);
@@ -444,7 +444,7 @@ struct CylGeo {
     float rda, rdb;
     upk(add2(R, dup2(ry.d0)), rda, rdb);
     const f32x2 Q = mul2(S, pk(rcp_approx(rda), rcp_approx(rdb)));
-    const f32x2 FT1 = fma2(mul2(Q, atan2x_poly2(mul2(Q, Q))), dup2(inv_dth), dup2(ry.ct));
+    const f32x2 FT1 = fma2(Q, atan2x_poly2(tc, mul2(Q, Q)), dup2(ry.ct));
     const f32x2 FR1 = add2(R, dup2(0.5f));
     const f32x2 BIG = dup2(8388608.0f);
     const f32x2 TR = add2_rd(FR1, BIG), TT = add2_rd(FT1, BIG), TH = add2_rd(FH1, BIG);
