@@ -28,6 +28,7 @@
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 namespace {
@@ -148,6 +149,16 @@ __device__ __forceinline__ float4 ld_quad(const float4* p) {
   asm("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];"
       : "=f"(q.x), "=f"(q.y), "=f"(q.z), "=f"(q.w) : "l"(p));
 #endif
+  return q;
+}
+
+// one corner quad of the large-volume layout (GL_QUAD)
+// (L1-allocating: in the large volumes neighbouring rays do meet in L1; A/B
+// at C5 -19 % against no_allocate)
+__device__ __forceinline__ float4 ld_vquad(const float4* p) {
+  float4 q;
+  asm("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];"
+      : "=f"(q.x), "=f"(q.y), "=f"(q.z), "=f"(q.w) : "l"(p));
   return q;
 }
 
@@ -294,9 +305,22 @@ __host__ __device__ inline unsigned gather_layer_stride(unsigned rows, unsigned 
   return ks + (256u - (ks + js + 1u) % 256u) % 256u;
 }
 
+// Large volumes use 16-byte per-layer bilinear cells (GL_QUAD) instead of the
+// 32-byte trilinear cells: half the bytes per h layer, so more of the band of
+// layers a wave of rays works on stays in L2, for one more load and two f32x2
+// subtractions per cell entered.  Measured (A/B): C5 -23.5 %, C4-cyl equal,
+// C4-cart (8.4 MB layers) +22 %, C2 (4.2 MB layers) +15 %; hence layers above
+// 10 MB.  CT_GATHER_QUAD=0/1 overrides.
+inline bool gather_quad(unsigned ks) {
+  const char* e = getenv("CT_GATHER_QUAD");
+  if (e && *e) return e[0] == '1';
+  return 32.0 * ks > 10.0e6;
+}
+
 struct CylGeo {
   const float* __restrict__ mu;
   const float4* __restrict__ oct;  // gather layout (ct_pack_gather_cyl) or null
+  bool quad;                       // oct holds GL_QUAD corner quads
   int nh, nt, nr;
   double radius, half_h;
   // fp32 sampling constants
@@ -322,6 +346,7 @@ struct CylGeo {
     const unsigned B = kMagicBits;
     cell_jstride = (unsigned)g.n_r + 1u;
     cell_kstride = gather_layer_stride((unsigned)gather_rows(g.n_theta), cell_jstride);
+    quad = gather_quad(cell_kstride);
     jb_wrap = B + (unsigned)g.n_theta;
   }
   // theta rows of the gather layout: indices -1 .. n_theta - 1 (see RayF)
@@ -502,6 +527,7 @@ struct CylGeo {
 struct CartGeo {
   const float* __restrict__ mu;
   const float4* __restrict__ oct;  // gather layout (ct_pack_gather_cart) or null
+  bool quad;                       // oct holds GL_QUAD corner quads
   int nz, ny, nx;
   double vs, lo[3], hi[3];
   float inv_vs, off[3], off1[3], nx_m1, ny_m1, nz_m1;
@@ -522,6 +548,7 @@ struct CartGeo {
     for (int a = 0; a < 3; ++a) off1[a] = off[a] + 1.0f;
     cell_jstride = (unsigned)nx + 1u;
     cell_kstride = gather_layer_stride((unsigned)ny + 1u, cell_jstride);
+    quad = gather_quad(cell_kstride);
   }
 
   // _kernels.py:207-231
@@ -645,6 +672,9 @@ struct CartGeo {
 // forward projection
 // ---------------------------------------------------------------------------
 enum FpEpi { EPI_PROJECT = 0, EPI_CORR = 1, EPI_RESID = 2, EPI_ROWMAX = 3 };
+// FP volume layouts: plain mu, the 32-byte polynomial cells (ct_pack_gather_*),
+// or 16-byte corner quads per h layer (large volumes; see gather_quad())
+enum FpLayout { GL_PLAIN = 0, GL_OCT = 1, GL_QUAD = 2 };
 
 // block = FP_WX x FP_WY warps, each warp a pixel patch (tile_ww x tile_wh rays)
 #ifndef CT_FP_WX
@@ -702,7 +732,7 @@ __host__ __device__ inline int tile_wh(int K) { return (32 / K) / tile_ww(K); }
 
 // Linear-interpolation march of samples [k, k_end) of one ray (+ the last
 // sample k_last when with_last), returning the fp32 sum of the values.
-template <class Geo, bool OCT, bool WRAP>
+template <class Geo, int OCT, bool WRAP>
 __device__ __forceinline__ float march_linear(const Geo& geo, const RayF& ry, int k, int k_end,
                                               bool with_last, float k_last) {
   // Linear interpolation.  OCT: consecutive samples are half a voxel apart, so
@@ -720,10 +750,26 @@ __device__ __forceinline__ float march_linear(const Geo& geo, const RayF& ry, in
     float sum = 0.0f;
   };
   auto value = [&](Chain& ch, const Cell& c) -> float {
-    if (OCT) {
+    if (OCT == GL_OCT) {
       const int idx = geo.template gather_index<WRAP>(c);
       if (idx != ch.prev) ld_cell(geo.oct + 2 * (size_t)(unsigned)idx, ch.pa, ch.pb);
       ch.prev = idx;   // (unconditional: equal when not reloaded; no predicated move)
+      return trilinear_eval(ch.pa, ch.pb, c.w0, c.w1, c.w2);
+    }
+    if (OCT == GL_QUAD) {
+      // bilinear layers k, k+1 of the cell; the h terms are their
+      // difference (two f32x2 subtractions)
+      const int idx = geo.template gather_index<WRAP>(c);
+      if (idx != ch.prev) {
+        const float4 a = ld_vquad(geo.oct + (size_t)(unsigned)idx);
+        const float4 b = ld_vquad(geo.oct + (size_t)(unsigned)idx + geo.cell_kstride);
+        ch.pa = a;
+        float x0, x1, y0, y1;
+        upk(sub2(pk(b.x, b.y), pk(a.x, a.y)), x0, x1);
+        upk(sub2(pk(b.z, b.w), pk(a.z, a.w)), y0, y1);
+        ch.pb = make_float4(x0, x1, y0, y1);
+      }
+      ch.prev = idx;
       return trilinear_eval(ch.pa, ch.pb, c.w0, c.w1, c.w2);
     }
     float4 a, b, ca, cb;
@@ -787,7 +833,7 @@ __device__ __forceinline__ float march_linear(const Geo& geo, const RayF& ry, in
 // One sub-ray, chunk `chunk` of `K`: returns this chunk's in-support sample
 // count and adds the fp32 sum of its interpolated values into acc (COUNT_ONLY:
 // chunk 0 returns the whole ray's count, without marching).
-template <class Geo, bool NEAREST, bool OCT, bool COUNT_ONLY>
+template <class Geo, bool NEAREST, int OCT, bool COUNT_ONLY>
 __device__ __forceinline__ int march(const Geo& geo, const ct_ray_view& v, double cu, double cv,
                                      double step, float& acc, int chunk, int K) {
   double d[3];
@@ -863,7 +909,7 @@ __device__ __forceinline__ double warp_max(double x) {
   return x;
 }
 
-template <class Geo, int EPI, bool NEAREST, bool OCT>
+template <class Geo, int EPI, bool NEAREST, int OCT>
 __global__ void __maxnreg__(CT_FP_MAXREG) fp_kernel(const FpArgs<Geo> a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int K = a.lanes;
@@ -1023,11 +1069,13 @@ int launch_fp(const Geo& geo, const ct_ray_view* views, const ct_batch& b, const
   a.out1 = o1;
   a.red = red;
   if (s.nearest)
-    fp_kernel<Geo, EPI, true, false><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
+    fp_kernel<Geo, EPI, true, GL_PLAIN><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
+  else if (EPI != EPI_ROWMAX && geo.oct && geo.quad)
+    fp_kernel<Geo, EPI, false, GL_QUAD><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
   else if (EPI != EPI_ROWMAX && geo.oct)
-    fp_kernel<Geo, EPI, false, true><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
+    fp_kernel<Geo, EPI, false, GL_OCT><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
   else
-    fp_kernel<Geo, EPI, false, false><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
+    fp_kernel<Geo, EPI, false, GL_PLAIN><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
   return check_launch("fp_kernel");
 }
 
@@ -1587,14 +1635,57 @@ __global__ void pack_quads_kernel(const float* __restrict__ corr, int64_t n, int
                          (ru && rv) ? __ldg(p + cols + 1) : 0.0f);
 }
 
+// GL_QUAD: cell (kc, jc, ic), kc in [0, nz+1]: the bilinear polynomial
+// (c0, cr, ct, crt) of layer kc-1 (clamped; -1 and n are halo copies) over
+// rows jc-1, jc (theta wraps / y clamps) and columns ic-1, ic (clamped).  The
+// trilinear cell of layers k, k+1 is (L_k, L_k+1 - L_k): the same fp32 ops as
+// trilinear_coeffs, so GL_QUAD, GL_OCT and the plain path agree bit for bit.
+template <bool CYL>
+__global__ void pack_vquad_kernel(const float* __restrict__ mu, int nk, int nj, int ni,
+                                  unsigned ks, float4* __restrict__ q) {
+  const unsigned rem = blockIdx.x * blockDim.x + threadIdx.x;
+  if (rem >= ks) return;
+  const int kc = blockIdx.y;
+  const size_t m = (size_t)kc * ks + rem;
+  const unsigned js = (unsigned)ni + 1u;
+  const int jc = (int)(rem / js), ic = (int)(rem % js);
+  if (jc > nj) {
+    q[m] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
+  const int k = min(max(kc - 1, 0), nk - 1);
+  const int i = max(ic - 1, 0), i1 = min(ic, ni - 1);
+  int j, j1;
+  if (CYL) {
+    j = (jc == 0) ? nj - 1 : jc - 1;
+    j1 = (jc == nj) ? 0 : jc;
+  } else {
+    j = max(jc - 1, 0);
+    j1 = min(jc, nj - 1);
+  }
+  const float* p0 = mu + ((int64_t)k * nj + j) * ni;
+  const float* p1 = mu + ((int64_t)k * nj + j1) * ni;
+  // the layer's bilinear coefficients (c0, cr, ct, crt), trilinear_coeffs' ops
+  const float a0 = __ldg(p0 + i), a1 = __ldg(p0 + i1), a2 = __ldg(p1 + i), a3 = __ldg(p1 + i1);
+  const float dr0 = a1 - a0, dr1 = a3 - a2;
+  q[m] = make_float4(a0, dr0, a2 - a0, dr1 - dr0);
+}
+
 unsigned gather_ks_cyl(const ct_cyl_grid& g) {
   return gather_layer_stride((unsigned)CylGeo::gather_rows(g.n_theta), (unsigned)g.n_r + 1u);
 }
 unsigned gather_ks_cart(const ct_cart_grid& g) {
   return gather_layer_stride((unsigned)g.n_y + 1u, (unsigned)g.n_x + 1u);
 }
-int64_t gather_cells_cyl(const ct_cyl_grid& g) { return (int64_t)(g.n_h + 1) * gather_ks_cyl(g); }
-int64_t gather_cells_cart(const ct_cart_grid& g) { return (int64_t)(g.n_z + 1) * gather_ks_cart(g); }
+// gather buffer length in floats: (n+1) layers x 8 floats, or GL_QUAD (n+2) x 4
+int64_t gather_floats_cyl(const ct_cyl_grid& g) {
+  const unsigned ks = gather_ks_cyl(g);
+  return gather_quad(ks) ? 4 * (int64_t)(g.n_h + 2) * ks : 8 * (int64_t)(g.n_h + 1) * ks;
+}
+int64_t gather_floats_cart(const ct_cart_grid& g) {
+  const unsigned ks = gather_ks_cart(g);
+  return gather_quad(ks) ? 4 * (int64_t)(g.n_z + 2) * ks : 8 * (int64_t)(g.n_z + 1) * ks;
+}
 
 // Beer-Lambert p = -ln(I / I0) (cyltomo/projector.py:169-181), fp64 log of the
 // fp32 inputs; flat field is a scalar or one image broadcast over the views.
@@ -2133,10 +2224,10 @@ int ct_line_integrals(const float* intensity, int64_t n, int64_t npix, const flo
 }
 
 int64_t ct_gather_floats_cyl(const ct_cyl_grid* grid) {
-  return check_cyl(grid) ? 0 : 8 * gather_cells_cyl(*grid);
+  return check_cyl(grid) ? 0 : gather_floats_cyl(*grid);
 }
 int64_t ct_gather_floats_cart(const ct_cart_grid* grid) {
-  return check_cart(grid) ? 0 : 8 * gather_cells_cart(*grid);
+  return check_cart(grid) ? 0 : gather_floats_cart(*grid);
 }
 
 int ct_pack_gather_cyl(const float* mu, const ct_cyl_grid* grid, float* gather,
@@ -2145,8 +2236,13 @@ int ct_pack_gather_cyl(const float* mu, const ct_cyl_grid* grid, float* gather,
   if (rc) return rc;
   if (!mu || !gather) return set_err(CT_ERR_ARG, "null mu/gather");
   if (reinterpret_cast<uintptr_t>(gather) % 16) return set_err(CT_ERR_ARG, "gather not 16B-aligned");
-  if (grid->n_h + 1 > 65535) return set_err(CT_ERR_ARG, "gather layout: n_h + 1 > 65535");
+  if (grid->n_h + 2 > 65535) return set_err(CT_ERR_ARG, "gather layout: n_h + 2 > 65535");
   const unsigned ks = gather_ks_cyl(*grid);
+  if (gather_quad(ks)) {
+    pack_vquad_kernel<true><<<dim3(blocks_for(ks, 256), grid->n_h + 2), 256, 0, CT_STREAM(stream)>>>(
+        mu, grid->n_h, grid->n_theta, grid->n_r, ks, reinterpret_cast<float4*>(gather));
+    return check_launch("pack_vquad_kernel");
+  }
   pack_gather_cyl_kernel<<<dim3(blocks_for(ks, 256), grid->n_h + 1), 256, 0, CT_STREAM(stream)>>>(
       mu, grid->n_h, grid->n_theta, grid->n_r, ks, reinterpret_cast<float4*>(gather));
   return check_launch("pack_gather_cyl_kernel");
@@ -2158,8 +2254,13 @@ int ct_pack_gather_cart(const float* mu, const ct_cart_grid* grid, float* gather
   if (rc) return rc;
   if (!mu || !gather) return set_err(CT_ERR_ARG, "null mu/gather");
   if (reinterpret_cast<uintptr_t>(gather) % 16) return set_err(CT_ERR_ARG, "gather not 16B-aligned");
-  if (grid->n_z + 1 > 65535) return set_err(CT_ERR_ARG, "gather layout: n_z + 1 > 65535");
+  if (grid->n_z + 2 > 65535) return set_err(CT_ERR_ARG, "gather layout: n_z + 2 > 65535");
   const unsigned ks = gather_ks_cart(*grid);
+  if (gather_quad(ks)) {
+    pack_vquad_kernel<false><<<dim3(blocks_for(ks, 256), grid->n_z + 2), 256, 0, CT_STREAM(stream)>>>(
+        mu, grid->n_z, grid->n_y, grid->n_x, ks, reinterpret_cast<float4*>(gather));
+    return check_launch("pack_vquad_kernel");
+  }
   pack_gather_cart_kernel<<<dim3(blocks_for(ks, 256), grid->n_z + 1), 256, 0, CT_STREAM(stream)>>>(
       mu, grid->n_z, grid->n_y, grid->n_x, ks, reinterpret_cast<float4*>(gather));
   return check_launch("pack_gather_cart_kernel");

@@ -320,10 +320,13 @@ def test_graph_replay_bit_identical(small_cyl_setup):
     assert ra.residuals == rb.residuals
 
 
+@pytest.mark.parametrize("quad", ["0", "1"])
 @pytest.mark.parametrize("kind", ["cyl", "cart"])
-def test_gather_layout_matches_plain_path(rng, kind):
-    """The gather layout (halo, stored differences, 256-bit loads, cell reuse)
-    changes the loads, not the result: bit-identical to the plain path."""
+def test_gather_layout_matches_plain_path(rng, kind, quad, monkeypatch):
+    """The gather layouts (GL_OCT: 32-byte polynomial cells; GL_QUAD: 16-byte
+    per-layer bilinear cells, forced with CT_GATHER_QUAD=1) change the loads,
+    not the result: bit-identical to the plain path."""
+    monkeypatch.setenv("CT_GATHER_QUAD", quad)
     import ctypes as C
     import torch
     from paper_2005_11976_b200 import _device as D, _native as N
@@ -388,3 +391,17 @@ def test_quad_footprints_match_plain_bp(rng, kind):
     assert torch.equal(d0 > 0, d1 > 0)
     assert torch.allclose(d0, d1, rtol=1e-6, atol=1e-6)
     assert torch.allclose(n0, n1, rtol=1e-5, atol=1e-5)
+
+
+def test_quad_layout_sart_bit_identical(small_cyl_setup, monkeypatch):
+    """A whole OS-SART run through the GL_QUAD volume layout (the large-volume
+    choice) gives the same bits as through GL_OCT."""
+    grid, vol, ps = small_cyl_setup
+    cfg = SartConfig(n_iterations=2, n_subsets=3, relaxation=0.6)
+    out = []
+    for quad in ("0", "1"):
+        monkeypatch.setenv("CT_GATHER_QUAD", quad)
+        v, r = sart_run(ps, grid, cfg)
+        out.append((v.mu, r.residuals))
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1]
