@@ -33,6 +33,9 @@
 
 namespace {
 
+#ifndef CT_ATAN_TERMS
+#define CT_ATAN_TERMS 7          // 2 atan polynomial terms (7: 4.8e-7 rad; 8: 5.7e-8 rad)
+#endif
 constexpr double kPi = 3.141592653589793;
 constexpr double kTwoPi = 2.0 * kPi;
 constexpr float kTwoPiF = 6.28318530717958647692f;
@@ -235,8 +238,21 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return r;
 }
 
-// 2 atan(q) / q as a polynomial in q^2 on q in [-1, 1]: degree-15 odd minimax
-// fit of 2 atan (max error 5.7e-8 rad; tools/fit_atan.py)
+// 2 atan(q) / q as a polynomial in q^2 on q in [-1, 1] (odd minimax fits of
+// 2 atan, tools/fit_atan.py)
+#if CT_ATAN_TERMS == 7
+// degree-13 odd minimax fit (4.8e-7 rad, 6.3e-7 evaluated in fp32 -- about
+// one fp32 ulp of theta near 2 pi; FP parity margins are unchanged, see
+// tools/parity_margins.py)
+#define CT_ATAN2X_C7 0.0f
+#define CT_ATAN2X_C6 0.013589471578598022f
+#define CT_ATAN2X_C5 -0.06711680442094803f
+#define CT_ATAN2X_C4 0.15916450321674347f
+#define CT_ATAN2X_C3 -0.26464372873306274f
+#define CT_ATAN2X_C2 0.3961613178253174f
+#define CT_ATAN2X_C1 -0.6663504242897034f
+#define CT_ATAN2X_C0 1.9999924898147583f
+#else
 #define CT_ATAN2X_C7 -0.008428506553173065f
 #define CT_ATAN2X_C6 0.044908907264471054f
 #define CT_ATAN2X_C5 -0.1135723665356636f
@@ -245,18 +261,19 @@ __device__ __forceinline__ float rcp_approx(float x) {
 #define CT_ATAN2X_C2 0.3990408182144165f
 #define CT_ATAN2X_C1 -0.6666072607040405f
 #define CT_ATAN2X_C0 1.999998927116394f
+#endif
 constexpr double kAtan2x[8] = {CT_ATAN2X_C0, CT_ATAN2X_C1, CT_ATAN2X_C2, CT_ATAN2X_C3,
                                CT_ATAN2X_C4, CT_ATAN2X_C5, CT_ATAN2X_C6, CT_ATAN2X_C7};
 // The polynomial with coefficients pre-scaled by 1/dtheta (CylGeo::tc): the
 // theta index is then one FFMA away, fma(q, p(q^2), ct).
 __device__ __forceinline__ float atan2x_poly(const float* c, float s) {
-  float p = fmaf(c[7], s, c[6]);
+  float p = CT_ATAN_TERMS == 7 ? c[6] : fmaf(c[7], s, c[6]);
 #pragma unroll
   for (int i = 5; i >= 0; --i) p = fmaf(p, s, c[i]);
   return p;
 }
 __device__ __forceinline__ f32x2 atan2x_poly2(const float* c, f32x2 s) {
-  f32x2 p = fma2(dup2(c[7]), s, dup2(c[6]));
+  f32x2 p = CT_ATAN_TERMS == 7 ? dup2(c[6]) : fma2(dup2(c[7]), s, dup2(c[6]));
 #pragma unroll
   for (int i = 5; i >= 0; --i) p = fma2(p, s, dup2(c[i]));
   return p;
@@ -434,8 +451,8 @@ struct CylGeo {
   }
 
   // Trilinear cell of sample k (see RayF): r = sqrt(s^2 + d0^2) and
-  // theta = phi + 2 atan(s / (r + d0)) with 2 atan from a degree-15 odd
-  // minimax polynomial on [-1, 1] (5.7e-8 rad; 2.8e-7 evaluated in fp32).
+  // theta = phi + 2 atan(s / (r + d0)) with 2 atan from a degree-13 odd
+  // minimax polynomial on [-1, 1] (4.8e-7 rad; 6.3e-7 evaluated in fp32).
   // floor() via x + 2^23 rounded toward -inf (bits = floor(x) + 0x4B000000).
   // The indices carry the gather layout's +1 halo offset.
   __device__ __forceinline__ Cell locate1(float k, const RayF& ry) const {
