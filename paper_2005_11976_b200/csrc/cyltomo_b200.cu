@@ -240,7 +240,17 @@ __device__ __forceinline__ float rcp_approx(float x) {
 
 // 2 atan(q) / q as a polynomial in q^2 on q in [-1, 1] (odd minimax fits of
 // 2 atan, tools/fit_atan.py)
-#if CT_ATAN_TERMS == 7
+#if CT_ATAN_TERMS == 6
+// degree-11 fit (3.3e-6 rad; A/B only)
+#define CT_ATAN2X_C7 0.0f
+#define CT_ATAN2X_C6 0.0f
+#define CT_ATAN2X_C5 -0.023422138765454292f
+#define CT_ATAN2X_C4 0.10525291413068771f
+#define CT_ATAN2X_C3 -0.23281531035900116f
+#define CT_ATAN2X_C2 0.38706788420677185f
+#define CT_ATAN2X_C1 -0.665244996547699f
+#define CT_ATAN2X_C0 1.9999547004699707f
+#elif CT_ATAN_TERMS == 7
 // degree-13 odd minimax fit (4.8e-7 rad, 6.3e-7 evaluated in fp32 -- about
 // one fp32 ulp of theta near 2 pi; FP parity margins are unchanged, see
 // tools/parity_margins.py)
@@ -267,15 +277,16 @@ constexpr double kAtan2x[8] = {CT_ATAN2X_C0, CT_ATAN2X_C1, CT_ATAN2X_C2, CT_ATAN
 // The polynomial with coefficients pre-scaled by 1/dtheta (CylGeo::tc): the
 // theta index is then one FFMA away, fma(q, p(q^2), ct).
 __device__ __forceinline__ float atan2x_poly(const float* c, float s) {
-  float p = CT_ATAN_TERMS == 7 ? c[6] : fmaf(c[7], s, c[6]);
+  float p = CT_ATAN_TERMS == 6 ? c[5] : CT_ATAN_TERMS == 7 ? c[6] : fmaf(c[7], s, c[6]);
 #pragma unroll
-  for (int i = 5; i >= 0; --i) p = fmaf(p, s, c[i]);
+  for (int i = CT_ATAN_TERMS == 6 ? 4 : 5; i >= 0; --i) p = fmaf(p, s, c[i]);
   return p;
 }
 __device__ __forceinline__ f32x2 atan2x_poly2(const float* c, f32x2 s) {
-  f32x2 p = CT_ATAN_TERMS == 7 ? dup2(c[6]) : fma2(dup2(c[7]), s, dup2(c[6]));
+  f32x2 p = CT_ATAN_TERMS == 6 ? dup2(c[5])
+           : CT_ATAN_TERMS == 7 ? dup2(c[6]) : fma2(dup2(c[7]), s, dup2(c[6]));
 #pragma unroll
-  for (int i = 5; i >= 0; --i) p = fma2(p, s, dup2(c[i]));
+  for (int i = CT_ATAN_TERMS == 6 ? 4 : 5; i >= 0; --i) p = fma2(p, s, dup2(c[i]));
   return p;
 }
 
