@@ -311,13 +311,20 @@ struct RayF {
 };
 
 // One sample's trilinear cell: bit patterns of floor(index + 1) (+0x4B000000,
-// the "+1" being the gather layout's halo offset) and the three weights.
+// the "+1" being the gather layout's halo offset; the cylindrical r bits carry
+// one less, see kRMagic) and the three weights.
 struct Cell {
   unsigned ib, jb, kb;
   float w0, w1, w2;
 };
 
 constexpr unsigned kMagicBits = 0x4B000000u;   // bits of 2^23
+// r floor: x + (2^23 - 1/2) rounded toward -inf has the bits of
+// 2^23 + floor(x + 1/2) - 1 (for x < 1/2 the grid below 2^23 still gives bits
+// 2^23 - 1), and x - (that - (2^23 - 1/2)) is frac(x + 1/2) exactly: the
+// cell-centre offset costs no add.  (For x < 1/2 -- the axis half-cell -- the
+// weight is off, but that cell is the r halo whose r terms are zero.)
+constexpr float kRMagic = 8388607.5f;
 
 // ---------------------------------------------------------------------------
 // grid policies: support interval (fp64), last-sample test (fp64) and the
@@ -359,7 +366,6 @@ struct CylGeo {
 
   __host__ void init(const float* m, const float* gather, const ct_cyl_grid& g) {
     mu = m;
-    oct = reinterpret_cast<const float4*>(gather);
     nh = g.n_h; nt = g.n_theta; nr = g.n_r;
     radius = g.radius;
     half_h = 0.5 * g.height;
@@ -375,6 +381,8 @@ struct CylGeo {
     cell_jstride = (unsigned)g.n_r + 1u;
     cell_kstride = gather_layer_stride((unsigned)gather_rows(g.n_theta), cell_jstride);
     quad = gather_quad(cell_kstride);
+    // the r floor bits carry index - 1 (kRMagic): the base is one cell on
+    oct = gather ? reinterpret_cast<const float4*>(gather) + (quad ? 1 : 2) : nullptr;
     jb_wrap = B + (unsigned)g.n_theta;
   }
   // theta rows of the gather layout: indices -1 .. n_theta - 1 (see RayF)
@@ -472,12 +480,11 @@ struct CylGeo {
     const float r = sqrt_approx(fmaf(s, s, ry.d2));
     const float q = __fmul_rn(s, rcp_approx(__fadd_rn(r, ry.d0)));
     const float ft1 = fmaf(q, atan2x_poly(tc, __fmul_rn(q, q)), ry.ct);
-    const float fr1 = __fadd_rn(r, 0.5f);
-    const float tr = __fadd_rd(fr1, 8388608.0f);
+    const float tr = __fadd_rd(r, kRMagic);
     const float th_ = __fadd_rd(fh1, 8388608.0f);
     const float tt = __fadd_rd(ft1, 8388608.0f);
     Cell c;
-    c.w0 = __fsub_rn(fr1, __fsub_rn(tr, 8388608.0f));
+    c.w0 = __fsub_rn(r, __fsub_rn(tr, kRMagic));
     c.w1 = __fsub_rn(ft1, __fsub_rn(tt, 8388608.0f));
     c.w2 = __fsub_rn(fh1, __fsub_rn(th_, 8388608.0f));
     c.ib = __float_as_uint(tr);
@@ -498,10 +505,11 @@ struct CylGeo {
     upk(add2(R, dup2(ry.d0)), rda, rdb);
     const f32x2 Q = mul2(S, pk(rcp_approx(rda), rcp_approx(rdb)));
     const f32x2 FT1 = fma2(Q, atan2x_poly2(tc, mul2(Q, Q)), dup2(ry.ct));
-    const f32x2 FR1 = add2(R, dup2(0.5f));
+
     const f32x2 BIG = dup2(8388608.0f);
-    const f32x2 TR = add2_rd(FR1, BIG), TT = add2_rd(FT1, BIG), TH = add2_rd(FH1, BIG);
-    const f32x2 WR = sub2(FR1, sub2(TR, BIG)), WT = sub2(FT1, sub2(TT, BIG));
+    const f32x2 RM = dup2(kRMagic);
+    const f32x2 TR = add2_rd(R, RM), TT = add2_rd(FT1, BIG), TH = add2_rd(FH1, BIG);
+    const f32x2 WR = sub2(R, sub2(TR, RM)), WT = sub2(FT1, sub2(TT, BIG));
     const f32x2 WH = sub2(FH1, sub2(TH, BIG));
     upk(WR, ca.w0, cb.w0);
     upk(WT, ca.w1, cb.w1);
@@ -526,7 +534,7 @@ struct CylGeo {
 
   // the same 8 values from the plain mu layout (r/h clamp, theta modulo n_theta)
   __device__ __forceinline__ void fetch_plain(const Cell& c, float4& a, float4& b) const {
-    const int i0 = (int)(c.ib - kMagicBits) - 1, g = (int)(c.jb - kMagicBits);
+    const int i0 = (int)(c.ib - kMagicBits), g = (int)(c.jb - kMagicBits);   // r: kRMagic
     const int k0 = (int)(c.kb - kMagicBits) - 1;
     const int ia = max(i0, 0), ib1 = min(i0 + 1, nr - 1);
     const int ka = max(k0, 0), kb1 = min(k0 + 1, nh - 1);
@@ -700,6 +708,7 @@ struct CartGeo {
 // forward projection
 // ---------------------------------------------------------------------------
 enum FpEpi { EPI_PROJECT = 0, EPI_CORR = 1, EPI_RESID = 2, EPI_ROWMAX = 3 };
+
 // FP volume layouts: plain mu, the 32-byte polynomial cells (ct_pack_gather_*),
 // or 16-byte corner quads per h layer (large volumes; see gather_quad())
 enum FpLayout { GL_PLAIN = 0, GL_OCT = 1, GL_QUAD = 2 };
@@ -773,14 +782,15 @@ __device__ __forceinline__ float march_linear(const Geo& geo, const RayF& ry, in
   // flight together (a single chain serialises load -> evaluate -> next load
   // through its cell registers), and one f32x2 locate serves two chains.
   struct Chain {
-    int prev = -1;
+    int prev = INT_MIN;   // no cell (indices are >= -1)
     float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pb = make_float4(0.f, 0.f, 0.f, 0.f);
     float sum = 0.0f;
   };
   auto value = [&](Chain& ch, const Cell& c) -> float {
     if (OCT == GL_OCT) {
       const int idx = geo.template gather_index<WRAP>(c);
-      if (idx != ch.prev) ld_cell(geo.oct + 2 * (size_t)(unsigned)idx, ch.pa, ch.pb);
+      // signed: the cylindrical r bits make the first cell's index -1 (kRMagic)
+      if (idx != ch.prev) ld_cell(geo.oct + 2 * (ptrdiff_t)idx, ch.pa, ch.pb);
       ch.prev = idx;   // (unconditional: equal when not reloaded; no predicated move)
       return trilinear_eval(ch.pa, ch.pb, c.w0, c.w1, c.w2);
     }
@@ -789,8 +799,8 @@ __device__ __forceinline__ float march_linear(const Geo& geo, const RayF& ry, in
       // difference (two f32x2 subtractions)
       const int idx = geo.template gather_index<WRAP>(c);
       if (idx != ch.prev) {
-        const float4 a = ld_vquad(geo.oct + (size_t)(unsigned)idx);
-        const float4 b = ld_vquad(geo.oct + (size_t)(unsigned)idx + geo.cell_kstride);
+        const float4 a = ld_vquad(geo.oct + (ptrdiff_t)idx);
+        const float4 b = ld_vquad(geo.oct + (ptrdiff_t)idx + geo.cell_kstride);
         ch.pa = a;
         float x0, x1, y0, y1;
         upk(sub2(pk(b.x, b.y), pk(a.x, a.y)), x0, x1);

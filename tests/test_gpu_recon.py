@@ -321,17 +321,21 @@ def test_graph_replay_bit_identical(small_cyl_setup):
 
 
 @pytest.mark.parametrize("quad", ["0", "1"])
-@pytest.mark.parametrize("kind", ["cyl", "cart"])
+@pytest.mark.parametrize("kind", ["cyl", "cyl_coarse", "cart"])
 def test_gather_layout_matches_plain_path(rng, kind, quad, monkeypatch):
     """The gather layouts (GL_OCT: 32-byte polynomial cells; GL_QUAD: 16-byte
     per-layer bilinear cells, forced with CT_GATHER_QUAD=1) change the loads,
-    not the result: bit-identical to the plain path."""
+    not the result: bit-identical to the plain path.  cyl_coarse (2x4x2 cells)
+    puts many samples into the first cell of the layout (bottom h halo, theta
+    row 0, axis r halo), whose index is -1 with the r floor magic."""
     monkeypatch.setenv("CT_GATHER_QUAD", quad)
     import ctypes as C
     import torch
     from paper_2005_11976_b200 import _device as D, _native as N
     if kind == "cyl":
         grid = CylGrid(12, 20, 10, 5.0, 9.0, Pose.tilt(0.2, 0.1, [0.3, 0.1, 0.2]))
+    elif kind == "cyl_coarse":
+        grid = CylGrid(2, 4, 2, 2.0, 2.0, Pose.tilt(0.0, 0.02, [0.0, 0.0, 0.0]))
     else:
         grid = CartGrid.centered(11, 9, 13, 0.7, center=(0.2, -0.3, 0.1))
     geom = ScanGeometry(300.0, 150.0, 40, 36, 0.25, (19.5, 17.5), P.full_turn_angles(6))
@@ -341,11 +345,12 @@ def test_gather_layout_matches_plain_path(rng, kind, quad, monkeypatch):
     s = D.sampling_c(RaySamplingConfig().step_for(grid), 1, False)
     b = D.batch_c(6, geom.det_rows, geom.det_cols)
     gather = D.alloc_gather(grid, "cuda")
-    N.call(f"ct_pack_gather_{kind}", D.ptr(mu), C.byref(g), D.ptr(gather), D.stream_handle())
+    gk = "cart" if kind == "cart" else "cyl"
+    N.call(f"ct_pack_gather_{gk}", D.ptr(mu), C.byref(g), D.ptr(gather), D.stream_handle())
     outs = []
     for gp in (None, gather):
         p = torch.empty((6, geom.det_rows, geom.det_cols), device="cuda")
-        N.call(f"ct_fp_{kind}", D.ptr(mu), D.ptr(gp), C.byref(g), D.ptr(table), C.byref(b),
+        N.call(f"ct_fp_{gk}", D.ptr(mu), D.ptr(gp), C.byref(g), D.ptr(table), C.byref(b),
                C.byref(s), D.ptr(p), None, D.stream_handle())
         outs.append(p)
     assert outs[0].abs().max() > 0
