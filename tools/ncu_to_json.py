@@ -27,7 +27,11 @@ FIELDS = {"duration_ms": ("gpu__time_duration.sum", 1.0),
           "l2_hit_pct": ("lts__t_sector_hit_rate.pct", 1.0),
           "l1_hit_pct": ("l1tex__t_sector_hit_rate.pct", 1.0),
           "registers": ("launch__registers_per_thread", 1.0),
-          "warps_active_pct": ("sm__warps_active.avg.pct_of_peak_sustained_active", 1.0)}
+          "warps_active_pct": ("sm__warps_active.avg.pct_of_peak_sustained_active", 1.0),
+          "fma_pipe_pct": ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", 1.0),
+          "alu_pipe_pct": ("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", 1.0),
+          "xu_pipe_pct": ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", 1.0),
+          "dram_throughput_pct": ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", 1.0)}
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 
