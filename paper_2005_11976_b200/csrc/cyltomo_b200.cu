@@ -1131,10 +1131,11 @@ constexpr int BP_THREADS = CT_BP_THREADS;
 #endif
 constexpr int BP_UNROLL = CT_BP_UNROLL;
 #ifndef CT_BP_MIN_BLOCKS
-#define CT_BP_MIN_BLOCKS 6       // <= 40 registers at 256 threads (A/B: 4-6)
+#define CT_BP_MIN_BLOCKS 8       // 32 registers, 64 warps/SM (A/B: 4-8)
 #endif
 constexpr int BP_MIN_BLOCKS = CT_BP_MIN_BLOCKS;
 constexpr int BP_CHUNK = 64;   // views staged in shared memory per pass
+static_assert(BP_CHUNK / 2 <= 32, "slow-pair mask is 32 bits");
 constexpr float BP_EDGE_EPS = 1e-3f;  // px band around the frame edge refined in fp64
 
 // a pair of views (batch slots 2i, 2i+1), lane-interleaved for f32x2
@@ -1337,6 +1338,7 @@ __global__ void __launch_bounds__(BP_THREADS, BP_MIN_BLOCKS) bp_kernel(const __g
     if (!active) continue;
     const float* __restrict__ img0 = a.corr + (size_t)c0 * npix;
     const int np = nc >> 1;
+    unsigned slow = 0;   // pairs of this chunk for the slow path (BP_CHUNK / 2 <= 32)
 #pragma unroll BP_UNROLL
     for (int i = 0; i < np; ++i) {
       const BpPairF f = sv[i];
@@ -1388,11 +1390,28 @@ __global__ void __launch_bounds__(BP_THREADS, BP_MIN_BLOCKS) bp_kernel(const __g
         }
         nfast += 2;
       } else {
-        const float* ia = img0 + (size_t)(2 * i) * npix;
-        const float2 ra = bp_view_slow(a, m, c0 + 2 * i, u1a, v1a, da, dfa, ia);
-        const float2 rb = bp_view_slow(a, m, c0 + 2 * i + 1, u1b, v1b, db, dfb, ia + npix);
-        NUM = add2(NUM, pk(ra.x, rb.x));
-        DEN = add2(DEN, pk(ra.y, rb.y));
+        slow |= 1u << i;   // deferred: keeps the slow path out of the hot loop
+      }
+    }
+    // the chunk's pairs with a frame-edge / refine-band / near-source view:
+    // recompute the projection per view (the same fp32 ops as the pair path)
+    while (slow) {
+      const int i = __ffs(slow) - 1;
+      slow &= slow - 1;
+      const float* fp = reinterpret_cast<const float*>(&sv[i]);
+#pragma unroll
+      for (int l = 0; l < 2; ++l) {
+        const float cphi = fp[0 + l], sphi = fp[2 + l], sod = fp[4 + l], sdd_p = fp[6 + l];
+        const float u0 = fp[8 + l], v0 = fp[10 + l], dfl = fp[12 + l];
+        const float xi = fmaf(cphi, xw, __fmul_rn(sphi, -yw));
+        const float yi = fmaf(sphi, xw, __fmul_rn(cphi, yw));
+        const float depth = __fadd_rn(sod, yi);
+        const float r = rcp_approx(depth);
+        const float sc = __fmul_rn(sdd_p, fmaf(r, fmaf(-depth, r, 1.0f), r));
+        const float2 rr = bp_view_slow(a, m, c0 + 2 * i + l, fmaf(xi, sc, u0), fmaf(zw, sc, v0),
+                                       depth, dfl, img0 + (size_t)(2 * i + l) * npix);
+        NUM = add2(NUM, l == 0 ? pk(rr.x, 0.0f) : pk(0.0f, rr.x));
+        DEN = add2(DEN, l == 0 ? pk(rr.y, 0.0f) : pk(0.0f, rr.y));
       }
     }
     if (nc & 1) {   // odd view of the chunk: scalar, into the even lane
