@@ -454,11 +454,16 @@ struct CylGeo {
       phi = atan2(e[1], e[0]);
     }
     // shift phi by 2 pi so the smallest theta of samples 0..n-1 is in [0, 2 pi)
+    // The 2 pi shift and the wrap flag only need the ray's theta range to
+    // ~1e-4 rad: fp32 atan2 (a few ulp) with margins.  Shifted so theta >=
+    // -2e-4 (the theta index stays >= 0.5 - 2e-4 n_theta / 2 pi > 0); wrap set
+    // whenever the range may reach 2 pi (the wrap loop is always correct).
     const double s_last = es + (n - 1) * is;
-    const double th_min = phi + atan2(fmin(es, s_last), d0);
-    phi -= kTwoPi * floor(th_min / kTwoPi);
-    // theta index passes n_theta (the fp32 index stays below n_theta + 1 otherwise)
-    ry.wrap = (phi + atan2(fmax(es, s_last), d0)) * ((double)nt / kTwoPi) > nt - 1e-3;
+    const float d0f = (float)d0;
+    const double th_min = phi + (double)atan2f((float)fmin(es, s_last), d0f);
+    phi -= kTwoPi * floor((th_min + 1e-4) / kTwoPi);
+    const double th_max = phi + (double)atan2f((float)fmax(es, s_last), d0f);
+    ry.wrap = th_max + 1e-4 >= kTwoPi * (1.0 - 1e-3 / nt);
     const double idr = (double)nr / radius, d0i = fmax(d0 * idr, 1e-30);
     ry.es = (float)(es * idr);
     ry.is = (float)(is * idr);
