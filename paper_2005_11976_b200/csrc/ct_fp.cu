@@ -1,0 +1,666 @@
+// ct_fp.cu -- forward projection (_kernels.py:238-343): ray march, correction /
+// residual / row-sum epilogues, and the volume gather layouts it reads.
+#include "ct_common.cuh"
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// forward projection
+// ---------------------------------------------------------------------------
+enum FpEpi { EPI_PROJECT = 0, EPI_CORR = 1, EPI_RESID = 2, EPI_ROWMAX = 3 };
+
+// FP volume layouts: plain mu, the 32-byte polynomial cells (ct_pack_gather_*),
+// or 16-byte corner quads per h layer (large volumes; see gather_quad())
+enum FpLayout { GL_PLAIN = 0, GL_OCT = 1, GL_QUAD = 2 };
+
+// block = FP_WX x FP_WY warps, each warp a pixel patch (tile_ww x tile_wh rays)
+#ifndef CT_FP_WX
+#define CT_FP_WX 4
+#endif
+#ifndef CT_FP_WY
+#define CT_FP_WY 1
+#endif
+#ifndef CT_FP_CHAINS
+#define CT_FP_CHAINS 2           // independent gather chains per ray chunk (2 or 4)
+#endif
+#ifndef CT_FP_UNROLL
+#define CT_FP_UNROLL 2           // main march loop unroll
+#endif
+#ifndef CT_FP_MAXREG
+#define CT_FP_MAXREG 64          // 32 warps/SM
+#endif
+#ifndef CT_FP_WW1
+#define CT_FP_WW1 4              // warp patch width at one lane per ray
+#endif
+constexpr int FP_WX = CT_FP_WX, FP_WY = CT_FP_WY, FP_CHAINS = CT_FP_CHAINS, FP_UNROLL = CT_FP_UNROLL;
+static_assert(FP_CHAINS == 2 || FP_CHAINS == 4, "FP_CHAINS");
+constexpr int FP_THREADS = 32 * FP_WX * FP_WY;
+
+template <class Geo>
+struct FpArgs {
+  Geo geo;
+  const ct_ray_view* __restrict__ views;
+  const int32_t* __restrict__ view_ids;
+  int rows, cols, ss;
+  int lanes;            // K lanes per ray (lanes_for(rows, cols))
+  double step;
+  const float* __restrict__ p_meas;
+  const double* __restrict__ row_thr;
+  float* __restrict__ out0;
+  float* __restrict__ out1;
+  double* __restrict__ red;  // residual partials / per-view max_row
+};
+
+// Lanes per ray.  Small detectors cannot fill 148 SMs with one thread per
+// ray, so each ray's samples are split into K contiguous chunks on K adjacent
+// lanes and summed with a fixed shuffle tree.  K is a function of the detector
+// size only, so every FP mode (projection, correction, residual; one view or a
+// batch) produces identical bits for the same ray.
+__host__ __device__ inline int lanes_for(int rows, int cols) {
+#ifdef CT_FORCE_LANES
+  return CT_FORCE_LANES;
+#endif
+  const long long px = (long long)rows * cols;
+  return px >= 131072 ? 1 : px >= 65536 ? 2 : px >= 32768 ? 4 : 8;
+}
+// warp pixel patch: K=1 8x4, K=2 4x4, K=4 4x2, K=8 2x2; block = FP_WX x FP_WY warps
+__host__ __device__ inline int tile_ww(int K) { return K == 1 ? CT_FP_WW1 : (K == 8 ? 2 : 4); }
+__host__ __device__ inline int tile_wh(int K) { return (32 / K) / tile_ww(K); }
+
+// Linear-interpolation march of samples [k, k_end) of one ray (+ the last
+// sample k_last when with_last), returning the fp32 sum of the values.
+template <class Geo, int OCT, bool WRAP>
+__device__ __forceinline__ float march_linear(const Geo& geo, const RayF& ry, int k, int k_end,
+                                              bool with_last, float k_last) {
+  // Linear interpolation.  OCT: consecutive samples are half a voxel apart, so
+  // a sample in the same cell as its predecessor skips its (predicated-off)
+  // 32-byte load and reuses the live cell.  Plain: the same 8 values from mu.
+  // Same cells, weights and summation grouping either way.
+  //
+  // The chunk is marched as FP_CHAINS independent chains over consecutive
+  // sub-ranges, each with its own live cell: the chains' gathers are in
+  // flight together (a single chain serialises load -> evaluate -> next load
+  // through its cell registers), and one f32x2 locate serves two chains.
+  struct Chain {
+    int prev = INT_MIN;   // no cell (indices are >= -1)
+    float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pb = make_float4(0.f, 0.f, 0.f, 0.f);
+    float sum = 0.0f;
+  };
+  auto value = [&](Chain& ch, const Cell& c) -> float {
+    if (OCT == GL_OCT) {
+      const int idx = geo.template gather_index<WRAP>(c);
+      // signed: the cylindrical r bits make the first cell's index -1 (kRMagic)
+      if (idx != ch.prev) ld_cell(geo.oct + 2 * (ptrdiff_t)idx, ch.pa, ch.pb);
+      ch.prev = idx;   // (unconditional: equal when not reloaded; no predicated move)
+      return trilinear_eval(ch.pa, ch.pb, c.w0, c.w1, c.w2);
+    }
+    if (OCT == GL_QUAD) {
+      // bilinear layers k, k+1 of the cell; the h terms are their
+      // difference (two f32x2 subtractions)
+      const int idx = geo.template gather_index<WRAP>(c);
+      if (idx != ch.prev) {
+        const float4 a = ld_vquad(geo.oct + (ptrdiff_t)idx);
+        const float4 b = ld_vquad(geo.oct + (ptrdiff_t)idx + geo.cell_kstride);
+        ch.pa = a;
+        float x0, x1, y0, y1;
+        upk(sub2(pk(b.x, b.y), pk(a.x, a.y)), x0, x1);
+        upk(sub2(pk(b.z, b.w), pk(a.z, a.w)), y0, y1);
+        ch.pb = make_float4(x0, x1, y0, y1);
+      }
+      ch.prev = idx;
+      return trilinear_eval(ch.pa, ch.pb, c.w0, c.w1, c.w2);
+    }
+    float4 a, b, ca, cb;
+    geo.fetch_plain(c, a, b);
+    trilinear_coeffs(a, b, ca, cb);
+    return trilinear_eval(ca, cb, c.w0, c.w1, c.w2);
+  };
+  constexpr int NC = FP_CHAINS;
+  Chain ch[NC];
+  int kc[NC], ke[NC];
+  {
+    const int len = k_end - k;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      kc[c] = k + (c * len) / NC;
+      ke[c] = k + ((c + 1) * len) / NC;
+    }
+  }
+  // every chain has >= len/NC - 1 samples; 4 samples per iteration
+  const int iters = ((k_end - k) / NC) / (4 / NC);
+  f32x2 kf01 = pk((float)kc[0], (float)kc[1]);
+#pragma unroll FP_UNROLL
+  for (int it = 0; it < iters; ++it) {
+    Cell c0, c1, c2, c3;
+    if (NC == 2) {
+      // float sample counters (exact below 2^24): no int->float conversions
+      geo.locate2(kf01, ry, c0, c1);
+      geo.locate2(add2(kf01, dup2(1.0f)), ry, c2, c3);
+      kf01 = add2(kf01, dup2(2.0f));
+      const float a0 = value(ch[0], c0);
+      const float b0 = value(ch[1], c1);
+      const float a1 = value(ch[0], c2);
+      const float b1 = value(ch[1], c3);
+      ch[0].sum += a0 + a1;
+      ch[1].sum += b0 + b1;
+    } else {
+      geo.locate2(pk((float)kc[0], (float)kc[1]), ry, c0, c1);
+      geo.locate2(pk((float)kc[NC - 2], (float)kc[NC - 1]), ry, c2, c3);
+      ch[0].sum += value(ch[0], c0);
+      ch[1].sum += value(ch[1], c1);
+      ch[NC - 2].sum += value(ch[NC - 2], c2);
+      ch[NC - 1].sum += value(ch[NC - 1], c3);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) ++kc[c];
+    }
+  }
+  if (NC == 2) {
+    kc[0] += 2 * iters;
+    kc[1] += 2 * iters;
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+    for (; kc[c] < ke[c]; ++kc[c]) ch[c].sum += value(ch[c], geo.locate1((float)kc[c], ry));
+  float sum = ch[0].sum;
+#pragma unroll
+  for (int c = 1; c < NC; ++c) sum += ch[c].sum;
+  if (with_last) sum += value(ch[NC - 1], geo.locate1(k_last, ry));
+  return sum;
+}
+
+// One sub-ray, chunk `chunk` of `K`: returns this chunk's in-support sample
+// count and adds the fp32 sum of its interpolated values into acc (COUNT_ONLY:
+// chunk 0 returns the whole ray's count, without marching).
+template <class Geo, bool NEAREST, int OCT, bool COUNT_ONLY>
+__device__ __forceinline__ int march(const Geo& geo, const ct_ray_view& v, double cu, double cv,
+                                     double step, float& acc, int chunk, int K) {
+  double d[3];
+  subray_dir(v, cu, cv, d);
+  double t0, t1;
+  if (!geo.interval(v.src, d, t0, t1)) return 0;
+  if (t1 <= t0) return 0;
+  const int n = (int)ceil(ddiv(dsub(t1, t0), step));
+  const double t_last = dadd(t0, dmul((double)(n - 1) + 0.5, step));
+  const bool last_in = geo.inside(v.src, d, t_last);
+  if (COUNT_ONLY) return chunk == 0 ? n - 1 + (last_in ? 1 : 0) : 0;
+  // fp32 march relative to the first sample position
+  const double ts = dadd(t0, dmul(0.5, step));
+  RayF ry;
+  {
+    double e[3], inc[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      e[a] = v.src[a] + ts * d[a];
+      inc[a] = step * d[a];
+    }
+    geo.setup_ray(e, inc, n, ry);
+  }
+  const int n_int = n - 1;
+  // interior samples [k, k_end) of this chunk; the last sample goes to chunk K-1
+  int k = (chunk * n_int) / K;
+  const int k_end = ((chunk + 1) * n_int) / K;
+  const bool own_last = chunk == K - 1;
+  float sum = 0.0f;
+  if (NEAREST) {
+    for (; k + 4 <= k_end; k += 4) {
+      float s4[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float kq = (float)(k + q);
+        s4[q] = geo.sample_nearest(fmaf(kq, ry.ix, ry.ex), fmaf(kq, ry.iy, ry.ey),
+                                   fmaf(kq, ry.iz, ry.ez));
+      }
+      sum += (s4[0] + s4[1]) + (s4[2] + s4[3]);
+    }
+    for (; k < k_end; ++k) {
+      const float kf = (float)k;
+      sum += geo.sample_nearest(fmaf(kf, ry.ix, ry.ex), fmaf(kf, ry.iy, ry.ey),
+                                fmaf(kf, ry.iz, ry.ez));
+    }
+    if (own_last && last_in && geo.interp_nonzero(v.src, d, t_last)) {
+      const float kf = (float)n_int;
+      sum += geo.sample_nearest(fmaf(kf, ry.ix, ry.ex), fmaf(kf, ry.iy, ry.ey),
+                                fmaf(kf, ry.iz, ry.ez));
+    }
+    acc += sum;
+    return (k_end - (chunk * n_int) / K) + ((own_last && last_in) ? 1 : 0);
+  }
+  const bool with_last = own_last && last_in && geo.interp_nonzero(v.src, d, t_last);
+  // rays crossing theta = 2 pi need the wrapped cell index; the choice is
+  // warp-uniform so the two loop versions never diverge within a warp
+  if (__any_sync(__activemask(), ry.wrap))
+    sum = march_linear<Geo, OCT, true>(geo, ry, k, k_end, with_last, (float)n_int);
+  else
+    sum = march_linear<Geo, OCT, false>(geo, ry, k, k_end, with_last, (float)n_int);
+  acc += sum;
+  return (k_end - (chunk * n_int) / K) + ((own_last && last_in) ? 1 : 0);
+}
+
+
+template <class Geo, int EPI, bool NEAREST, int OCT>
+__global__ void __maxnreg__(CT_FP_MAXREG) fp_kernel(const FpArgs<Geo> a) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int K = a.lanes;
+  const int ww = tile_ww(K), wh = tile_wh(K);
+  const int chunk = lane & (K - 1);
+  const int rslot = lane / K;
+  // each warp covers a ww x wh pixel patch, the block FP_WX x FP_WY warps
+  const int col = blockIdx.x * (FP_WX * ww) + (warp % FP_WX) * ww + rslot % ww;
+  const int row = blockIdx.z * (FP_WY * wh) + (warp / FP_WX) * wh + rslot / ww;
+  const int b = blockIdx.y;
+  const int vid = a.view_ids ? a.view_ids[b] : b;
+  const bool active = row < a.rows && col < a.cols;
+  const size_t npix = (size_t)a.rows * a.cols;
+  const size_t pix = (size_t)row * a.cols + col;
+
+  float acc = 0.0f;
+  int count = 0;
+  if (active && a.ss == 1) {
+    // one sub-ray at the pixel centre ((0 + .5)/1 - .5 = 0 exactly): the view
+    // basis is dead after the per-ray setup, keeping the march loop's
+    // register footprint small
+    count = march<Geo, NEAREST, OCT, EPI == EPI_ROWMAX>(a.geo, a.views[vid], (double)col,
+                                                       (double)row, a.step, acc, chunk, K);
+  } else if (active) {
+    const ct_ray_view& v = a.views[vid];
+    const int ss = a.ss;
+    for (int sv = 0; sv < ss; ++sv) {
+      const double off_v = dsub(ddiv((double)sv + 0.5, (double)ss), 0.5);
+      for (int su = 0; su < ss; ++su) {
+        const double off_u = dsub(ddiv((double)su + 0.5, (double)ss), 0.5);
+        count += march<Geo, NEAREST, OCT, EPI == EPI_ROWMAX>(
+            a.geo, v, dadd((double)col, off_u), dadd((double)row, off_v), a.step, acc, chunk, K);
+      }
+    }
+  }
+  if (K > 1) {
+    // fixed-order tree over the K chunks of a ray (lanes of a ray are adjacent)
+    for (int o = 1; o < K; o <<= 1) {
+      acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      count += __shfl_xor_sync(0xffffffffu, count, o);
+    }
+  }
+  const bool lead = chunk == 0;   // writes the ray's outputs
+  const double inv_ss2 = ddiv(1.0, (double)(a.ss * a.ss));
+  // out_w = wacc * step * inv_ss2, out_p = acc * step * inv_ss2 (_kernels.py:292-293)
+  const double w64 = dmul(dmul((double)count, a.step), inv_ss2);
+  const double p64 = (double)acc * a.step * inv_ss2;
+
+  if (EPI == EPI_PROJECT) {
+    if (active && lead) {
+      a.out0[(size_t)b * npix + pix] = (float)p64;
+      if (a.out1) a.out1[(size_t)b * npix + pix] = (float)w64;
+    }
+  } else if (EPI == EPI_CORR) {
+    if (active && lead) {
+      float c = 0.0f;
+      if (w64 > a.row_thr[vid]) {
+        const float pm = a.p_meas[(size_t)vid * npix + pix];
+        c = (pm - (float)p64) / (float)w64;
+      }
+      a.out0[(size_t)b * npix + pix] = c;
+    }
+  } else {
+    double x = 0.0;
+    if (active && lead) {
+      if (EPI == EPI_RESID) {
+        // compare with the fp32 simulation, i.e. what a stored projection of
+        // this volume holds: consistent data gives exactly 0, as in the reference
+        const double r = (double)a.p_meas[(size_t)vid * npix + pix] - (double)(float)p64;
+        x = r * r;
+      } else {
+        x = w64;
+      }
+    }
+    __shared__ double sred[FP_THREADS / 32];
+    x = (EPI == EPI_RESID) ? warp_sum(x) : warp_max(x);
+    if (lane == 0) sred[warp] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = sred[0];
+      for (int w = 1; w < FP_THREADS / 32; ++w)
+        t = (EPI == EPI_RESID) ? t + sred[w] : fmax(t, sred[w]);
+      if (EPI == EPI_RESID) {
+        const size_t blk = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        a.red[blk] = t;
+      } else {
+        // non-negative doubles order like their bit patterns
+        atomicMax(reinterpret_cast<unsigned long long*>(a.red + b),
+                  (unsigned long long)__double_as_longlong(t));
+      }
+    }
+  }
+}
+
+// Deterministic second stage: fixed-order sum of the per-block partials.
+__global__ void __launch_bounds__(1024) sum_partials_kernel(const double* __restrict__ part,
+                                                            int64_t n, double* accum) {
+  __shared__ double s[32];
+  double x = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) x += part[i];
+  x = warp_sum(x);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
+    *accum += t;
+  }
+}
+
+dim3 fp_grid(const ct_batch& b) {
+  const int K = lanes_for(b.det_rows, b.det_cols);
+  const int tw = FP_WX * tile_ww(K), th = FP_WY * tile_wh(K);
+  return dim3((b.det_cols + tw - 1) / tw, b.n_batch, (b.det_rows + th - 1) / th);
+}
+
+int check_batch(const ct_batch* b, const void* views, const ct_sampling* s) {
+  if (!b || !views || !s) return set_err(CT_ERR_ARG, "null batch/views/sampling");
+  if (b->n_batch < 1 || b->n_batch > 65535 || b->det_rows < 1 || b->det_cols < 1 ||
+      fp_grid(*b).z > 65535)
+    return set_err(CT_ERR_ARG, "bad batch dimensions");
+  if (!(s->step > 0.0) || s->supersample < 1) return set_err(CT_ERR_ARG, "bad sampling");
+  return CT_OK;
+}
+
+template <class Geo, int EPI>
+int launch_fp(const Geo& geo, const ct_ray_view* views, const ct_batch& b, const ct_sampling& s,
+              const float* p_meas, const double* thr, float* o0, float* o1, double* red,
+              cudaStream_t st) {
+  FpArgs<Geo> a;
+  a.geo = geo;
+  a.views = views;
+  a.view_ids = b.view_ids;
+  a.rows = b.det_rows;
+  a.cols = b.det_cols;
+  a.ss = s.supersample;
+  a.lanes = lanes_for(b.det_rows, b.det_cols);
+  a.step = s.step;
+  a.p_meas = p_meas;
+  a.row_thr = thr;
+  a.out0 = o0;
+  a.out1 = o1;
+  a.red = red;
+  if (s.nearest)
+    fp_kernel<Geo, EPI, true, GL_PLAIN><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
+  else if (EPI != EPI_ROWMAX && geo.oct && geo.quad)
+    fp_kernel<Geo, EPI, false, GL_QUAD><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
+  else if (EPI != EPI_ROWMAX && geo.oct)
+    fp_kernel<Geo, EPI, false, GL_OCT><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
+  else
+    fp_kernel<Geo, EPI, false, GL_PLAIN><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
+  return check_launch("fp_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// gather layout: cell m holds the trilinear polynomial coefficients of its
+// 2x2x2 neighbourhood (r/h or x/y/z clamp, theta wrap) as two float4 = one
+// 32-byte sector, so one FP sample is one 256-bit load instead of 8 scattered
+// loads.
+// ---------------------------------------------------------------------------
+// one h-layer (blockIdx.y = kc) per grid row; cells past the layer's rows are
+// the stride padding (zeroed, never read)
+__global__ void pack_gather_cyl_kernel(const float* __restrict__ mu, int nh, int nt, int nr,
+                                       unsigned ks, float4* __restrict__ oct) {
+  // cells (kc, jc, ic), kc in [0, nh], jc in [0, nt], ic in [0, nr]: corner
+  // (kc-1, jc-1, ic-1); index -1 is a halo (r/h: copy of 0; theta: row nt-1)
+  const unsigned rem = blockIdx.x * blockDim.x + threadIdx.x;
+  if (rem >= ks) return;
+  const int kc = blockIdx.y;
+  const size_t m = (size_t)kc * ks + rem;
+  const unsigned js = (unsigned)nr + 1u;
+  const int jc = (int)(rem / js), ic = (int)(rem % js);
+  if (jc > nt) {
+    oct[2 * m] = oct[2 * m + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
+  const int i = max(ic - 1, 0), i1 = min(ic, nr - 1);
+  const int k = max(kc - 1, 0), k1 = min(kc, nh - 1);
+  const int j = (jc == 0) ? nt - 1 : jc - 1, j1 = (jc == nt) ? 0 : jc;
+  auto M = [&](int kk, int jj, int ii) { return __ldg(mu + ((int64_t)kk * nt + jj) * nr + ii); };
+  float4 ca, cb;
+  trilinear_coeffs(make_float4(M(k, j, i), M(k, j, i1), M(k, j1, i), M(k, j1, i1)),
+                   make_float4(M(k1, j, i), M(k1, j, i1), M(k1, j1, i), M(k1, j1, i1)), ca, cb);
+  oct[2 * m] = ca;
+  oct[2 * m + 1] = cb;
+}
+
+__global__ void pack_gather_cart_kernel(const float* __restrict__ mu, int nz, int ny, int nx,
+                                        unsigned ks, float4* __restrict__ oct) {
+  // cells (kc, jc, ic) in [0, n] per axis: corner (kc-1, jc-1, ic-1)
+  const unsigned rem = blockIdx.x * blockDim.x + threadIdx.x;
+  if (rem >= ks) return;
+  const int kc = blockIdx.y;
+  const size_t m = (size_t)kc * ks + rem;
+  const unsigned js = (unsigned)nx + 1u;
+  const int jc = (int)(rem / js), ic = (int)(rem % js);
+  if (jc > ny) {
+    oct[2 * m] = oct[2 * m + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
+  const int i = max(ic - 1, 0), i1 = min(ic, nx - 1);
+  const int j = max(jc - 1, 0), j1 = min(jc, ny - 1);
+  const int k = max(kc - 1, 0), k1 = min(kc, nz - 1);
+  auto M = [&](int kk, int jj, int ii) { return __ldg(mu + ((int64_t)kk * ny + jj) * nx + ii); };
+  float4 ca, cb;
+  trilinear_coeffs(make_float4(M(k, j, i), M(k, j, i1), M(k, j1, i), M(k, j1, i1)),
+                   make_float4(M(k1, j, i), M(k1, j, i1), M(k1, j1, i), M(k1, j1, i1)), ca, cb);
+  oct[2 * m] = ca;
+  oct[2 * m + 1] = cb;
+}
+
+// GL_QUAD: cell (kc, jc, ic), kc in [0, nz+1]: the bilinear polynomial
+// (c0, cr, ct, crt) of layer kc-1 (clamped; -1 and n are halo copies) over
+// rows jc-1, jc (theta wraps / y clamps) and columns ic-1, ic (clamped).  The
+// trilinear cell of layers k, k+1 is (L_k, L_k+1 - L_k): the same fp32 ops as
+// trilinear_coeffs, so GL_QUAD, GL_OCT and the plain path agree bit for bit.
+template <bool CYL>
+__global__ void pack_vquad_kernel(const float* __restrict__ mu, int nk, int nj, int ni,
+                                  unsigned ks, float4* __restrict__ q) {
+  const unsigned rem = blockIdx.x * blockDim.x + threadIdx.x;
+  if (rem >= ks) return;
+  const int kc = blockIdx.y;
+  const size_t m = (size_t)kc * ks + rem;
+  const unsigned js = (unsigned)ni + 1u;
+  const int jc = (int)(rem / js), ic = (int)(rem % js);
+  if (jc > nj) {
+    q[m] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
+  const int k = min(max(kc - 1, 0), nk - 1);
+  const int i = max(ic - 1, 0), i1 = min(ic, ni - 1);
+  int j, j1;
+  if (CYL) {
+    j = (jc == 0) ? nj - 1 : jc - 1;
+    j1 = (jc == nj) ? 0 : jc;
+  } else {
+    j = max(jc - 1, 0);
+    j1 = min(jc, nj - 1);
+  }
+  const float* p0 = mu + ((int64_t)k * nj + j) * ni;
+  const float* p1 = mu + ((int64_t)k * nj + j1) * ni;
+  // the layer's bilinear coefficients (c0, cr, ct, crt), trilinear_coeffs' ops
+  const float a0 = __ldg(p0 + i), a1 = __ldg(p0 + i1), a2 = __ldg(p1 + i), a3 = __ldg(p1 + i1);
+  const float dr0 = a1 - a0, dr1 = a3 - a2;
+  q[m] = make_float4(a0, dr0, a2 - a0, dr1 - dr0);
+}
+
+unsigned gather_ks_cyl(const ct_cyl_grid& g) {
+  return gather_layer_stride((unsigned)CylGeo::gather_rows(g.n_theta), (unsigned)g.n_r + 1u);
+}
+unsigned gather_ks_cart(const ct_cart_grid& g) {
+  return gather_layer_stride((unsigned)g.n_y + 1u, (unsigned)g.n_x + 1u);
+}
+// gather buffer length in floats: (n+1) layers x 8 floats, or GL_QUAD (n+2) x 4
+int64_t gather_floats_cyl(const ct_cyl_grid& g) {
+  const unsigned ks = gather_ks_cyl(g);
+  return gather_quad(ks) ? 4 * (int64_t)(g.n_h + 2) * ks : 8 * (int64_t)(g.n_h + 1) * ks;
+}
+int64_t gather_floats_cart(const ct_cart_grid& g) {
+  const unsigned ks = gather_ks_cart(g);
+  return gather_quad(ks) ? 4 * (int64_t)(g.n_z + 2) * ks : 8 * (int64_t)(g.n_z + 1) * ks;
+}
+
+
+}  // namespace
+
+extern "C" {
+
+int ct_fp_cyl(const float* mu, const float* gather, const ct_cyl_grid* grid, const ct_ray_view* views,
+              const ct_batch* batch, const ct_sampling* s, float* out_p, float* out_w,
+              ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cyl(grid))) return rc;
+  if (!mu || !out_p) return set_err(CT_ERR_ARG, "null mu/out_p");
+  CylGeo geo;
+  geo.init(mu, gather, *grid);
+  return launch_fp<CylGeo, EPI_PROJECT>(geo, views, *batch, *s, nullptr, nullptr, out_p, out_w,
+                                        nullptr, CT_STREAM(stream));
+}
+
+int ct_fp_cart(const float* mu, const float* gather, const ct_cart_grid* grid, const ct_ray_view* views,
+               const ct_batch* batch, const ct_sampling* s, float* out_p, float* out_w,
+               ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cart(grid))) return rc;
+  if (!mu || !out_p) return set_err(CT_ERR_ARG, "null mu/out_p");
+  CartGeo geo;
+  geo.init(mu, gather, *grid);
+  return launch_fp<CartGeo, EPI_PROJECT>(geo, views, *batch, *s, nullptr, nullptr, out_p, out_w,
+                                         nullptr, CT_STREAM(stream));
+}
+
+int ct_fp_cyl_correction(const float* mu, const float* gather, const ct_cyl_grid* grid, const ct_ray_view* views,
+                         const ct_batch* batch, const ct_sampling* s, const float* p_meas,
+                         const double* row_thr, float* corr, ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cyl(grid))) return rc;
+  if (!mu || !p_meas || !row_thr || !corr) return set_err(CT_ERR_ARG, "null pointer");
+  CylGeo geo;
+  geo.init(mu, gather, *grid);
+  return launch_fp<CylGeo, EPI_CORR>(geo, views, *batch, *s, p_meas, row_thr, corr, nullptr,
+                                     nullptr, CT_STREAM(stream));
+}
+
+int ct_fp_cart_correction(const float* mu, const float* gather, const ct_cart_grid* grid, const ct_ray_view* views,
+                          const ct_batch* batch, const ct_sampling* s, const float* p_meas,
+                          const double* row_thr, float* corr, ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cart(grid))) return rc;
+  if (!mu || !p_meas || !row_thr || !corr) return set_err(CT_ERR_ARG, "null pointer");
+  CartGeo geo;
+  geo.init(mu, gather, *grid);
+  return launch_fp<CartGeo, EPI_CORR>(geo, views, *batch, *s, p_meas, row_thr, corr, nullptr,
+                                      nullptr, CT_STREAM(stream));
+}
+
+int64_t ct_residual_scratch_len(const ct_batch* batch) {
+  if (!batch) return 0;
+  dim3 g = fp_grid(*batch);
+  return (int64_t)g.x * g.y * g.z;
+}
+
+static int finish_residual(const ct_batch* batch, double* scratch, double* accum,
+                           cudaStream_t st) {
+  sum_partials_kernel<<<1, 1024, 0, st>>>(scratch, ct_residual_scratch_len(batch), accum);
+  return check_launch("sum_partials_kernel");
+}
+
+int ct_fp_cyl_residual(const float* mu, const float* gather, const ct_cyl_grid* grid, const ct_ray_view* views,
+                       const ct_batch* batch, const ct_sampling* s, const float* p_meas,
+                       double* scratch, double* accum, ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cyl(grid))) return rc;
+  if (!mu || !p_meas || !scratch || !accum) return set_err(CT_ERR_ARG, "null pointer");
+  CylGeo geo;
+  geo.init(mu, gather, *grid);
+  rc = launch_fp<CylGeo, EPI_RESID>(geo, views, *batch, *s, p_meas, nullptr, nullptr, nullptr,
+                                    scratch, CT_STREAM(stream));
+  return rc ? rc : finish_residual(batch, scratch, accum, CT_STREAM(stream));
+}
+
+int ct_fp_cart_residual(const float* mu, const float* gather, const ct_cart_grid* grid, const ct_ray_view* views,
+                        const ct_batch* batch, const ct_sampling* s, const float* p_meas,
+                        double* scratch, double* accum, ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cart(grid))) return rc;
+  if (!mu || !p_meas || !scratch || !accum) return set_err(CT_ERR_ARG, "null pointer");
+  CartGeo geo;
+  geo.init(mu, gather, *grid);
+  rc = launch_fp<CartGeo, EPI_RESID>(geo, views, *batch, *s, p_meas, nullptr, nullptr, nullptr,
+                                     scratch, CT_STREAM(stream));
+  return rc ? rc : finish_residual(batch, scratch, accum, CT_STREAM(stream));
+}
+
+int ct_rowsum_max_cyl(const ct_cyl_grid* grid, const ct_ray_view* views, const ct_batch* batch,
+                      const ct_sampling* s, double* max_row, ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cyl(grid))) return rc;
+  if (!max_row) return set_err(CT_ERR_ARG, "null max_row");
+  if (cudaMemsetAsync(max_row, 0, sizeof(double) * batch->n_batch, CT_STREAM(stream)))
+    return check_launch("memset");
+  CylGeo geo;
+  geo.init(nullptr, nullptr, *grid);
+  return launch_fp<CylGeo, EPI_ROWMAX>(geo, views, *batch, *s, nullptr, nullptr, nullptr,
+                                       nullptr, max_row, CT_STREAM(stream));
+}
+
+int ct_rowsum_max_cart(const ct_cart_grid* grid, const ct_ray_view* views,
+                       const ct_batch* batch, const ct_sampling* s, double* max_row,
+                       ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cart(grid))) return rc;
+  if (!max_row) return set_err(CT_ERR_ARG, "null max_row");
+  if (cudaMemsetAsync(max_row, 0, sizeof(double) * batch->n_batch, CT_STREAM(stream)))
+    return check_launch("memset");
+  CartGeo geo;
+  geo.init(nullptr, nullptr, *grid);
+  return launch_fp<CartGeo, EPI_ROWMAX>(geo, views, *batch, *s, nullptr, nullptr, nullptr,
+                                        nullptr, max_row, CT_STREAM(stream));
+}
+
+int64_t ct_gather_floats_cyl(const ct_cyl_grid* grid) {
+  return check_cyl(grid) ? 0 : gather_floats_cyl(*grid);
+}
+
+int64_t ct_gather_floats_cart(const ct_cart_grid* grid) {
+  return check_cart(grid) ? 0 : gather_floats_cart(*grid);
+}
+
+int ct_pack_gather_cyl(const float* mu, const ct_cyl_grid* grid, float* gather,
+                       ct_stream_t stream) {
+  int rc = check_cyl(grid);
+  if (rc) return rc;
+  if (!mu || !gather) return set_err(CT_ERR_ARG, "null mu/gather");
+  if (reinterpret_cast<uintptr_t>(gather) % 16) return set_err(CT_ERR_ARG, "gather not 16B-aligned");
+  if (grid->n_h + 2 > 65535) return set_err(CT_ERR_ARG, "gather layout: n_h + 2 > 65535");
+  const unsigned ks = gather_ks_cyl(*grid);
+  if (gather_quad(ks)) {
+    pack_vquad_kernel<true><<<dim3(blocks_for(ks, 256), grid->n_h + 2), 256, 0, CT_STREAM(stream)>>>(
+        mu, grid->n_h, grid->n_theta, grid->n_r, ks, reinterpret_cast<float4*>(gather));
+    return check_launch("pack_vquad_kernel");
+  }
+  pack_gather_cyl_kernel<<<dim3(blocks_for(ks, 256), grid->n_h + 1), 256, 0, CT_STREAM(stream)>>>(
+      mu, grid->n_h, grid->n_theta, grid->n_r, ks, reinterpret_cast<float4*>(gather));
+  return check_launch("pack_gather_cyl_kernel");
+}
+
+int ct_pack_gather_cart(const float* mu, const ct_cart_grid* grid, float* gather,
+                        ct_stream_t stream) {
+  int rc = check_cart(grid);
+  if (rc) return rc;
+  if (!mu || !gather) return set_err(CT_ERR_ARG, "null mu/gather");
+  if (reinterpret_cast<uintptr_t>(gather) % 16) return set_err(CT_ERR_ARG, "gather not 16B-aligned");
+  if (grid->n_z + 2 > 65535) return set_err(CT_ERR_ARG, "gather layout: n_z + 2 > 65535");
+  const unsigned ks = gather_ks_cart(*grid);
+  if (gather_quad(ks)) {
+    pack_vquad_kernel<false><<<dim3(blocks_for(ks, 256), grid->n_z + 2), 256, 0, CT_STREAM(stream)>>>(
+        mu, grid->n_z, grid->n_y, grid->n_x, ks, reinterpret_cast<float4*>(gather));
+    return check_launch("pack_vquad_kernel");
+  }
+  pack_gather_cart_kernel<<<dim3(blocks_for(ks, 256), grid->n_z + 1), 256, 0, CT_STREAM(stream)>>>(
+      mu, grid->n_z, grid->n_y, grid->n_x, ks, reinterpret_cast<float4*>(gather));
+  return check_launch("pack_gather_cart_kernel");
+}
+
+}  // extern "C"
