@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define CT_ABI_VERSION 5
+#define CT_ABI_VERSION 6
 
 #define CT_OK 0
 #define CT_ERR_ARG (-1)   /* invalid argument (null pointer, bad size) */
@@ -156,6 +156,38 @@ int ct_fp_cart_residual(const float *mu, const float *gather, const ct_cart_grid
                         const ct_batch *batch, const ct_sampling *sampling,
                         const float *p_meas, double *scratch, double *accum,
                         ct_stream_t stream);
+
+/* Residual partials at view-id slots, for a residual split across launches
+ * (ABI v6).  Block partials land where an identity-ordered batch of n_slots
+ * views (view_ids 0..n_slots-1) would put them, so launches over disjoint
+ * view sets fill one scratch (ct_residual_scratch_len of an n_slots batch)
+ * and ct_residual_sum over it is bit-identical to ct_fp_*_residual over all
+ * n_slots views.  batch->view_ids is required.
+ *  - ct_fp_*_correction_resid: the correction epilogue of ct_fp_*_correction
+ *    plus the residual partials of the same simulation (SART: the residual
+ *    FP of pass k and the first subset's correction FP of pass k+1 read the
+ *    same mu, recon.py:171-181 / PAPER.md:182-187);
+ *  - ct_fp_*_residual_slots: residual partials only (no sum);
+ *  - ct_residual_sum: *accum += fixed-order sum of scratch[0..n). */
+int ct_fp_cyl_correction_resid(const float *mu, const float *gather, const ct_cyl_grid *grid,
+                               const ct_ray_view *views, const ct_batch *batch,
+                               const ct_sampling *sampling, const float *p_meas,
+                               const double *row_thr, float *corr, int n_slots,
+                               double *scratch, ct_stream_t stream);
+int ct_fp_cart_correction_resid(const float *mu, const float *gather, const ct_cart_grid *grid,
+                                const ct_ray_view *views, const ct_batch *batch,
+                                const ct_sampling *sampling, const float *p_meas,
+                                const double *row_thr, float *corr, int n_slots,
+                                double *scratch, ct_stream_t stream);
+int ct_fp_cyl_residual_slots(const float *mu, const float *gather, const ct_cyl_grid *grid,
+                             const ct_ray_view *views, const ct_batch *batch,
+                             const ct_sampling *sampling, const float *p_meas, int n_slots,
+                             double *scratch, ct_stream_t stream);
+int ct_fp_cart_residual_slots(const float *mu, const float *gather, const ct_cart_grid *grid,
+                              const ct_ray_view *views, const ct_batch *batch,
+                              const ct_sampling *sampling, const float *p_meas, int n_slots,
+                              double *scratch, ct_stream_t stream);
+int ct_residual_sum(const double *scratch, int64_t n, double *accum, ct_stream_t stream);
 
 /* Geometry-only row-sum maximum per view (the max_row of
  * cyltomo/recon.py:96-98), computed without marching: max_row[b] (device,

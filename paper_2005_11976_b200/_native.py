@@ -20,7 +20,7 @@ LIB_NAME = "libcyltomo_b200.so"
 LIB_PATH = Path(os.environ.get("CT_LIBRARY") or Path(__file__).resolve().parent / LIB_NAME)
 
 CT_OK = 0
-CT_ABI_VERSION = 5
+CT_ABI_VERSION = 6
 
 
 class CylGridC(C.Structure):
@@ -77,6 +77,15 @@ _SIGNATURES = {
                                      C.POINTER(SamplingC), P, P, P, P]),
     "ct_fp_cart_residual": (C.c_int, [P, P, C.POINTER(CartGridC), P, C.POINTER(BatchC),
                                       C.POINTER(SamplingC), P, P, P, P]),
+    "ct_fp_cyl_correction_resid": (C.c_int, [P, P, C.POINTER(CylGridC), P, C.POINTER(BatchC),
+                                             C.POINTER(SamplingC), P, P, P, C.c_int, P, P]),
+    "ct_fp_cart_correction_resid": (C.c_int, [P, P, C.POINTER(CartGridC), P, C.POINTER(BatchC),
+                                              C.POINTER(SamplingC), P, P, P, C.c_int, P, P]),
+    "ct_fp_cyl_residual_slots": (C.c_int, [P, P, C.POINTER(CylGridC), P, C.POINTER(BatchC),
+                                           C.POINTER(SamplingC), P, C.c_int, P, P]),
+    "ct_fp_cart_residual_slots": (C.c_int, [P, P, C.POINTER(CartGridC), P, C.POINTER(BatchC),
+                                            C.POINTER(SamplingC), P, C.c_int, P, P]),
+    "ct_residual_sum": (C.c_int, [P, C.c_int64, P, P]),
     "ct_gather_floats_cyl": (C.c_int64, [C.POINTER(CylGridC)]),
     "ct_gather_floats_cart": (C.c_int64, [C.POINTER(CartGridC)]),
     "ct_pack_gather_cyl": (C.c_int, [P, C.POINTER(CylGridC), P, P]),

@@ -7,7 +7,10 @@ namespace {
 // ---------------------------------------------------------------------------
 // forward projection
 // ---------------------------------------------------------------------------
-enum FpEpi { EPI_PROJECT = 0, EPI_CORR = 1, EPI_RESID = 2, EPI_ROWMAX = 3 };
+// EPI_CORR_RESID: the correction epilogue plus residual partials -- the
+// residual FP of pass k and the first subset's correction FP of pass k+1 read
+// the same mu, so one march serves both (recon.SartRun)
+enum FpEpi { EPI_PROJECT = 0, EPI_CORR = 1, EPI_RESID = 2, EPI_ROWMAX = 3, EPI_CORR_RESID = 4 };
 
 // FP volume layouts: plain mu, the 32-byte polynomial cells (ct_pack_gather_*),
 // or 16-byte corner quads per h layer (large volumes; see gather_quad())
@@ -49,6 +52,12 @@ struct FpArgs {
   float* __restrict__ out0;
   float* __restrict__ out1;
   double* __restrict__ red;  // residual partials / per-view max_row
+  // residual partial slots: 0 -> block (x, b, z) writes partial
+  // (z * gridDim.y + b) * gridDim.x + x; > 0 -> (z * red_rows + view_ids[b]) *
+  // gridDim.x + x, i.e. the slot of the view in an identity-ordered batch of
+  // red_rows views, so launches over disjoint view sets fill one scratch whose
+  // fixed-order sum equals the single launch's bit for bit
+  int red_rows;
 };
 
 // Lanes per ray.  Small detectors cannot fill 148 SMs with one thread per
@@ -303,7 +312,16 @@ __global__ void __maxnreg__(CT_FP_MAXREG) fp_kernel(const FpArgs<Geo> a) {
   } else {
     double x = 0.0;
     if (active && lead) {
-      if (EPI == EPI_RESID) {
+      if (EPI == EPI_CORR_RESID) {
+        // both epilogues from one read of p_meas, with the same ops as
+        // EPI_CORR and EPI_RESID
+        const float pm = a.p_meas[(size_t)vid * npix + pix];
+        float c = 0.0f;
+        if (w64 > a.row_thr[vid]) c = (pm - (float)p64) / (float)w64;
+        a.out0[(size_t)b * npix + pix] = c;
+        const double r = (double)pm - (double)(float)p64;
+        x = r * r;
+      } else if (EPI == EPI_RESID) {
         // compare with the fp32 simulation, i.e. what a stored projection of
         // this volume holds: consistent data gives exactly 0, as in the reference
         const double r = (double)a.p_meas[(size_t)vid * npix + pix] - (double)(float)p64;
@@ -312,16 +330,19 @@ __global__ void __maxnreg__(CT_FP_MAXREG) fp_kernel(const FpArgs<Geo> a) {
         x = w64;
       }
     }
+    constexpr bool SUM = EPI == EPI_RESID || EPI == EPI_CORR_RESID;
     __shared__ double sred[FP_THREADS / 32];
-    x = (EPI == EPI_RESID) ? warp_sum(x) : warp_max(x);
+    x = SUM ? warp_sum(x) : warp_max(x);
     if (lane == 0) sred[warp] = x;
     __syncthreads();
     if (threadIdx.x == 0) {
       double t = sred[0];
       for (int w = 1; w < FP_THREADS / 32; ++w)
-        t = (EPI == EPI_RESID) ? t + sred[w] : fmax(t, sred[w]);
-      if (EPI == EPI_RESID) {
-        const size_t blk = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        t = SUM ? t + sred[w] : fmax(t, sred[w]);
+      if (SUM) {
+        const size_t blk = a.red_rows > 0
+            ? ((size_t)blockIdx.z * a.red_rows + vid) * gridDim.x + blockIdx.x
+            : ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
         a.red[blk] = t;
       } else {
         // non-negative doubles order like their bit patterns
@@ -366,8 +387,9 @@ int check_batch(const ct_batch* b, const void* views, const ct_sampling* s) {
 template <class Geo, int EPI>
 int launch_fp(const Geo& geo, const ct_ray_view* views, const ct_batch& b, const ct_sampling& s,
               const float* p_meas, const double* thr, float* o0, float* o1, double* red,
-              cudaStream_t st) {
+              cudaStream_t st, int red_rows = 0) {
   FpArgs<Geo> a;
+  a.red_rows = red_rows;
   a.geo = geo;
   a.views = views;
   a.view_ids = b.view_ids;
@@ -502,6 +524,26 @@ int64_t gather_floats_cart(const ct_cart_grid& g) {
 }
 
 
+// Residual partials at view-id slots (FpArgs::red_rows): the scratch of an
+// identity-ordered batch of n_slots views, filled by launches over disjoint
+// view sets and summed once by ct_residual_sum.
+int check_slots(const ct_batch* batch, int n_slots, const double* scratch) {
+  if (!batch->view_ids) return set_err(CT_ERR_ARG, "residual slots need view ids");
+  if (n_slots < 1 || n_slots > 65535) return set_err(CT_ERR_ARG, "bad residual slot count");
+  if (!scratch) return set_err(CT_ERR_ARG, "null scratch");
+  return CT_OK;
+}
+
+template <class Geo, int EPI>
+int fp_slots(const Geo& geo, const ct_ray_view* views, const ct_batch* batch,
+                    const ct_sampling* s, const float* p_meas, const double* row_thr,
+                    float* corr, int n_slots, double* scratch, ct_stream_t stream) {
+  int rc = check_slots(batch, n_slots, scratch);
+  if (rc) return rc;
+  return launch_fp<Geo, EPI>(geo, views, *batch, *s, p_meas, row_thr, corr, nullptr, scratch,
+                             CT_STREAM(stream), n_slots);
+}
+
 }  // namespace
 
 extern "C" {
@@ -590,6 +632,66 @@ int ct_fp_cart_residual(const float* mu, const float* gather, const ct_cart_grid
   rc = launch_fp<CartGeo, EPI_RESID>(geo, views, *batch, *s, p_meas, nullptr, nullptr, nullptr,
                                      scratch, CT_STREAM(stream));
   return rc ? rc : finish_residual(batch, scratch, accum, CT_STREAM(stream));
+}
+
+int ct_fp_cyl_correction_resid(const float* mu, const float* gather, const ct_cyl_grid* grid,
+                               const ct_ray_view* views, const ct_batch* batch,
+                               const ct_sampling* s, const float* p_meas,
+                               const double* row_thr, float* corr, int n_slots,
+                               double* scratch, ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cyl(grid))) return rc;
+  if (!mu || !p_meas || !row_thr || !corr) return set_err(CT_ERR_ARG, "null pointer");
+  CylGeo geo;
+  geo.init(mu, gather, *grid);
+  return fp_slots<CylGeo, EPI_CORR_RESID>(geo, views, batch, s, p_meas, row_thr, corr, n_slots,
+                                          scratch, stream);
+}
+
+int ct_fp_cart_correction_resid(const float* mu, const float* gather, const ct_cart_grid* grid,
+                                const ct_ray_view* views, const ct_batch* batch,
+                                const ct_sampling* s, const float* p_meas,
+                                const double* row_thr, float* corr, int n_slots,
+                                double* scratch, ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cart(grid))) return rc;
+  if (!mu || !p_meas || !row_thr || !corr) return set_err(CT_ERR_ARG, "null pointer");
+  CartGeo geo;
+  geo.init(mu, gather, *grid);
+  return fp_slots<CartGeo, EPI_CORR_RESID>(geo, views, batch, s, p_meas, row_thr, corr, n_slots,
+                                           scratch, stream);
+}
+
+int ct_fp_cyl_residual_slots(const float* mu, const float* gather, const ct_cyl_grid* grid,
+                             const ct_ray_view* views, const ct_batch* batch,
+                             const ct_sampling* s, const float* p_meas, int n_slots,
+                             double* scratch, ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cyl(grid))) return rc;
+  if (!mu || !p_meas) return set_err(CT_ERR_ARG, "null pointer");
+  CylGeo geo;
+  geo.init(mu, gather, *grid);
+  return fp_slots<CylGeo, EPI_RESID>(geo, views, batch, s, p_meas, nullptr, nullptr, n_slots,
+                                     scratch, stream);
+}
+
+int ct_fp_cart_residual_slots(const float* mu, const float* gather, const ct_cart_grid* grid,
+                              const ct_ray_view* views, const ct_batch* batch,
+                              const ct_sampling* s, const float* p_meas, int n_slots,
+                              double* scratch, ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cart(grid))) return rc;
+  if (!mu || !p_meas) return set_err(CT_ERR_ARG, "null pointer");
+  CartGeo geo;
+  geo.init(mu, gather, *grid);
+  return fp_slots<CartGeo, EPI_RESID>(geo, views, batch, s, p_meas, nullptr, nullptr, n_slots,
+                                      scratch, stream);
+}
+
+int ct_residual_sum(const double* scratch, int64_t n, double* accum, ct_stream_t stream) {
+  if (!scratch || !accum || n < 1) return set_err(CT_ERR_ARG, "bad residual sum arguments");
+  sum_partials_kernel<<<1, 1024, 0, CT_STREAM(stream)>>>(scratch, n, accum);
+  return check_launch("sum_partials_kernel");
 }
 
 int ct_rowsum_max_cyl(const ct_cyl_grid* grid, const ct_ray_view* views, const ct_batch* batch,

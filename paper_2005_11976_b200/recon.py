@@ -254,6 +254,30 @@ class SartEngine:
             self._scratch[n] = torch.empty(length, dtype=torch.float64, device=self.device)
         return self._scratch[n]
 
+    def correction_resid(self, mu, p_meas, slots, n: int, corr, n_slots: int, scratch,
+                         gather=None) -> None:
+        """correction() plus the residual partials of the same simulation at
+        the views' slots of an n_slots-view residual scratch."""
+        b = D.batch_c(n, self.rows, self.cols, slots)
+        fn = "ct_fp_cyl_correction_resid" if self.cyl else "ct_fp_cart_correction_resid"
+        N.call(fn, D.ptr(mu), D.ptr(gather), C.byref(self.gc), D.ptr(self.fp_views),
+               C.byref(b), C.byref(self.samp), D.ptr(p_meas), D.ptr(self.row_thr), D.ptr(corr),
+               int(n_slots), D.ptr(scratch), D.stream_handle())
+
+    def residual_slots(self, mu, p_meas, slots, n: int, n_slots: int, scratch,
+                       gather=None) -> None:
+        """Residual partials of a view set at its slots (no sum)."""
+        b = D.batch_c(n, self.rows, self.cols, slots)
+        fn = "ct_fp_cyl_residual_slots" if self.cyl else "ct_fp_cart_residual_slots"
+        N.call(fn, D.ptr(mu), D.ptr(gather), C.byref(self.gc), D.ptr(self.fp_views),
+               C.byref(b), C.byref(self.samp), D.ptr(p_meas), int(n_slots), D.ptr(scratch),
+               D.stream_handle())
+
+    def residual_sum(self, scratch, accum) -> None:
+        """accum += fixed-order sum of a residual scratch."""
+        N.call("ct_residual_sum", D.ptr(scratch), int(scratch.numel()), D.ptr(accum),
+               D.stream_handle())
+
     def residual(self, mu, p_meas, slots, n: int, accum, gather=None) -> None:
         """accum (device f64 scalar view) += sum (p - A mu)^2 over the batch."""
         b = D.batch_c(n, self.rows, self.cols, slots)
@@ -442,6 +466,20 @@ class SartRun:
         self.use_graph = (len(self.subsets) >= self.GRAPH_MIN_SUBSETS
                           if use_graph is None else bool(use_graph))
         self._graphs = {}
+        # Deferred residual (OS-SART, eager passes): the residual FP of pass k
+        # and the correction FP of pass k+1's first subset read the same mu,
+        # so pass k marches only the other subsets' views for its residual and
+        # pass k+1's first correction launch adds the first subset's partials
+        # (same slots, same fixed-order sum: bit-identical residuals, one
+        # subset's FP fewer per pass).  finalize() completes a pending one.
+        self.fuse_residual = (not self.use_graph and len(self.subsets) > 1
+                              and os.environ.get("CT_RESID_FUSE", "1") != "0")
+        self._pending = None                             # pass index awaiting subset 0
+        self._gather_mu = False                          # gather holds the current mu
+        if self.fuse_residual:
+            rest = np.setdiff1d(np.arange(ps.geom.n_proj), self.subsets[0])
+            self.rest_slots = D.upload_i32(rest) if len(rest) else None
+            self.n_rest = len(rest)
 
     def _timed(self, kind, s, fn, *args):
         if self.launch_log is None:
@@ -470,25 +508,70 @@ class SartRun:
             self._empty_checked = True
             self.eng.check_empty_views(self._max_row.numpy(), order_slots=self.order)
 
-    def _pass_body(self, residual: bool, after_updates=None) -> None:
+    def _pack(self, k) -> None:
+        if not self._gather_mu:
+            self._timed("pack_gather", k, self.eng.pack, self.mu, self.gather)
+        self._gather_mu = True
+
+    def _store_residual(self, k) -> None:
+        k = min(k, self.resid.numel() - 1)
+        self.resid[k:k + 1].copy_(self.resid_cur)
+
+    def _pass_body(self, residual: bool, after_updates=None, fuse: bool = False) -> None:
         e = self.eng
         up = self._upload if (self._upload is not None and not self._upload.done) else None
+        n_proj = self.ps.geom.n_proj
         for k, (s, slots) in enumerate(zip(self.subsets, self.subset_slots)):
             if up is not None:
                 up.before_subset(k)
-            self._timed("pack_gather", k, e.pack, self.mu, self.gather)
-            self._timed("fp_correction", k, e.correction, self.mu, self._p_meas, slots, len(s),
-                        self.corr, self.gather)
+            self._pack(k)
+            if k == 0 and self._pending is not None:
+                # completes the previous pass's residual (same mu)
+                scratch = e.residual_scratch(n_proj)
+                self._timed("fp_correction_resid", k, e.correction_resid, self.mu,
+                            self._p_meas, slots, len(s), self.corr, n_proj, scratch,
+                            self.gather)
+                self.resid_cur.zero_()
+                e.residual_sum(scratch, self.resid_cur)
+                self._store_residual(self._pending)
+                self._pending = None
+            else:
+                self._timed("fp_correction", k, e.correction, self.mu, self._p_meas, slots,
+                            len(s), self.corr, self.gather)
             self._timed("pack_quads", k, e.pack_quads, self.corr, len(s), self.quads)
             self._timed("bp_update", k, e.bp_update, self.corr, slots, len(s), self.upd,
                         self.quads)
+            self._gather_mu = False
         if after_updates is not None:
             after_updates()
-        if residual:
+        if residual and fuse:
+            self._pack(-1)
+            if self.n_rest:
+                self._timed("fp_residual", -1, e.residual_slots, self.mu, self._p_meas,
+                            self.rest_slots, self.n_rest, n_proj,
+                            e.residual_scratch(n_proj), self.gather)
+            self._pending = self.passes_done
+        elif residual:
             self.resid_cur.zero_()
-            self._timed("pack_gather", -1, e.pack, self.mu, self.gather)
+            self._pack(-1)
             self._timed("fp_residual", -1, e.residual, self.mu, self._p_meas, self.all_slots,
-                        self.ps.geom.n_proj, self.resid_cur, self.gather)
+                        n_proj, self.resid_cur, self.gather)
+
+    def finalize(self) -> None:
+        """Complete a deferred residual: the first subset's views on the
+        current mu (the gather layout still holds it)."""
+        if self._pending is None:
+            return
+        e = self.eng
+        n_proj = self.ps.geom.n_proj
+        scratch = e.residual_scratch(n_proj)
+        self._pack(-1)
+        self._timed("fp_residual", -2, e.residual_slots, self.mu, self._p_meas,
+                    self.subset_slots[0], len(self.subsets[0]), n_proj, scratch, self.gather)
+        self.resid_cur.zero_()
+        e.residual_sum(scratch, self.resid_cur)
+        self._store_residual(self._pending)
+        self._pending = None
 
     def run_pass(self, residual: bool | None = None) -> None:
         """One pass over all subsets (+ the residual FP if enabled).
@@ -498,6 +581,7 @@ class SartRun:
         per view, which would otherwise be launch-bound."""
         want = self.cfg.compute_residuals if residual is None else residual
         if self.use_graph and self.launch_log is None:
+            self._gather_mu = False          # graph bodies always pack
             torch = D.torch_mod()
             g = self._graphs.get(want)
             if g is None:
@@ -517,20 +601,25 @@ class SartRun:
                 torch.cuda.current_stream().wait_stream(side)
                 self._graphs[want] = g
             g.replay()
+            self._gather_mu = False
+            if want:
+                self._store_residual(self.passes_done)
         else:
-            self._pass_body(want)
-        if want:
-            k = min(self.passes_done, self.resid.numel() - 1)
-            self.resid[k:k + 1].copy_(self.resid_cur)
+            self._eager_pass(want)
         self.passes_done += 1
+
+    def _eager_pass(self, want: bool, after_updates=None) -> None:
+        if want and self.fuse_residual:
+            self._pass_body(True, after_updates, fuse=True)
+            return
+        self.finalize()
+        self._pass_body(want, after_updates)
+        if want:
+            self._store_residual(self.passes_done)
 
     def _run_pass_hooked(self, after_updates) -> None:
         """run_pass (eager) with a hook queued after the last subset's update."""
-        want = self.cfg.compute_residuals
-        self._pass_body(want, after_updates)
-        if want:
-            k = min(self.passes_done, self.resid.numel() - 1)
-            self.resid[k:k + 1].copy_(self.resid_cur)
+        self._eager_pass(self.cfg.compute_residuals, after_updates)
         self.passes_done += 1
 
     def run(self):
@@ -555,6 +644,7 @@ class SartRun:
             else:
                 self.run_pass()
             self.check_empty_views()
+        self.finalize()
         torch.cuda.synchronize(self.eng.device)
         wall = time.perf_counter() - t0
         residuals = ([math.sqrt(float(x)) for x in D.to_host(self.resid)]

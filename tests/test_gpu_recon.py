@@ -320,6 +320,51 @@ def test_graph_replay_bit_identical(small_cyl_setup):
     assert ra.residuals == rb.residuals
 
 
+@pytest.mark.parametrize("n_subsets,n_iter", [(2, 1), (3, 3), (5, 4)])
+def test_deferred_residual_bit_identical(small_cyl_setup, monkeypatch, n_subsets, n_iter):
+    """The residual of pass k split between pass k's FP over the other
+    subsets' views and pass k+1's first correction FP (slot-positioned
+    partials, one fixed-order sum) gives the same bits as one residual launch
+    over all views, and the volumes are unchanged."""
+    from paper_2005_11976_b200.recon import SartRun
+    grid, vol, ps = small_cyl_setup
+    noisy = ProjectionSet(ps.geom, ps.images * 1.02)
+    cfg = SartConfig(n_iterations=n_iter, n_subsets=n_subsets, relaxation=0.6)
+    fused = SartRun(noisy, grid, cfg)
+    assert fused.fuse_residual
+    va, ra = fused.run()
+    monkeypatch.setenv("CT_RESID_FUSE", "0")
+    plain = SartRun(noisy, grid, cfg)
+    assert not plain.fuse_residual
+    vb, rb = plain.run()
+    assert np.array_equal(va.mu, vb.mu)
+    assert ra.residuals == rb.residuals
+    assert len(ra.residuals) == n_iter and all(r > 0 for r in ra.residuals)
+
+
+def test_deferred_residual_cartesian_and_mixed_passes(monkeypatch):
+    """Cartesian grid; passes with and without the residual interleaved
+    (run_pass(residual=...)), finalize() between them."""
+    from paper_2005_11976_b200.recon import SartRun
+    grid = CartGrid.centered(10, 9, 8, 0.5)
+    geom = ScanGeometry(40.0, 30.0, 24, 20, 0.4, (11.5, 9.5), make_circular_trajectory(12, np.radians(330.0)))
+    rng = np.random.default_rng(5)
+    truth = CartVolume(grid, rng.uniform(0.0, 0.1, grid.shape))
+    ps = forward_project_all(truth, geom)
+    cfg = SartConfig(n_iterations=4, n_subsets=3, relaxation=0.5, compute_residuals=False)
+    out = []
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("CT_RESID_FUSE", fuse)
+        run = SartRun(ps, grid, cfg)
+        for want in (True, False, True, True):
+            run.run_pass(residual=want)
+        run.finalize()
+        out.append((run.mu.cpu().numpy(), run.resid.cpu().numpy()))
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1])
+    assert out[0][1][0] > 0 and out[0][1][1] == 0 and out[0][1][3] > 0
+
+
 @pytest.mark.parametrize("quad", ["0", "1"])
 @pytest.mark.parametrize("kind", ["cyl", "cyl_coarse", "cart"])
 def test_gather_layout_matches_plain_path(rng, kind, quad, monkeypatch):
