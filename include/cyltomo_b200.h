@@ -157,36 +157,43 @@ int ct_fp_cart_residual(const float *mu, const float *gather, const ct_cart_grid
                         const float *p_meas, double *scratch, double *accum,
                         ct_stream_t stream);
 
-/* Residual partials at view-id slots, for a residual split across launches
- * (ABI v6).  Block partials land where an identity-ordered batch of n_slots
- * views (view_ids 0..n_slots-1) would put them, so launches over disjoint
- * view sets fill one scratch (ct_residual_scratch_len of an n_slots batch)
- * and ct_residual_sum over it is bit-identical to ct_fp_*_residual over all
- * n_slots views.  batch->view_ids is required.
- *  - ct_fp_*_correction_resid: the correction epilogue of ct_fp_*_correction
- *    plus the residual partials of the same simulation (SART: the residual
- *    FP of pass k and the first subset's correction FP of pass k+1 read the
- *    same mu, recon.py:171-181 / PAPER.md:182-187);
- *  - ct_fp_*_residual_slots: residual partials only (no sum);
- *  - ct_residual_sum: *accum += fixed-order sum of scratch[0..n). */
-int ct_fp_cyl_correction_resid(const float *mu, const float *gather, const ct_cyl_grid *grid,
+/* Row ranges and residual slots (ABI v6), for work split across launches and
+ * ranks (SART residual deferral, recon.py; angle sharding, distributed.py).
+ *  - Rows: the batch's rays are numbered by flattened row f = b * det_rows +
+ *    row; only rows in [row_lo, row_hi) are marched, and the correction of
+ *    row f lands at corr[(f - row_lo) * det_cols + col].
+ *  - Residual slots: block partials land where an identity-ordered batch of
+ *    n_slots views (view_ids 0..n_slots-1) would put them, so launches over
+ *    disjoint views / row ranges aligned to ct_fp_row_tile() fill one
+ *    scratch (ct_residual_scratch_len of an n_slots batch) whose
+ *    ct_residual_sum is bit-identical to ct_fp_*_residual over all n_slots
+ *    views.  batch->view_ids is required with a scratch.
+ *  - ct_fp_*_correction_rows: the correction epilogue of ct_fp_*_correction;
+ *    with a scratch also the residual partials of the same simulation (the
+ *    residual FP of pass k and the first subset's correction FP of pass k+1
+ *    read the same mu, recon.py:171-181 / PAPER.md:182-187);
+ *  - ct_fp_*_residual_rows: residual partials only (no sum);
+ *  - ct_residual_sum: *accum += fixed-order sum of scratch[0..n);
+ *  - ct_fp_row_tile: rows per FP block for this detector. */
+int ct_fp_row_tile(const ct_batch *batch);
+int ct_fp_cyl_correction_rows(const float *mu, const float *gather, const ct_cyl_grid *grid,
+                              const ct_ray_view *views, const ct_batch *batch,
+                              const ct_sampling *sampling, const float *p_meas,
+                              const double *row_thr, float *corr, int64_t row_lo,
+                              int64_t row_hi, int n_slots, double *scratch, ct_stream_t stream);
+int ct_fp_cart_correction_rows(const float *mu, const float *gather, const ct_cart_grid *grid,
                                const ct_ray_view *views, const ct_batch *batch,
                                const ct_sampling *sampling, const float *p_meas,
-                               const double *row_thr, float *corr, int n_slots,
-                               double *scratch, ct_stream_t stream);
-int ct_fp_cart_correction_resid(const float *mu, const float *gather, const ct_cart_grid *grid,
-                                const ct_ray_view *views, const ct_batch *batch,
-                                const ct_sampling *sampling, const float *p_meas,
-                                const double *row_thr, float *corr, int n_slots,
-                                double *scratch, ct_stream_t stream);
-int ct_fp_cyl_residual_slots(const float *mu, const float *gather, const ct_cyl_grid *grid,
+                               const double *row_thr, float *corr, int64_t row_lo,
+                               int64_t row_hi, int n_slots, double *scratch, ct_stream_t stream);
+int ct_fp_cyl_residual_rows(const float *mu, const float *gather, const ct_cyl_grid *grid,
+                            const ct_ray_view *views, const ct_batch *batch,
+                            const ct_sampling *sampling, const float *p_meas, int64_t row_lo,
+                            int64_t row_hi, int n_slots, double *scratch, ct_stream_t stream);
+int ct_fp_cart_residual_rows(const float *mu, const float *gather, const ct_cart_grid *grid,
                              const ct_ray_view *views, const ct_batch *batch,
-                             const ct_sampling *sampling, const float *p_meas, int n_slots,
-                             double *scratch, ct_stream_t stream);
-int ct_fp_cart_residual_slots(const float *mu, const float *gather, const ct_cart_grid *grid,
-                              const ct_ray_view *views, const ct_batch *batch,
-                              const ct_sampling *sampling, const float *p_meas, int n_slots,
-                              double *scratch, ct_stream_t stream);
+                             const ct_sampling *sampling, const float *p_meas, int64_t row_lo,
+                             int64_t row_hi, int n_slots, double *scratch, ct_stream_t stream);
 int ct_residual_sum(const double *scratch, int64_t n, double *accum, ct_stream_t stream);
 
 /* Geometry-only row-sum maximum per view (the max_row of
@@ -236,6 +243,19 @@ int64_t ct_quads_floats(const ct_batch *batch);
 int ct_pack_quads(const float *corr, const ct_batch *batch, float *quads, ct_stream_t stream);
 
 /* Fill trig[0:n] = cos((j+.5)dtheta), trig[n:2n] = sin(...) (fp64). */
+/* Fused BP + SART update restricted to voxels [offset, offset+count) of the
+ * flat [n_h][n_theta][n_r] (or [n_z][n_y][n_x]) volume: a rank's shard in
+ * the angle-sharded OS-SART (distributed.py); every voxel's result equals
+ * ct_bp_*_update's (ABI v6). */
+int ct_bp_cyl_update_range(const float *corr, const float *quads, const ct_det_view *dets,
+                           const ct_batch *batch, const ct_cyl_grid *grid, const double *trig,
+                           const ct_update *upd, int64_t offset, int64_t count,
+                           ct_stream_t stream);
+int ct_bp_cart_update_range(const float *corr, const float *quads, const ct_det_view *dets,
+                            const ct_batch *batch, const ct_cart_grid *grid,
+                            const ct_update *upd, int64_t offset, int64_t count,
+                            ct_stream_t stream);
+
 int ct_cyl_trig(const ct_cyl_grid *grid, double *trig, ct_stream_t stream);
 
 /* Stand-alone update from reduced num/den over voxels [offset, offset+count)

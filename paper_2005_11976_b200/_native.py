@@ -77,14 +77,19 @@ _SIGNATURES = {
                                      C.POINTER(SamplingC), P, P, P, P]),
     "ct_fp_cart_residual": (C.c_int, [P, P, C.POINTER(CartGridC), P, C.POINTER(BatchC),
                                       C.POINTER(SamplingC), P, P, P, P]),
-    "ct_fp_cyl_correction_resid": (C.c_int, [P, P, C.POINTER(CylGridC), P, C.POINTER(BatchC),
-                                             C.POINTER(SamplingC), P, P, P, C.c_int, P, P]),
-    "ct_fp_cart_correction_resid": (C.c_int, [P, P, C.POINTER(CartGridC), P, C.POINTER(BatchC),
-                                              C.POINTER(SamplingC), P, P, P, C.c_int, P, P]),
-    "ct_fp_cyl_residual_slots": (C.c_int, [P, P, C.POINTER(CylGridC), P, C.POINTER(BatchC),
-                                           C.POINTER(SamplingC), P, C.c_int, P, P]),
-    "ct_fp_cart_residual_slots": (C.c_int, [P, P, C.POINTER(CartGridC), P, C.POINTER(BatchC),
-                                            C.POINTER(SamplingC), P, C.c_int, P, P]),
+    "ct_fp_row_tile": (C.c_int, [C.POINTER(BatchC)]),
+    "ct_fp_cyl_correction_rows": (C.c_int, [P, P, C.POINTER(CylGridC), P, C.POINTER(BatchC),
+                                            C.POINTER(SamplingC), P, P, P, C.c_int64,
+                                            C.c_int64, C.c_int, P, P]),
+    "ct_fp_cart_correction_rows": (C.c_int, [P, P, C.POINTER(CartGridC), P, C.POINTER(BatchC),
+                                             C.POINTER(SamplingC), P, P, P, C.c_int64,
+                                             C.c_int64, C.c_int, P, P]),
+    "ct_fp_cyl_residual_rows": (C.c_int, [P, P, C.POINTER(CylGridC), P, C.POINTER(BatchC),
+                                          C.POINTER(SamplingC), P, C.c_int64, C.c_int64,
+                                          C.c_int, P, P]),
+    "ct_fp_cart_residual_rows": (C.c_int, [P, P, C.POINTER(CartGridC), P, C.POINTER(BatchC),
+                                           C.POINTER(SamplingC), P, C.c_int64, C.c_int64,
+                                           C.c_int, P, P]),
     "ct_residual_sum": (C.c_int, [P, C.c_int64, P, P]),
     "ct_gather_floats_cyl": (C.c_int64, [C.POINTER(CylGridC)]),
     "ct_gather_floats_cart": (C.c_int64, [C.POINTER(CartGridC)]),
@@ -102,6 +107,10 @@ _SIGNATURES = {
                                    C.POINTER(UpdateC), P]),
     "ct_bp_cart_update": (C.c_int, [P, P, P, C.POINTER(BatchC), C.POINTER(CartGridC),
                                     C.POINTER(UpdateC), P]),
+    "ct_bp_cyl_update_range": (C.c_int, [P, P, P, C.POINTER(BatchC), C.POINTER(CylGridC), P,
+                                         C.POINTER(UpdateC), C.c_int64, C.c_int64, P]),
+    "ct_bp_cart_update_range": (C.c_int, [P, P, P, C.POINTER(BatchC), C.POINTER(CartGridC),
+                                          C.POINTER(UpdateC), C.c_int64, C.c_int64, P]),
     "ct_quads_floats": (C.c_int64, [C.POINTER(BatchC)]),
     "ct_pack_quads": (C.c_int, [P, C.POINTER(BatchC), P, P]),
     "ct_cyl_trig": (C.c_int, [C.POINTER(CylGridC), P, P]),

@@ -94,6 +94,7 @@ struct BpArgs {
   float* num;
   float* den;
   ct_update upd;
+  int vox_off, vox_end;   // voxels [vox_off, vox_end) (a rank's shard, distributed.py)
 };
 
 // fp64 re-evaluation of one voxel-view with the reference's arithmetic
@@ -182,9 +183,8 @@ __device__ __forceinline__ float2 bp_view_slow(const BpArgs<Vox>& a, int m, int 
 template <class Vox, int MODE, bool QUADS>
 __global__ void __launch_bounds__(BP_THREADS, BP_MIN_BLOCKS) bp_kernel(const __grid_constant__ BpArgs<Vox> a) {
   __shared__ BpPairF sv[BP_CHUNK / 2];
-  const int64_t nvox = a.vox.count();
-  const int m = blockIdx.x * BP_THREADS + threadIdx.x;
-  const bool active = m < nvox;
+  const int m = a.vox_off + blockIdx.x * BP_THREADS + threadIdx.x;
+  const bool active = m < a.vox_end;
   float xw = 0.0f, yw = 0.0f, zw = 0.0f;
   if (active) {
     double w64[3];
@@ -352,7 +352,8 @@ __global__ void __launch_bounds__(BP_THREADS, BP_MIN_BLOCKS) bp_kernel(const __g
 
 template <class Vox, int MODE>
 int launch_bp(const Vox& vox, const float* corr, const float* quads, const ct_det_view* dets,
-              const ct_batch& b, float* num, float* den, const ct_update* upd, cudaStream_t st) {
+              const ct_batch& b, float* num, float* den, const ct_update* upd, cudaStream_t st,
+              int64_t offset = 0, int64_t count = -1) {
   BpArgs<Vox> a;
   a.vox = vox;
   a.corr = corr;
@@ -365,7 +366,10 @@ int launch_bp(const Vox& vox, const float* corr, const float* quads, const ct_de
   a.num = num;
   a.den = den;
   if (upd) a.upd = *upd; else memset(&a.upd, 0, sizeof a.upd);
-  const int64_t nvox = vox.count();
+  const int64_t nvox = count < 0 ? vox.count() : count;
+  a.vox_off = (int)offset;
+  a.vox_end = (int)(offset + nvox);
+  if (nvox == 0) return CT_OK;
   const unsigned blocks = (unsigned)((nvox + BP_THREADS - 1) / BP_THREADS);
   if (quads)
     bp_kernel<Vox, MODE, true><<<blocks, BP_THREADS, 0, st>>>(a);
@@ -476,6 +480,35 @@ int ct_bp_cart_update(const float* corr, const float* quads, const ct_det_view* 
   vox.init(*grid);
   return launch_bp<CartVox, BP_UPDATE>(vox, corr, quads, dets, *batch, nullptr, nullptr, upd,
                                        CT_STREAM(stream));
+}
+
+int ct_bp_cyl_update_range(const float* corr, const float* quads, const ct_det_view* dets,
+                           const ct_batch* batch, const ct_cyl_grid* grid, const double* trig,
+                           const ct_update* upd, int64_t offset, int64_t count,
+                           ct_stream_t stream) {
+  int rc = check_bp(corr, dets, batch);
+  if (rc || (rc = check_cyl(grid))) return rc;
+  if (!trig || !upd || !upd->mu) return set_err(CT_ERR_ARG, "null trig/update/mu");
+  const int64_t n = (int64_t)grid->n_h * grid->n_theta * grid->n_r;
+  if (offset < 0 || count < 0 || offset + count > n) return set_err(CT_ERR_ARG, "bad voxel range");
+  CylVox vox;
+  vox.init(*grid, trig);
+  return launch_bp<CylVox, BP_UPDATE>(vox, corr, quads, dets, *batch, nullptr, nullptr, upd,
+                                      CT_STREAM(stream), offset, count);
+}
+
+int ct_bp_cart_update_range(const float* corr, const float* quads, const ct_det_view* dets,
+                            const ct_batch* batch, const ct_cart_grid* grid, const ct_update* upd,
+                            int64_t offset, int64_t count, ct_stream_t stream) {
+  int rc = check_bp(corr, dets, batch);
+  if (rc || (rc = check_cart(grid))) return rc;
+  if (!upd || !upd->mu) return set_err(CT_ERR_ARG, "null update/mu");
+  const int64_t n = (int64_t)grid->n_z * grid->n_y * grid->n_x;
+  if (offset < 0 || count < 0 || offset + count > n) return set_err(CT_ERR_ARG, "bad voxel range");
+  CartVox vox;
+  vox.init(*grid);
+  return launch_bp<CartVox, BP_UPDATE>(vox, corr, quads, dets, *batch, nullptr, nullptr, upd,
+                                       CT_STREAM(stream), offset, count);
 }
 
 int ct_cyl_trig(const ct_cyl_grid* grid, double* trig, ct_stream_t stream) {

@@ -58,6 +58,10 @@ struct FpArgs {
   // red_rows views, so launches over disjoint view sets fill one scratch whose
   // fixed-order sum equals the single launch's bit for bit
   int red_rows;
+  // flattened-row range (angle sharding, distributed.py): only rays of rows
+  // f = b * rows + row in [frow_lo, frow_hi) are marched, and the correction
+  // of row f lands at out0[(f - frow_lo) * cols + col].  Defaults: all rows.
+  int64_t frow_lo, frow_hi;
 };
 
 // Lanes per ray.  Small detectors cannot fill 148 SMs with one thread per
@@ -258,9 +262,11 @@ __global__ void __maxnreg__(CT_FP_MAXREG) fp_kernel(const FpArgs<Geo> a) {
   const int row = blockIdx.z * (FP_WY * wh) + (warp / FP_WX) * wh + rslot / ww;
   const int b = blockIdx.y;
   const int vid = a.view_ids ? a.view_ids[b] : b;
-  const bool active = row < a.rows && col < a.cols;
+  const int64_t frow = (int64_t)b * a.rows + row;
+  const bool active = row < a.rows && col < a.cols && frow >= a.frow_lo && frow < a.frow_hi;
   const size_t npix = (size_t)a.rows * a.cols;
   const size_t pix = (size_t)row * a.cols + col;
+  const size_t oidx = (size_t)b * npix + pix - (size_t)a.frow_lo * a.cols;   // out0 element
 
   float acc = 0.0f;
   int count = 0;
@@ -307,7 +313,7 @@ __global__ void __maxnreg__(CT_FP_MAXREG) fp_kernel(const FpArgs<Geo> a) {
         const float pm = a.p_meas[(size_t)vid * npix + pix];
         c = (pm - (float)p64) / (float)w64;
       }
-      a.out0[(size_t)b * npix + pix] = c;
+      a.out0[oidx] = c;
     }
   } else {
     double x = 0.0;
@@ -318,7 +324,7 @@ __global__ void __maxnreg__(CT_FP_MAXREG) fp_kernel(const FpArgs<Geo> a) {
         const float pm = a.p_meas[(size_t)vid * npix + pix];
         float c = 0.0f;
         if (w64 > a.row_thr[vid]) c = (pm - (float)p64) / (float)w64;
-        a.out0[(size_t)b * npix + pix] = c;
+        a.out0[oidx] = c;
         const double r = (double)pm - (double)(float)p64;
         x = r * r;
       } else if (EPI == EPI_RESID) {
@@ -387,9 +393,12 @@ int check_batch(const ct_batch* b, const void* views, const ct_sampling* s) {
 template <class Geo, int EPI>
 int launch_fp(const Geo& geo, const ct_ray_view* views, const ct_batch& b, const ct_sampling& s,
               const float* p_meas, const double* thr, float* o0, float* o1, double* red,
-              cudaStream_t st, int red_rows = 0) {
+              cudaStream_t st, int red_rows = 0, int64_t frow_lo = 0,
+              int64_t frow_hi = INT64_MAX) {
   FpArgs<Geo> a;
   a.red_rows = red_rows;
+  a.frow_lo = frow_lo;
+  a.frow_hi = frow_hi;
   a.geo = geo;
   a.views = views;
   a.view_ids = b.view_ids;
@@ -526,7 +535,13 @@ int64_t gather_floats_cart(const ct_cart_grid& g) {
 
 // Residual partials at view-id slots (FpArgs::red_rows): the scratch of an
 // identity-ordered batch of n_slots views, filled by launches over disjoint
-// view sets and summed once by ct_residual_sum.
+// view sets / row ranges and summed once by ct_residual_sum.
+int check_rows(const ct_batch* batch, int64_t row_lo, int64_t row_hi) {
+  if (row_lo < 0 || row_hi <= row_lo || row_hi > (int64_t)batch->n_batch * batch->det_rows)
+    return set_err(CT_ERR_ARG, "bad row range");
+  return CT_OK;
+}
+
 int check_slots(const ct_batch* batch, int n_slots, const double* scratch) {
   if (!batch->view_ids) return set_err(CT_ERR_ARG, "residual slots need view ids");
   if (n_slots < 1 || n_slots > 65535) return set_err(CT_ERR_ARG, "bad residual slot count");
@@ -534,14 +549,21 @@ int check_slots(const ct_batch* batch, int n_slots, const double* scratch) {
   return CT_OK;
 }
 
-template <class Geo, int EPI>
-int fp_slots(const Geo& geo, const ct_ray_view* views, const ct_batch* batch,
-                    const ct_sampling* s, const float* p_meas, const double* row_thr,
-                    float* corr, int n_slots, double* scratch, ct_stream_t stream) {
-  int rc = check_slots(batch, n_slots, scratch);
+template <class Geo>
+int fp_rows(const Geo& geo, const ct_ray_view* views, const ct_batch* batch,
+            const ct_sampling* s, const float* p_meas, const double* row_thr, float* corr,
+            int64_t row_lo, int64_t row_hi, int n_slots, double* scratch, ct_stream_t stream) {
+  int rc = check_rows(batch, row_lo, row_hi);
   if (rc) return rc;
-  return launch_fp<Geo, EPI>(geo, views, *batch, *s, p_meas, row_thr, corr, nullptr, scratch,
-                             CT_STREAM(stream), n_slots);
+  if (corr && !scratch)
+    return launch_fp<Geo, EPI_CORR>(geo, views, *batch, *s, p_meas, row_thr, corr, nullptr,
+                                    nullptr, CT_STREAM(stream), 0, row_lo, row_hi);
+  if ((rc = check_slots(batch, n_slots, scratch))) return rc;
+  if (corr)
+    return launch_fp<Geo, EPI_CORR_RESID>(geo, views, *batch, *s, p_meas, row_thr, corr, nullptr,
+                                          scratch, CT_STREAM(stream), n_slots, row_lo, row_hi);
+  return launch_fp<Geo, EPI_RESID>(geo, views, *batch, *s, p_meas, nullptr, nullptr, nullptr,
+                                   scratch, CT_STREAM(stream), n_slots, row_lo, row_hi);
 }
 
 }  // namespace
@@ -634,58 +656,63 @@ int ct_fp_cart_residual(const float* mu, const float* gather, const ct_cart_grid
   return rc ? rc : finish_residual(batch, scratch, accum, CT_STREAM(stream));
 }
 
-int ct_fp_cyl_correction_resid(const float* mu, const float* gather, const ct_cyl_grid* grid,
-                               const ct_ray_view* views, const ct_batch* batch,
-                               const ct_sampling* s, const float* p_meas,
-                               const double* row_thr, float* corr, int n_slots,
-                               double* scratch, ct_stream_t stream) {
-  int rc = check_batch(batch, views, s);
-  if (rc || (rc = check_cyl(grid))) return rc;
-  if (!mu || !p_meas || !row_thr || !corr) return set_err(CT_ERR_ARG, "null pointer");
-  CylGeo geo;
-  geo.init(mu, gather, *grid);
-  return fp_slots<CylGeo, EPI_CORR_RESID>(geo, views, batch, s, p_meas, row_thr, corr, n_slots,
-                                          scratch, stream);
+int ct_fp_row_tile(const ct_batch* batch) {
+  if (!batch || batch->det_rows < 1 || batch->det_cols < 1) return 0;
+  return FP_WY * tile_wh(lanes_for(batch->det_rows, batch->det_cols));
 }
 
-int ct_fp_cart_correction_resid(const float* mu, const float* gather, const ct_cart_grid* grid,
-                                const ct_ray_view* views, const ct_batch* batch,
-                                const ct_sampling* s, const float* p_meas,
-                                const double* row_thr, float* corr, int n_slots,
-                                double* scratch, ct_stream_t stream) {
-  int rc = check_batch(batch, views, s);
-  if (rc || (rc = check_cart(grid))) return rc;
-  if (!mu || !p_meas || !row_thr || !corr) return set_err(CT_ERR_ARG, "null pointer");
-  CartGeo geo;
-  geo.init(mu, gather, *grid);
-  return fp_slots<CartGeo, EPI_CORR_RESID>(geo, views, batch, s, p_meas, row_thr, corr, n_slots,
-                                           scratch, stream);
-}
-
-int ct_fp_cyl_residual_slots(const float* mu, const float* gather, const ct_cyl_grid* grid,
-                             const ct_ray_view* views, const ct_batch* batch,
-                             const ct_sampling* s, const float* p_meas, int n_slots,
-                             double* scratch, ct_stream_t stream) {
-  int rc = check_batch(batch, views, s);
-  if (rc || (rc = check_cyl(grid))) return rc;
-  if (!mu || !p_meas) return set_err(CT_ERR_ARG, "null pointer");
-  CylGeo geo;
-  geo.init(mu, gather, *grid);
-  return fp_slots<CylGeo, EPI_RESID>(geo, views, batch, s, p_meas, nullptr, nullptr, n_slots,
-                                     scratch, stream);
-}
-
-int ct_fp_cart_residual_slots(const float* mu, const float* gather, const ct_cart_grid* grid,
+int ct_fp_cyl_correction_rows(const float* mu, const float* gather, const ct_cyl_grid* grid,
                               const ct_ray_view* views, const ct_batch* batch,
-                              const ct_sampling* s, const float* p_meas, int n_slots,
+                              const ct_sampling* s, const float* p_meas, const double* row_thr,
+                              float* corr, int64_t row_lo, int64_t row_hi, int n_slots,
                               double* scratch, ct_stream_t stream) {
   int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cyl(grid))) return rc;
+  if (!mu || !p_meas || !row_thr || !corr) return set_err(CT_ERR_ARG, "null pointer");
+  CylGeo geo;
+  geo.init(mu, gather, *grid);
+  return fp_rows(geo, views, batch, s, p_meas, row_thr, corr, row_lo, row_hi, n_slots, scratch,
+                 stream);
+}
+
+int ct_fp_cart_correction_rows(const float* mu, const float* gather, const ct_cart_grid* grid,
+                               const ct_ray_view* views, const ct_batch* batch,
+                               const ct_sampling* s, const float* p_meas, const double* row_thr,
+                               float* corr, int64_t row_lo, int64_t row_hi, int n_slots,
+                               double* scratch, ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
   if (rc || (rc = check_cart(grid))) return rc;
-  if (!mu || !p_meas) return set_err(CT_ERR_ARG, "null pointer");
+  if (!mu || !p_meas || !row_thr || !corr) return set_err(CT_ERR_ARG, "null pointer");
   CartGeo geo;
   geo.init(mu, gather, *grid);
-  return fp_slots<CartGeo, EPI_RESID>(geo, views, batch, s, p_meas, nullptr, nullptr, n_slots,
-                                      scratch, stream);
+  return fp_rows(geo, views, batch, s, p_meas, row_thr, corr, row_lo, row_hi, n_slots, scratch,
+                 stream);
+}
+
+int ct_fp_cyl_residual_rows(const float* mu, const float* gather, const ct_cyl_grid* grid,
+                            const ct_ray_view* views, const ct_batch* batch,
+                            const ct_sampling* s, const float* p_meas, int64_t row_lo,
+                            int64_t row_hi, int n_slots, double* scratch, ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cyl(grid))) return rc;
+  if (!mu || !p_meas || !scratch) return set_err(CT_ERR_ARG, "null pointer");
+  CylGeo geo;
+  geo.init(mu, gather, *grid);
+  return fp_rows(geo, views, batch, s, p_meas, nullptr, nullptr, row_lo, row_hi, n_slots,
+                 scratch, stream);
+}
+
+int ct_fp_cart_residual_rows(const float* mu, const float* gather, const ct_cart_grid* grid,
+                             const ct_ray_view* views, const ct_batch* batch,
+                             const ct_sampling* s, const float* p_meas, int64_t row_lo,
+                             int64_t row_hi, int n_slots, double* scratch, ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cart(grid))) return rc;
+  if (!mu || !p_meas || !scratch) return set_err(CT_ERR_ARG, "null pointer");
+  CartGeo geo;
+  geo.init(mu, gather, *grid);
+  return fp_rows(geo, views, batch, s, p_meas, nullptr, nullptr, row_lo, row_hi, n_slots,
+                 scratch, stream);
 }
 
 int ct_residual_sum(const double* scratch, int64_t n, double* accum, ct_stream_t stream) {

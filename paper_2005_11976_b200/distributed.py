@@ -1,27 +1,35 @@
-"""Multi-GPU OS-SART: views of every subset sharded across ranks, and object batches.
+"""Multi-GPU OS-SART: every subset's rays and voxels sharded across ranks, and object batches.
 
 One process per GPU (``torch.distributed``, NCCL over NVLink/NVSwitch).  The
 reference is single-process; the sharding follows the
-north_star and SURVEY.md §8e:
+north_star and SURVEY.md §8e, with the exchange chosen to move the fewest
+bytes:
 
-* **angle sharding** -- within OS-SART subset s, rank r projects and
-  back-projects the views subset[r::G] on the same mu (views of a subset are
-  independent given mu) and writes its partial num; the one real exchange
-  step runs: reduce-scatter(num) -> the fused update on the rank's voxel
-  shard -> all-gather(mu).  den is mu-independent -- the BP weights of the
-  in-bounds taps are pure geometry (cyltomo/_kernels.py:365-376) -- so each
-  subset's den shard is computed and reduce-scattered ONCE at setup
-   and only num moves per subset.  Every rank ends the subset
-  with the same mu (the gather broadcasts one owner's values).  The residual
-  is an all-reduce of one fp64 per pass.
+* **angle sharding** -- within OS-SART subset s (n views of H x W pixels)
+  the subset's rays are split by flattened detector row f = b*H + row into G
+  contiguous ranges, balanced to one FP block tile (ct_fp_row_tile), so each
+  rank marches ~1/G of the subset's rays on the same mu.  The corrections are
+  all-gathered (n*H*W floats: 45 MiB at C2, against 128 MiB for a
+  reduce-scatter of num), then every rank back-projects ALL the subset's
+  views onto its own 1/G voxel shard with the fused SART update
+  (ct_bp_*_update_range: num and den never leave the kernel, nothing to
+  reduce), and mu is all-gathered.  Every correction and every voxel update
+  is computed by exactly one rank with the single-GPU arithmetic, so mu is
+  bit-identical to the 1-GPU run for any G.
+* **residual** -- deferred like recon.SartRun: pass k marches the other
+  subsets' views (row-split across ranks) and pass k+1's first correction FP
+  adds the first subset's partials; the partials sit at fixed (view, block)
+  slots and each slot is written by one rank (row ranges are tile-aligned),
+  so an all-reduce of the slot scratch (x + 0 + ... = x) and one fixed-order
+  sum give the single-GPU residual bit for bit.
 * **object sharding** -- independent objects (config C5 batches) are
   assigned round-robin, no collective on the data path
   (:func:`reconstruct_batch`).
 
-The compute engine is injectable so the host logic (partitioning, collective
-sequence, update offsets) is testable on CPU with the gloo backend and the
-oracle (tests/test_distributed.py); the production engine is
-:class:`GpuEngine` over the sm_100a kernels.
+The compute engine is injectable so the host logic (row / voxel
+partitioning, collective sequence, residual slots) is testable on CPU with
+the gloo backend and the oracle (tests/test_distributed.py); the production
+engine is :class:`GpuEngine` over the sm_100a kernels.
 """
 
 from __future__ import annotations
@@ -61,11 +69,6 @@ def init_from_env(backend: str | None = None):
     return rank, world, local
 
 
-def shard_views(subset, rank: int, world: int):
-    """Views of one subset owned by `rank` (round-robin: subset[rank::world])."""
-    return np.asarray(subset)[rank::world]
-
-
 def shard_range(n: int, rank: int, world: int):
     """Voxel range [offset, offset+count) updated by `rank` (chunk = ceil(n/world))."""
     chunk = -(-n // world)
@@ -73,16 +76,26 @@ def shard_range(n: int, rank: int, world: int):
     return off, max(0, min(chunk, n - off)), chunk
 
 
-def _reduce_scatter(full, out_chunk, group=None):
-    """Sum `full` ([world*chunk]) over ranks, keep this rank's chunk."""
-    dist = _dist()
-    if dist.get_backend(group) == "nccl":
-        dist.reduce_scatter_tensor(out_chunk, full, group=group)
-    else:  # gloo: no reduce-scatter -- all-reduce then slice (same result)
-        dist.all_reduce(full, group=group)
-        r = dist.get_rank(group)
-        c = out_chunk.numel()
-        out_chunk.copy_(full[r * c:(r + 1) * c])
+def row_bounds(n_views: int, rows: int, world: int, tile: int) -> np.ndarray:
+    """Split the flattened rows [0, n_views*rows) of a view batch into `world`
+    contiguous ranges at FP block-tile boundaries (v*rows + z*tile, and view
+    ends), each boundary the tile boundary nearest to r*N/world.  Returns
+    world+1 non-decreasing bounds; rank r owns [b[r], b[r+1])."""
+    n_tiles = -(-rows // tile)
+    starts = (np.arange(n_views)[:, None] * rows
+              + np.minimum(np.arange(n_tiles)[None, :] * tile, rows)).ravel()
+    cand = np.append(starts, n_views * rows)
+    total = n_views * rows
+    b = [0]
+    for r in range(1, world):
+        t = r * total / world
+        i = int(np.searchsorted(cand, t))
+        lo = cand[max(i - 1, 0)]
+        hi = cand[min(i, len(cand) - 1)]
+        pick = lo if (t - lo) <= (hi - t) else hi
+        b.append(max(int(pick), b[-1]))
+    b.append(total)
+    return np.asarray(b, dtype=np.int64)
 
 
 def _all_gather(full, my_chunk, group=None):
@@ -96,7 +109,7 @@ def _all_gather(full, my_chunk, group=None):
 
 
 class GpuEngine:
-    """Angle-sharded OS-SART compute on one GPU (wraps recon.SartEngine)."""
+    """Sharded OS-SART compute on one GPU (over recon.SartEngine's launchers)."""
 
     def __init__(self, ps: ProjectionSet, grid, cfg: SartConfig):
         from . import _device as D
@@ -107,8 +120,9 @@ class GpuEngine:
         self.p_meas = D.to_device(ps.images, device=self.device)
         self.weights = _device_weights(cfg, grid.shape, self.device)
         self.cfg = cfg
-        self.gather = None
+        self.gather = self.eng.alloc_gather()
         self.quads = None
+        self._upd = None
 
     def tensor(self, shape, dtype="float32"):
         torch = self.D.torch_mod()
@@ -120,37 +134,61 @@ class GpuEngine:
     def slots(self, views):
         return self.D.upload_i32(views)
 
-    def correction(self, mu, slots, n, corr):
-        if self.gather is None:
-            self.gather = self.eng.alloc_gather()
-        self.eng.pack(mu, self.gather)
-        self.eng.correction(mu, self.p_meas, slots, n, corr, self.gather)
+    def row_tile(self) -> int:
+        return self.eng.row_tile()
 
-    def bp_partial(self, corr, slots, n, num, den):
-        if self.quads is None:
-            self.quads = self.eng.alloc_quads(corr.shape[0])
+    def scratch(self, n_slots: int):
+        torch = self.D.torch_mod()
+        s = self.eng.residual_scratch(n_slots)
+        return torch.zeros_like(s)
+
+    def pack(self, mu) -> None:
+        self.eng.pack(mu, self.gather)
+
+    def correction_rows(self, mu, slots, n, out, lo, hi, n_slots, scratch):
+        self.eng.correction_rows(mu, self.p_meas, slots, n, out, lo, hi, n_slots, scratch,
+                                 self.gather)
+
+    def residual_rows(self, mu, slots, n, lo, hi, n_slots, scratch):
+        self.eng.residual_rows(mu, self.p_meas, slots, n, n_slots, scratch, lo, hi, self.gather)
+
+    def residual_sum(self, scratch, acc):
+        self.eng.residual_sum(scratch, acc)
+
+    def bp_update_range(self, corr, slots, n, offset, count, mu):
+        if self.quads is None or self.quads.numel() < 4 * corr[:n].numel():
+            self.quads = self.eng.alloc_quads(n)
+        if self._upd is None:
+            self._upd = make_update(mu, self.weights, self.cfg)
         self.eng.pack_quads(corr, n, self.quads)
-        self.eng.bp_partial(corr, slots, n, num, den, self.quads)
-
-    def update(self, num_c, den_c, offset, count, mu):
-        from . import _native as N
-        import ctypes as C
-        upd = make_update(mu, self.weights, self.cfg)
-        N.call("ct_sart_update", self.D.ptr(num_c), self.D.ptr(den_c), offset, count,
-               C.byref(upd), self.D.stream_handle())
-
-    def residual(self, mu, slots, n, accum):
-        if self.gather is None:
-            self.gather = self.eng.alloc_gather()
-        self.eng.pack(mu, self.gather)
-        self.eng.residual(mu, self.p_meas, slots, n, accum, self.gather)
+        self.eng.bp_update_range(corr, slots, n, self._upd, offset, count, self.quads)
 
     def synchronize(self):
         self.D.torch_mod().cuda.synchronize(self.device)
 
 
+class _RowShard:
+    """This rank's flattened-row range of a view batch and the launch it needs."""
+
+    def __init__(self, views, rows, rank, world, tile, engine):
+        self.views = np.asarray(views)
+        self.n = len(self.views)
+        self.bounds = row_bounds(self.n, rows, world, tile)
+        self.lo, self.hi = int(self.bounds[rank]), int(self.bounds[rank + 1])
+        self.sizes = np.diff(self.bounds)
+        self.chunk = int(self.sizes.max()) if self.n else 0
+        self.equal = bool(np.all(self.sizes == self.chunk))
+        if self.hi > self.lo:
+            v0, v1 = self.lo // rows, (self.hi - 1) // rows
+            self.slots = engine.slots(self.views[v0:v1 + 1])     # the views the range spans
+            self.nb = v1 - v0 + 1
+            self.rlo, self.rhi = self.lo - v0 * rows, self.hi - v0 * rows
+        else:
+            self.slots, self.nb = None, 0
+
+
 class ShardedSartRun:
-    """OS-SART with every subset's views sharded over the ranks of `group`."""
+    """OS-SART with every subset's rays and voxels sharded over the ranks of `group`."""
 
     def __init__(self, ps: ProjectionSet, grid, cfg: SartConfig, group=None, engine=None):
         if ps.kind != LINE_INTEGRAL:
@@ -174,37 +212,34 @@ class ShardedSartRun:
         self.order = projection_order(cfg, ps.geom.n_proj)
         self.subsets = make_subsets(self.order, cfg.n_subsets)
         self.e.prepare(self.order)
-        self.local = [shard_views(s, self.rank, self.world) for s in self.subsets]
-        self.local_slots = [self.e.slots(v) if len(v) else None for v in self.local]
-        my_views = np.arange(ps.geom.n_proj)[self.rank::self.world]
-        self.resid_views = my_views
-        self.resid_slots = self.e.slots(my_views) if len(my_views) else None
-        nmax = max(1, max(len(v) for v in self.local))
-        self.corr = self.e.tensor((nmax, ps.geom.det_rows, ps.geom.det_cols))
-        self.num = self.e.tensor(pad)
-        self.num_c = self.e.tensor(self.chunk)
-        self.den_c = self._subset_den(pad)
+        rows, cols = ps.geom.det_rows, ps.geom.det_cols
+        self.rows, self.cols = rows, cols
+        tile = self.e.row_tile()
+        self.shards = [_RowShard(s, rows, self.rank, self.world, tile, self.e)
+                       for s in self.subsets]
+        self.subset_slots = [self.e.slots(s) for s in self.subsets]
+        nmax = max(len(s) for s in self.subsets)
+        cmax = max(sh.chunk for sh in self.shards)
+        self.corr_all = self.e.tensor(self.world * cmax * cols)      # gather target
+        self.corr = self.e.tensor((nmax, rows, cols))                 # compacted stack
+        n_proj = ps.geom.n_proj
+        rest = np.setdiff1d(np.arange(n_proj), self.subsets[0])
+        self.rest = _RowShard(rest, rows, self.rank, self.world, tile, self.e) \
+            if len(rest) else None
+        self.scratch = self.e.scratch(n_proj)       # this rank's residual slot partials
+        self.red = self.e.scratch(n_proj)           # their all-reduced copy
         self.resid = self.e.tensor(cfg.n_iterations, "float64")
+        self.acc = self.e.tensor(1, "float64")
         self.passes_done = 0
+        self._pending = None
+        self._packed = False
         self.launch_log = None
 
-    def _subset_den(self, pad):
-        """Per-subset den shards [n_subsets][chunk]: one partial BP (den only;
-        the correction values do not enter den) and one reduce-scatter per
-        subset, at setup."""
-        den = self.e.tensor(pad)
-        dv = den[:self.nvox].view(self.grid.shape)
-        nv = self.num[:self.nvox].view(self.grid.shape)
-        out = []
-        for views, slots in zip(self.local, self.local_slots):
-            if len(views):
-                self.e.bp_partial(self.corr, slots, len(views), nv, dv)
-            else:
-                den.zero_()
-            chunk = self.e.tensor(self.chunk)
-            _reduce_scatter(den, chunk, self.group)
-            out.append(chunk)
-        return out
+    # views of subset s this rank marches (tests / accounting)
+    @property
+    def local(self):
+        return [sh.views[sh.lo // self.rows:(sh.hi - 1) // self.rows + 1] if sh.hi > sh.lo
+                else sh.views[:0] for sh in self.shards]
 
     def _timed(self, kind, s, fn, *args):
         """Run fn; with launch_log set (GPU engine), bracket it with CUDA events."""
@@ -219,41 +254,90 @@ class ShardedSartRun:
         b.record()
         self.launch_log.append((kind, s, a, b))
 
+    def _pack(self, s):
+        if not self._packed:
+            self._timed("pack_gather", s, self.e.pack, self.mu)
+        self._packed = True
+
+    def _finish_residual(self):
+        """All-reduce the slot partials (one owner per slot) and sum them."""
+        self.red.copy_(self.scratch)
+        self._timed("all_reduce_resid", -1, _dist().all_reduce, self.red, _dist().ReduceOp.SUM,
+                    self.group)
+        self.acc.zero_()
+        self.e.residual_sum(self.red, self.acc)
+        k = min(self._pending, self.resid.numel() - 1)
+        self.resid[k:k + 1].copy_(self.acc)
+        self._pending = None
+
     def run_subset(self, s: int) -> None:
-        views, slots = self.local[s], self.local_slots[s]
-        nv = self.num[:self.nvox].view(self.grid.shape)
-        if len(views):
-            self._timed("fp_correction", s, self.e.correction, self.mu, slots, len(views),
-                        self.corr)
-            self._timed("bp_partial", s, self.e.bp_partial, self.corr, slots, len(views), nv,
-                        None)
-        else:
-            self.num.zero_()
-        self._timed("reduce_scatter", s, _reduce_scatter, self.num, self.num_c, self.group)
+        sh = self.shards[s]
+        cols = self.cols
+        n_proj = self.ps.geom.n_proj
+        self._pack(s)
+        mine = self.corr_all[self.rank * sh.chunk * cols:(self.rank + 1) * sh.chunk * cols]
+        fused = s == 0 and self._pending is not None
+        if sh.nb:
+            if fused:
+                self._timed("fp_correction_resid", s, self.e.correction_rows, self.mu,
+                            sh.slots, sh.nb, mine, sh.rlo, sh.rhi, n_proj, self.scratch)
+            else:
+                self._timed("fp_correction", s, self.e.correction_rows, self.mu, sh.slots,
+                            sh.nb, mine, sh.rlo, sh.rhi, 0, None)
+        if fused:
+            self._finish_residual()
+        full = self.corr_all[:self.world * sh.chunk * cols]
+        self._timed("all_gather_corr", s, _all_gather, full, mine, self.group)
+        npix_rows = sh.n * self.rows
+        if sh.equal and self.world * sh.chunk == npix_rows:
+            stack = full.view(-1)[:npix_rows * cols].view(sh.n, self.rows, cols)
+        else:                     # uneven chunks: compact into the [n][H][W] stack
+            flat = self.corr.view(-1)
+            for r in range(self.world):
+                a, b = int(sh.bounds[r]), int(sh.bounds[r + 1])
+                if b > a:
+                    flat[a * cols:b * cols].copy_(full[r * sh.chunk * cols:
+                                                       (r * sh.chunk + b - a) * cols])
+            stack = self.corr[:sh.n]
         if self.count:
-            self._timed("update", s, self.e.update, self.num_c, self.den_c[s], self.offset,
-                        self.count, self.mu)
+            self._timed("bp_update", s, self.e.bp_update_range, stack, self.subset_slots[s],
+                        sh.n, self.offset, self.count, self.mu)
         self._timed("all_gather", s, _all_gather, self.mu_flat,
                     self.mu_flat[self.rank * self.chunk:(self.rank + 1) * self.chunk],
                     self.group)
+        self._packed = False
 
     def run_pass(self, residual: bool | None = None) -> None:
+        want = self.cfg.compute_residuals if residual is None else residual
+        if not want:
+            self.finalize()
         for s in range(len(self.subsets)):
             self.run_subset(s)
-        want = self.cfg.compute_residuals if residual is None else residual
         if want:
-            k = min(self.passes_done, self.cfg.n_iterations - 1)
-            acc = self.resid[k:k + 1]
-            if self.resid_slots is not None:
-                self._timed("fp_residual", -1, self.e.residual, self.mu, self.resid_slots,
-                            len(self.resid_views), acc)
-            _dist().all_reduce(acc, group=self.group)
+            if self.rest is not None and self.rest.nb:
+                self._pack(-1)
+                self._timed("fp_residual", -1, self.e.residual_rows, self.mu, self.rest.slots,
+                            self.rest.nb, self.rest.rlo, self.rest.rhi, self.ps.geom.n_proj,
+                            self.scratch)
+            self._pending = self.passes_done
         self.passes_done += 1
+
+    def finalize(self) -> None:
+        """Complete a deferred residual: the first subset's rows on the current mu."""
+        if self._pending is None:
+            return
+        sh = self.shards[0]
+        if sh.nb:
+            self._pack(-2)
+            self._timed("fp_residual", -2, self.e.residual_rows, self.mu, sh.slots, sh.nb,
+                        sh.rlo, sh.rhi, self.ps.geom.n_proj, self.scratch)
+        self._finish_residual()
 
     def run(self):
         t0 = time.perf_counter()
         for _ in range(self.cfg.n_iterations):
             self.run_pass()
+        self.finalize()
         if hasattr(self.e, "synchronize"):
             self.e.synchronize()
         wall = time.perf_counter() - t0

@@ -254,24 +254,49 @@ class SartEngine:
             self._scratch[n] = torch.empty(length, dtype=torch.float64, device=self.device)
         return self._scratch[n]
 
-    def correction_resid(self, mu, p_meas, slots, n: int, corr, n_slots: int, scratch,
-                         gather=None) -> None:
-        """correction() plus the residual partials of the same simulation at
-        the views' slots of an n_slots-view residual scratch."""
+    def row_tile(self) -> int:
+        """Detector rows per FP block: row ranges aligned to it keep every
+        residual partial on one launch (exact split sums)."""
+        b = D.batch_c(1, self.rows, self.cols)
+        return int(N.load_library().ct_fp_row_tile(C.byref(b)))
+
+    def correction_rows(self, mu, p_meas, slots, n: int, corr, row_lo: int = 0,
+                        row_hi: int | None = None, n_slots: int = 0, scratch=None,
+                        gather=None) -> None:
+        """Correction FP over flattened rows [row_lo, row_hi) of an n-view batch
+        (corr holds rows from row_lo); with a scratch also the residual
+        partials of the same simulation at the views' slots of an
+        n_slots-view residual scratch."""
         b = D.batch_c(n, self.rows, self.cols, slots)
-        fn = "ct_fp_cyl_correction_resid" if self.cyl else "ct_fp_cart_correction_resid"
+        hi = n * self.rows if row_hi is None else row_hi
+        fn = "ct_fp_cyl_correction_rows" if self.cyl else "ct_fp_cart_correction_rows"
         N.call(fn, D.ptr(mu), D.ptr(gather), C.byref(self.gc), D.ptr(self.fp_views),
                C.byref(b), C.byref(self.samp), D.ptr(p_meas), D.ptr(self.row_thr), D.ptr(corr),
+               int(row_lo), int(hi), int(n_slots), D.ptr(scratch), D.stream_handle())
+
+    def residual_rows(self, mu, p_meas, slots, n: int, n_slots: int, scratch, row_lo: int = 0,
+                      row_hi: int | None = None, gather=None) -> None:
+        """Residual partials of flattened rows [row_lo, row_hi) of an n-view
+        batch at the views' slots (no sum)."""
+        b = D.batch_c(n, self.rows, self.cols, slots)
+        hi = n * self.rows if row_hi is None else row_hi
+        fn = "ct_fp_cyl_residual_rows" if self.cyl else "ct_fp_cart_residual_rows"
+        N.call(fn, D.ptr(mu), D.ptr(gather), C.byref(self.gc), D.ptr(self.fp_views),
+               C.byref(b), C.byref(self.samp), D.ptr(p_meas), int(row_lo), int(hi),
                int(n_slots), D.ptr(scratch), D.stream_handle())
 
-    def residual_slots(self, mu, p_meas, slots, n: int, n_slots: int, scratch,
-                       gather=None) -> None:
-        """Residual partials of a view set at its slots (no sum)."""
+    def bp_update_range(self, corr, slots, n: int, upd: N.UpdateC, offset: int, count: int,
+                        quads=None) -> None:
+        """bp_update restricted to voxels [offset, offset+count)."""
         b = D.batch_c(n, self.rows, self.cols, slots)
-        fn = "ct_fp_cyl_residual_slots" if self.cyl else "ct_fp_cart_residual_slots"
-        N.call(fn, D.ptr(mu), D.ptr(gather), C.byref(self.gc), D.ptr(self.fp_views),
-               C.byref(b), C.byref(self.samp), D.ptr(p_meas), int(n_slots), D.ptr(scratch),
-               D.stream_handle())
+        if self.cyl:
+            N.call("ct_bp_cyl_update_range", D.ptr(corr), D.ptr(quads), D.ptr(self.bp_dets),
+                   C.byref(b), C.byref(self.gc), D.ptr(self.trig), C.byref(upd), int(offset),
+                   int(count), D.stream_handle())
+        else:
+            N.call("ct_bp_cart_update_range", D.ptr(corr), D.ptr(quads), D.ptr(self.bp_dets),
+                   C.byref(b), C.byref(self.gc), C.byref(upd), int(offset), int(count),
+                   D.stream_handle())
 
     def residual_sum(self, scratch, accum) -> None:
         """accum += fixed-order sum of a residual scratch."""
@@ -528,8 +553,8 @@ class SartRun:
             if k == 0 and self._pending is not None:
                 # completes the previous pass's residual (same mu)
                 scratch = e.residual_scratch(n_proj)
-                self._timed("fp_correction_resid", k, e.correction_resid, self.mu,
-                            self._p_meas, slots, len(s), self.corr, n_proj, scratch,
+                self._timed("fp_correction_resid", k, e.correction_rows, self.mu,
+                            self._p_meas, slots, len(s), self.corr, 0, None, n_proj, scratch,
                             self.gather)
                 self.resid_cur.zero_()
                 e.residual_sum(scratch, self.resid_cur)
@@ -547,9 +572,9 @@ class SartRun:
         if residual and fuse:
             self._pack(-1)
             if self.n_rest:
-                self._timed("fp_residual", -1, e.residual_slots, self.mu, self._p_meas,
+                self._timed("fp_residual", -1, e.residual_rows, self.mu, self._p_meas,
                             self.rest_slots, self.n_rest, n_proj,
-                            e.residual_scratch(n_proj), self.gather)
+                            e.residual_scratch(n_proj), 0, None, self.gather)
             self._pending = self.passes_done
         elif residual:
             self.resid_cur.zero_()
@@ -566,8 +591,9 @@ class SartRun:
         n_proj = self.ps.geom.n_proj
         scratch = e.residual_scratch(n_proj)
         self._pack(-1)
-        self._timed("fp_residual", -2, e.residual_slots, self.mu, self._p_meas,
-                    self.subset_slots[0], len(self.subsets[0]), n_proj, scratch, self.gather)
+        self._timed("fp_residual", -2, e.residual_rows, self.mu, self._p_meas,
+                    self.subset_slots[0], len(self.subsets[0]), n_proj, scratch, 0, None,
+                    self.gather)
         self.resid_cur.zero_()
         e.residual_sum(scratch, self.resid_cur)
         self._store_residual(self._pending)

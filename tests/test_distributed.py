@@ -26,14 +26,21 @@ def _free_port():
 
 
 class OracleEngine:
-    """CPU engine with GpuEngine's interface, computing with the fp64 oracle."""
+    """CPU engine with GpuEngine's interface, computing with the fp64 oracle.
+
+    Residual scratch layout: one partial per (view slot, detector row)."""
+
+    TILE = 4
 
     def __init__(self, orc, ps, grid, cfg):
         import torch
         self.torch, self.o = torch, orc
         self.ps, self.grid, self.cfg = ps, grid, cfg
+        self.H, self.W = ps.geom.det_rows, ps.geom.det_cols
         self.images = np.asarray(ps.images, dtype=np.float64)
         self.max_row = None
+        self.marched = []            # (view, row) pairs this rank marched (FP)
+        self.updated = []            # voxel ranges this rank updated
 
     def tensor(self, shape, dtype="float32"):
         return self.torch.zeros(shape, dtype=self.torch.float64)
@@ -48,35 +55,56 @@ class OracleEngine:
     def slots(self, views):
         return np.asarray(views)
 
-    def correction(self, mu, slots, n, corr):
-        for b, i in enumerate(slots[:n]):
-            c = self.o.correction(mu.numpy(), self.grid, self.ps.geom, int(i), self.images[i],
-                                  max_row=self.max_row[int(i)])
-            corr[b] = self.torch.from_numpy(c)
+    def row_tile(self):
+        return self.TILE
 
-    def bp_partial(self, corr, slots, n, num, den):
-        num.zero_()
-        if den is None:               # num-only partial (den precomputed per subset)
-            den = self.torch.zeros_like(num)
-        den.zero_()
-        out = (num.numpy(), den.numpy())
-        for b, i in enumerate(slots[:n]):
-            self.o.back(corr[b].numpy(), self.ps.geom, int(i), self.grid, out=out)
+    def scratch(self, n_slots):
+        return self.torch.zeros(n_slots * self.H, dtype=self.torch.float64)
 
-    def update(self, num_c, den_c, offset, count, mu):
+    def pack(self, mu):
+        pass
+
+    def _rows(self, slots, n, lo, hi):
+        for f in range(lo, hi):
+            yield f, int(slots[f // self.H]), f % self.H
+
+    def correction_rows(self, mu, slots, n, out, lo, hi, n_slots, scratch):
+        cache = {}
+        for f, v, r in self._rows(slots, n, lo, hi):
+            if v not in cache:
+                c = self.o.correction(mu.numpy(), self.grid, self.ps.geom, v, self.images[v],
+                                      max_row=self.max_row[v])
+                sim, _ = self.o.forward(mu.numpy(), self.grid, self.ps.geom, v)
+                cache[v] = (c, sim)
+            c, sim = cache[v]
+            out[(f - lo) * self.W:(f - lo + 1) * self.W] = self.torch.from_numpy(c[r])
+            if scratch is not None:
+                scratch[v * self.H + r] = float(np.sum((self.images[v][r] - sim[r]) ** 2))
+            self.marched.append((v, r))
+
+    def residual_rows(self, mu, slots, n, lo, hi, n_slots, scratch):
+        cache = {}
+        for f, v, r in self._rows(slots, n, lo, hi):
+            if v not in cache:
+                cache[v], _ = self.o.forward(mu.numpy(), self.grid, self.ps.geom, v)
+            scratch[v * self.H + r] = float(np.sum((self.images[v][r] - cache[v][r]) ** 2))
+
+    def residual_sum(self, scratch, acc):
+        acc += float(np.sum(scratch.numpy()))
+
+    def bp_update_range(self, corr, slots, n, offset, count, mu):
+        shape = self.o.grid_shape(self.grid)
+        num, den = np.zeros(shape), np.zeros(shape)
+        for b, i in enumerate(slots[:n]):
+            self.o.back(corr[b].numpy(), self.ps.geom, int(i), self.grid, out=(num, den))
         w = None
         if self.cfg.weights is not None:
             w = np.asarray(self.cfg.weights, dtype=np.float64).ravel()[offset:offset + count]
         self.o._apply_update(mu.view(-1)[offset:offset + count].numpy(),
-                             num_c[:count].numpy(), den_c[:count].numpy(), w,
+                             num.ravel()[offset:offset + count],
+                             den.ravel()[offset:offset + count], w,
                              self.cfg.relaxation, self.cfg.nonnegativity)
-
-    def residual(self, mu, slots, n, accum):
-        tot = 0.0
-        for i in slots[:n]:
-            sim, _ = self.o.forward(mu.numpy(), self.grid, self.ps.geom, int(i))
-            tot += float(np.sum((self.images[int(i)] - sim) ** 2))
-        accum += tot
+        self.updated.append((offset, count))
 
 
 def _problem():
@@ -104,16 +132,19 @@ def _worker(rank, world, port, outdir):
     ps = P.ProjectionSet(geom, images)
     cfg = P.SartConfig(relaxation=0.4, n_iterations=2, n_subsets=3, weights=weights,
                        projection_order="fixed_permutation", order_seed=1)
-    run = PD.ShardedSartRun(ps, grid, cfg, engine=OracleEngine(orc, ps, grid, cfg))
+    eng = OracleEngine(orc, ps, grid, cfg)
+    run = PD.ShardedSartRun(ps, grid, cfg, engine=eng)
     vol, rep = run.run()
+    n_sub = len(run.subsets)
     np.savez(Path(outdir) / f"rank{rank}.npz", mu=run.mu.numpy(), res=rep.residuals,
-             views=np.concatenate([v for v in run.local]) if run.local else np.zeros(0))
+             marched=np.array(eng.marched), updated=np.array(eng.updated), n_sub=n_sub)
     dist.destroy_process_group()
 
 
-def test_angle_sharded_os_sart_matches_single_process(oracle, tmp_path):
+@pytest.mark.parametrize("world", [2, 3])
+def test_angle_sharded_os_sart_matches_single_process(oracle, tmp_path, world):
+    """world 3 gives uneven row chunks (the compaction path)."""
     import torch.multiprocessing as mp
-    world = 2
     mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
                        start_method="spawn", join=True)
     P, geom, grid, truth, weights = _problem()
@@ -122,21 +153,36 @@ def test_angle_sharded_os_sart_matches_single_process(oracle, tmp_path):
     order = np.random.default_rng(1).permutation(geom.n_proj)
     mu_ref, res_ref = oracle.sart(images, grid, geom, relaxation=0.4, n_iterations=2,
                                   order=order, weights=weights, n_subsets=3)
-    r0 = np.load(tmp_path / "rank0.npz")
-    r1 = np.load(tmp_path / "rank1.npz")
-    assert np.array_equal(r0["mu"], r1["mu"])            # replicas stay identical
+    rs = [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
+    r0 = rs[0]
+    for r in rs[1:]:
+        assert np.array_equal(r0["mu"], r["mu"])          # replicas stay identical
     assert np.abs(r0["mu"] - mu_ref).max() <= 1e-12 * np.abs(mu_ref).max()
     assert np.allclose(r0["res"], res_ref, rtol=1e-12)
-    # every view processed exactly once per pass across the ranks
-    views = np.sort(np.concatenate([r0["views"], r1["views"]]))
-    assert np.array_equal(views, np.arange(geom.n_proj))
+    # every detector row of every view corrected exactly once per pass across
+    # the ranks (2 passes), every voxel updated once per subset
+    rows = np.concatenate([r["marched"] for r in rs])
+    keys = rows[:, 0] * geom.det_rows + rows[:, 1]
+    assert np.array_equal(np.bincount(keys, minlength=geom.n_proj * geom.det_rows),
+                          np.full(geom.n_proj * geom.det_rows, 2))
+    n_vox = int(np.prod(grid.shape))
+    upd = np.concatenate([r["updated"] for r in rs])
+    assert upd[:, 1].sum() == n_vox * int(r0["n_sub"]) * 2
 
 
 def test_shard_helpers():
     from paper_2005_11976_b200 import distributed as PD
-    subset = np.array([7, 3, 9, 1, 5])
-    parts = [PD.shard_views(subset, r, 3) for r in range(3)]
-    assert sorted(np.concatenate(parts).tolist()) == sorted(subset.tolist())
+    # row ranges: contiguous, covering, at tile boundaries, balanced to a tile
+    for n_views, rows, world, tile in [(45, 512, 8, 8), (20, 1024, 8, 8), (5, 20, 3, 4),
+                                       (3, 13, 4, 4), (1, 8, 4, 8), (7, 40, 2, 8)]:
+        b = PD.row_bounds(n_views, rows, world, tile)
+        assert len(b) == world + 1 and b[0] == 0 and b[-1] == n_views * rows
+        assert np.all(np.diff(b) >= 0)
+        inner = b % rows
+        assert np.all((inner % tile == 0) | (b % rows == 0) | (b == n_views * rows))
+        if n_views * rows >= world * tile:
+            assert np.abs(np.diff(b) - n_views * rows / world).max() <= tile
+    assert np.array_equal(PD.row_bounds(45, 512, 8, 8), np.arange(9) * 2880)
     n = 1001
     ranges = [PD.shard_range(n, r, 4) for r in range(4)]
     covered = sum(c for _, c, _ in ranges)
