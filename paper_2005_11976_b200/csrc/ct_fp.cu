@@ -32,6 +32,15 @@ enum FpLayout { GL_PLAIN = 0, GL_OCT = 1, GL_QUAD = 2 };
 #ifndef CT_FP_MAXREG
 #define CT_FP_MAXREG 64          // 32 warps/SM
 #endif
+// GL_OCT volumes whose 32-byte-cell layers fit well inside L2 (<= 6 MB: C1-C3)
+// run a 56-register variant (36 warps/SM; A/B C2 -1.1 %); larger ones (C4-cart)
+// lose 3 % with it, the GL_QUAD path 11 % (C5)
+#ifndef CT_FP_MAXREG_SMALL
+#define CT_FP_MAXREG_SMALL 56
+#endif
+#ifndef CT_FP_SMALL_LAYER_BYTES
+#define CT_FP_SMALL_LAYER_BYTES 6.0e6
+#endif
 #ifndef CT_FP_WW1
 #define CT_FP_WW1 4              // warp patch width at one lane per ray
 #endif
@@ -251,7 +260,21 @@ __device__ __forceinline__ int march(const Geo& geo, const ct_ray_view& v, doubl
 
 
 template <class Geo, int EPI, bool NEAREST, int OCT>
+__device__ __forceinline__ void fp_body(const FpArgs<Geo>& a);
+
+template <class Geo, int EPI, bool NEAREST, int OCT>
 __global__ void __maxnreg__(CT_FP_MAXREG) fp_kernel(const FpArgs<Geo> a) {
+  fp_body<Geo, EPI, NEAREST, OCT>(a);
+}
+
+// the same kernel under the small-volume register cap (see CT_FP_MAXREG_SMALL)
+template <class Geo, int EPI, bool NEAREST, int OCT>
+__global__ void __maxnreg__(CT_FP_MAXREG_SMALL) fp_kernel_small(const FpArgs<Geo> a) {
+  fp_body<Geo, EPI, NEAREST, OCT>(a);
+}
+
+template <class Geo, int EPI, bool NEAREST, int OCT>
+__device__ __forceinline__ void fp_body(const FpArgs<Geo>& a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int K = a.lanes;
   const int ww = tile_ww(K), wh = tile_wh(K);
@@ -417,7 +440,12 @@ int launch_fp(const Geo& geo, const ct_ray_view* views, const ct_batch& b, const
   else if (EPI != EPI_ROWMAX && geo.oct && geo.quad)
     fp_kernel<Geo, EPI, false, GL_QUAD><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
   else if (EPI != EPI_ROWMAX && geo.oct)
-    fp_kernel<Geo, EPI, false, GL_OCT><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
+  {
+    if (32.0 * geo.cell_kstride <= CT_FP_SMALL_LAYER_BYTES)
+      fp_kernel_small<Geo, EPI, false, GL_OCT><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
+    else
+      fp_kernel<Geo, EPI, false, GL_OCT><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
+  }
   else
     fp_kernel<Geo, EPI, false, GL_PLAIN><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
   return check_launch("fp_kernel");

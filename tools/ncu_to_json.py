@@ -12,7 +12,10 @@ import sys
 from pathlib import Path
 
 KIND = [("fp_kernel<<unnamed>::CylGeo, 1", "fp_correction"),
+        ("fp_kernel_small<<unnamed>::CylGeo, 1", "fp_correction"),
         ("fp_kernel<<unnamed>::CylGeo, 2", "fp_residual"),
+        ("fp_kernel_small<<unnamed>::CylGeo, 2", "fp_residual"),
+        ("fp_kernel_small<<unnamed>::CylGeo, 4", "fp_correction_resid"),
         ("bp_kernel<<unnamed>::CylVox, 2", "bp_update"),
         ("pack_gather_cyl", "pack_gather"),
         ("pack_quads", "pack_quads")]
