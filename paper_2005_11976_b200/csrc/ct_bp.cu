@@ -24,6 +24,18 @@ constexpr int BP_MIN_BLOCKS = CT_BP_MIN_BLOCKS;
 constexpr int BP_CHUNK = 64;   // views staged in shared memory per pass
 static_assert(BP_CHUNK / 2 <= 32, "slow-pair mask is 32 bits");
 constexpr float BP_EDGE_EPS = 1e-3f;  // px band around the frame edge refined in fp64
+// Voxel patch per warp: BP_PR consecutive voxels along a row (r / x) times
+// 32 / BP_PR consecutive rows (theta / y).  A compact patch projects onto
+// fewer detector quads than a 32-voxel line (whose spread along u follows
+// the line's extent across the view direction), so a warp's footprint loads
+// touch fewer L1 sectors; mu I/O stays 32-byte sectors.  CTA = BP_THREADS/32
+// warps side by side along the row.
+#ifndef CT_BP_PR
+#define CT_BP_PR 8
+#endif
+constexpr int BP_PR = CT_BP_PR, BP_PT = 32 / BP_PR;
+constexpr int BP_SEG = BP_PR * (BP_THREADS / 32);   // row voxels per CTA
+static_assert(32 % BP_PR == 0, "BP_PR");
 
 // a pair of views (batch slots 2i, 2i+1), lane-interleaved for f32x2
 struct __align__(16) BpPairF {
@@ -47,6 +59,7 @@ struct CylVox {
     trig = tr;
   }
   __host__ __device__ int64_t count() const { return (int64_t)nh * nt * nr; }
+  __host__ __device__ int row_len() const { return nr; }
   // voxel centre, object -> world (_kernels.py:396-406), reference op order
   __device__ __forceinline__ void world(int m, double w[3]) const {
     const int ir = m % nr;
@@ -72,6 +85,7 @@ struct CartVox {
     for (int i = 0; i < 3; ++i) o[i] = g.origin[i];
   }
   __host__ __device__ int64_t count() const { return (int64_t)nz * ny * nx; }
+  __host__ __device__ int row_len() const { return nx; }
   // _kernels.py:431-437
   __device__ __forceinline__ void world(int m, double w[3]) const {
     const int i = m % nx;
@@ -95,6 +109,7 @@ struct BpArgs {
   float* den;
   ct_update upd;
   int vox_off, vox_end;   // voxels [vox_off, vox_end) (a rank's shard, distributed.py)
+  int row0, nseg;         // first row of the range; CTAs per row group
 };
 
 // fp64 re-evaluation of one voxel-view with the reference's arithmetic
@@ -183,8 +198,12 @@ __device__ __forceinline__ float2 bp_view_slow(const BpArgs<Vox>& a, int m, int 
 template <class Vox, int MODE, bool QUADS>
 __global__ void __launch_bounds__(BP_THREADS, BP_MIN_BLOCKS) bp_kernel(const __grid_constant__ BpArgs<Vox> a) {
   __shared__ BpPairF sv[BP_CHUNK / 2];
-  const int m = a.vox_off + blockIdx.x * BP_THREADS + threadIdx.x;
-  const bool active = m < a.vox_end;
+  const int nr = a.vox.row_len();
+  const int bs = (int)(blockIdx.x % (unsigned)a.nseg), bg = (int)(blockIdx.x / (unsigned)a.nseg);
+  const int i = bs * BP_SEG + (threadIdx.x >> 5) * BP_PR + (threadIdx.x & (BP_PR - 1));
+  const int q = a.row0 + bg * BP_PT + (threadIdx.x & 31) / BP_PR;
+  const int m = q * nr + i;
+  const bool active = i < nr && m >= a.vox_off && m < a.vox_end;
   float xw = 0.0f, yw = 0.0f, zw = 0.0f;
   if (active) {
     double w64[3];
@@ -370,7 +389,12 @@ int launch_bp(const Vox& vox, const float* corr, const float* quads, const ct_de
   a.vox_off = (int)offset;
   a.vox_end = (int)(offset + nvox);
   if (nvox == 0) return CT_OK;
-  const unsigned blocks = (unsigned)((nvox + BP_THREADS - 1) / BP_THREADS);
+  const int nr = vox.row_len();
+  const int64_t row0 = offset / nr, row_end = (offset + nvox + nr - 1) / nr;
+  a.row0 = (int)row0;
+  a.nseg = (nr + BP_SEG - 1) / BP_SEG;
+  const int64_t groups = (row_end - row0 + BP_PT - 1) / BP_PT;
+  const unsigned blocks = (unsigned)(groups * a.nseg);
   if (quads)
     bp_kernel<Vox, MODE, true><<<blocks, BP_THREADS, 0, st>>>(a);
   else
