@@ -280,8 +280,17 @@ __global__ void __launch_bounds__(BP_THREADS, BP_MIN_BLOCKS) bp_kernel(const __g
           float fua, fub, fva, fvb;
           upk(FU, fua, fub);
           upk(FV, fva, fvb);
-          const float aa = fmaf(fua, qa.y - qa.x, qa.x), ba = fmaf(fua, qa.w - qa.z, qa.z);
-          const float ab = fmaf(fub, qb.y - qb.x, qb.x), bb = fmaf(fub, qb.w - qb.z, qb.z);
+          // quad = (t00, t10 | t01, t11): the u-lerps of both rows are one
+          // f32x2 subtract + one FFMA2 (the ops of the scalar lerps, lane for lane)
+          float aa, ba, ab, bb;
+          {
+            const f32x2 P0 = pk(qa.x, qa.y), P1 = pk(qa.z, qa.w);
+            upk(fma2(sub2(P1, P0), dup2(fua), P0), aa, ba);
+          }
+          {
+            const f32x2 P0 = pk(qb.x, qb.y), P1 = pk(qb.z, qb.w);
+            upk(fma2(sub2(P1, P0), dup2(fub), P0), ab, bb);
+          }
           NUM = add2(NUM, pk(fmaf(fva, ba - aa, aa), fmaf(fvb, bb - ab, ab)));
         } else {
           const float* qa = a.corr + oa;
@@ -294,11 +303,13 @@ __global__ void __launch_bounds__(BP_THREADS, BP_MIN_BLOCKS) bp_kernel(const __g
           const f32x2 B = fma2(FU, sub2(T11, T10), T10);
           NUM = add2(NUM, fma2(FV, sub2(B, A), A));
         }
-        nfast += 2;
       } else {
         slow |= 1u << i;   // deferred: keeps the slow path out of the hot loop
       }
     }
+    // interior pairs: den += 1 per view, counted from the slow mask (no
+    // per-pair counter in the hot loop)
+    nfast += 2 * (np - __popc(slow));
     // the chunk's pairs with a frame-edge / refine-band / near-source view:
     // recompute the projection per view (the same fp32 ops as the pair path)
     while (slow) {
@@ -428,9 +439,10 @@ __global__ void trig_kernel(int nt, double* trig) {
   trig[nt + j] = sin(th);
 }
 
-// bilinear footprints of a correction stack: quad (v, u) = (c[v][u], c[v][u+1],
-// c[v+1][u], c[v+1][u+1]) of the same image, 0 past the last row / column
-// (never read: the BP's fast path only takes footprints inside the frame)
+// bilinear footprints of a correction stack: quad (v, u) = (c[v][u], c[v+1][u],
+// c[v][u+1], c[v+1][u+1]) of the same image (column pairs, so the BP's two
+// u-lerps are one f32x2 op), 0 past the last row / column (never read: the
+// BP's fast path only takes footprints inside the frame)
 __global__ void pack_quads_kernel(const float* __restrict__ corr, int64_t n, int rows, int cols,
                                   float4* __restrict__ quads) {
   const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -438,7 +450,7 @@ __global__ void pack_quads_kernel(const float* __restrict__ corr, int64_t n, int
   const int u = (int)(m % cols), v = (int)((m / cols) % rows);
   const bool ru = u + 1 < cols, rv = v + 1 < rows;
   const float* p = corr + m;
-  quads[m] = make_float4(__ldg(p), ru ? __ldg(p + 1) : 0.0f, rv ? __ldg(p + cols) : 0.0f,
+  quads[m] = make_float4(__ldg(p), rv ? __ldg(p + cols) : 0.0f, ru ? __ldg(p + 1) : 0.0f,
                          (ru && rv) ? __ldg(p + cols + 1) : 0.0f);
 }
 
