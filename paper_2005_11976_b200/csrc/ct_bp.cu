@@ -14,7 +14,7 @@ enum BpMode { BP_ACC = 0, BP_WRITE = 1, BP_UPDATE = 2 };
 #endif
 constexpr int BP_THREADS = CT_BP_THREADS;
 #ifndef CT_BP_UNROLL
-#define CT_BP_UNROLL 4
+#define CT_BP_UNROLL 8
 #endif
 constexpr int BP_UNROLL = CT_BP_UNROLL;
 #ifndef CT_BP_MIN_BLOCKS
