@@ -196,6 +196,15 @@ int ct_fp_cart_residual_rows(const float *mu, const float *gather, const ct_cart
                              int64_t row_hi, int n_slots, double *scratch, ct_stream_t stream);
 int ct_residual_sum(const double *scratch, int64_t n, double *accum, ct_stream_t stream);
 
+/* Geometry-only in-support sample count summed per detector row:
+ * row_samples[b * det_rows + row] (uint64, overwritten), the per-row cost
+ * model of the angle-sharded row split (distributed.py; ABI v6). */
+int ct_row_samples_cyl(const ct_cyl_grid *grid, const ct_ray_view *views, const ct_batch *batch,
+                       const ct_sampling *sampling, uint64_t *row_samples, ct_stream_t stream);
+int ct_row_samples_cart(const ct_cart_grid *grid, const ct_ray_view *views,
+                        const ct_batch *batch, const ct_sampling *sampling,
+                        uint64_t *row_samples, ct_stream_t stream);
+
 /* Geometry-only row-sum maximum per view (the max_row of
  * cyltomo/recon.py:96-98), computed without marching: max_row[b] (device,
  * float64, [n_batch]) = max over pixels of out_w.  Exact (sample counts are

@@ -99,6 +99,10 @@ _SIGNATURES = {
                                     C.POINTER(SamplingC), P, P]),
     "ct_rowsum_max_cart": (C.c_int, [C.POINTER(CartGridC), P, C.POINTER(BatchC),
                                      C.POINTER(SamplingC), P, P]),
+    "ct_row_samples_cyl": (C.c_int, [C.POINTER(CylGridC), P, C.POINTER(BatchC),
+                                     C.POINTER(SamplingC), P, P]),
+    "ct_row_samples_cart": (C.c_int, [C.POINTER(CartGridC), P, C.POINTER(BatchC),
+                                      C.POINTER(SamplingC), P, P]),
     "ct_bp_cyl": (C.c_int, [P, P, P, C.POINTER(BatchC), C.POINTER(CylGridC), P, P, P,
                             C.c_int, P]),
     "ct_bp_cart": (C.c_int, [P, P, P, C.POINTER(BatchC), C.POINTER(CartGridC), P, P,

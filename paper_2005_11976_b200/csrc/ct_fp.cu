@@ -10,7 +10,10 @@ namespace {
 // EPI_CORR_RESID: the correction epilogue plus residual partials -- the
 // residual FP of pass k and the first subset's correction FP of pass k+1 read
 // the same mu, so one march serves both (recon.SartRun)
-enum FpEpi { EPI_PROJECT = 0, EPI_CORR = 1, EPI_RESID = 2, EPI_ROWMAX = 3, EPI_CORR_RESID = 4 };
+// EPI_ROWCOUNT: in-support samples summed per detector row (no march; the
+// per-row cost model of the angle-sharded row split, distributed.py)
+enum FpEpi { EPI_PROJECT = 0, EPI_CORR = 1, EPI_RESID = 2, EPI_ROWMAX = 3, EPI_CORR_RESID = 4,
+             EPI_ROWCOUNT = 5 };
 
 // FP volume layouts: plain mu, the 32-byte polynomial cells (ct_pack_gather_*),
 // or 16-byte corner quads per h layer (large volumes; see gather_quad())
@@ -297,7 +300,7 @@ __device__ __forceinline__ void fp_body(const FpArgs<Geo>& a) {
     // one sub-ray at the pixel centre ((0 + .5)/1 - .5 = 0 exactly): the view
     // basis is dead after the per-ray setup, keeping the march loop's
     // register footprint small
-    count = march<Geo, NEAREST, OCT, EPI == EPI_ROWMAX>(a.geo, a.views[vid], (double)col,
+    count = march<Geo, NEAREST, OCT, EPI == EPI_ROWMAX || EPI == EPI_ROWCOUNT>(a.geo, a.views[vid], (double)col,
                                                        (double)row, a.step, acc, chunk, K);
   } else if (active) {
     const ct_ray_view& v = a.views[vid];
@@ -306,7 +309,7 @@ __device__ __forceinline__ void fp_body(const FpArgs<Geo>& a) {
       const double off_v = dsub(ddiv((double)sv + 0.5, (double)ss), 0.5);
       for (int su = 0; su < ss; ++su) {
         const double off_u = dsub(ddiv((double)su + 0.5, (double)ss), 0.5);
-        count += march<Geo, NEAREST, OCT, EPI == EPI_ROWMAX>(
+        count += march<Geo, NEAREST, OCT, EPI == EPI_ROWMAX || EPI == EPI_ROWCOUNT>(
             a.geo, v, dadd((double)col, off_u), dadd((double)row, off_v), a.step, acc, chunk, K);
       }
     }
@@ -329,6 +332,10 @@ __device__ __forceinline__ void fp_body(const FpArgs<Geo>& a) {
       a.out0[(size_t)b * npix + pix] = (float)p64;
       if (a.out1) a.out1[(size_t)b * npix + pix] = (float)w64;
     }
+  } else if (EPI == EPI_ROWCOUNT) {
+    if (active && lead && count > 0)
+      atomicAdd(reinterpret_cast<unsigned long long*>(a.red) + (size_t)b * a.rows + row,
+                (unsigned long long)count);
   } else if (EPI == EPI_CORR) {
     if (active && lead) {
       float c = 0.0f;
@@ -437,9 +444,9 @@ int launch_fp(const Geo& geo, const ct_ray_view* views, const ct_batch& b, const
   a.red = red;
   if (s.nearest)
     fp_kernel<Geo, EPI, true, GL_PLAIN><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
-  else if (EPI != EPI_ROWMAX && geo.oct && geo.quad)
+  else if (EPI != EPI_ROWMAX && EPI != EPI_ROWCOUNT && geo.oct && geo.quad)
     fp_kernel<Geo, EPI, false, GL_QUAD><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
-  else if (EPI != EPI_ROWMAX && geo.oct)
+  else if (EPI != EPI_ROWMAX && EPI != EPI_ROWCOUNT && geo.oct)
   {
     if (32.0 * geo.cell_kstride <= CT_FP_SMALL_LAYER_BYTES)
       fp_kernel_small<Geo, EPI, false, GL_OCT><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
@@ -592,6 +599,17 @@ int fp_rows(const Geo& geo, const ct_ray_view* views, const ct_batch* batch,
                                           scratch, CT_STREAM(stream), n_slots, row_lo, row_hi);
   return launch_fp<Geo, EPI_RESID>(geo, views, *batch, *s, p_meas, nullptr, nullptr, nullptr,
                                    scratch, CT_STREAM(stream), n_slots, row_lo, row_hi);
+}
+
+template <class Geo>
+int launch_row_samples(const Geo& geo, const ct_ray_view* views, const ct_batch* batch,
+                       const ct_sampling* s, uint64_t* out, ct_stream_t stream) {
+  if (!out) return set_err(CT_ERR_ARG, "null row_samples");
+  if (cudaMemsetAsync(out, 0, sizeof(uint64_t) * batch->n_batch * batch->det_rows,
+                      CT_STREAM(stream)))
+    return check_launch("memset");
+  return launch_fp<Geo, EPI_ROWCOUNT>(geo, views, *batch, *s, nullptr, nullptr, nullptr, nullptr,
+                                      reinterpret_cast<double*>(out), CT_STREAM(stream));
 }
 
 }  // namespace
@@ -760,6 +778,25 @@ int ct_rowsum_max_cyl(const ct_cyl_grid* grid, const ct_ray_view* views, const c
   geo.init(nullptr, nullptr, *grid);
   return launch_fp<CylGeo, EPI_ROWMAX>(geo, views, *batch, *s, nullptr, nullptr, nullptr,
                                        nullptr, max_row, CT_STREAM(stream));
+}
+
+int ct_row_samples_cyl(const ct_cyl_grid* grid, const ct_ray_view* views, const ct_batch* batch,
+                       const ct_sampling* s, uint64_t* row_samples, ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cyl(grid))) return rc;
+  CylGeo geo;
+  geo.init(nullptr, nullptr, *grid);
+  return launch_row_samples(geo, views, batch, s, row_samples, stream);
+}
+
+int ct_row_samples_cart(const ct_cart_grid* grid, const ct_ray_view* views,
+                        const ct_batch* batch, const ct_sampling* s, uint64_t* row_samples,
+                        ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cart(grid))) return rc;
+  CartGeo geo;
+  geo.init(nullptr, nullptr, *grid);
+  return launch_row_samples(geo, views, batch, s, row_samples, stream);
 }
 
 int ct_rowsum_max_cart(const ct_cart_grid* grid, const ct_ray_view* views,

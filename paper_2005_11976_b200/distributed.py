@@ -7,8 +7,9 @@ bytes:
 
 * **angle sharding** -- within OS-SART subset s (n views of H x W pixels)
   the subset's rays are split by flattened detector row f = b*H + row into G
-  contiguous ranges, balanced to one FP block tile (ct_fp_row_tile), so each
-  rank marches ~1/G of the subset's rays on the same mu.  The corrections are
+  contiguous ranges at FP block tiles (ct_fp_row_tile), balanced by the
+  rows' in-support sample counts (ct_row_samples_*), so each rank marches
+  ~1/G of the subset's samples on the same mu.  The corrections are
   all-gathered (n*H*W floats: 45 MiB at C2, against 128 MiB for a
   reduce-scatter of num), then every rank back-projects ALL the subset's
   views onto its own 1/G voxel shard with the fused SART update
@@ -76,23 +77,29 @@ def shard_range(n: int, rank: int, world: int):
     return off, max(0, min(chunk, n - off)), chunk
 
 
-def row_bounds(n_views: int, rows: int, world: int, tile: int) -> np.ndarray:
+def row_bounds(n_views: int, rows: int, world: int, tile: int, cost=None) -> np.ndarray:
     """Split the flattened rows [0, n_views*rows) of a view batch into `world`
     contiguous ranges at FP block-tile boundaries (v*rows + z*tile, and view
-    ends), each boundary the tile boundary nearest to r*N/world.  Returns
-    world+1 non-decreasing bounds; rank r owns [b[r], b[r+1])."""
+    ends), each boundary the tile boundary whose cumulative cost is nearest
+    to r/world of the total (cost: one weight per flattened row, default
+    uniform).  Returns world+1 non-decreasing bounds; rank r owns
+    [b[r], b[r+1])."""
+    total = n_views * rows
     n_tiles = -(-rows // tile)
     starts = (np.arange(n_views)[:, None] * rows
               + np.minimum(np.arange(n_tiles)[None, :] * tile, rows)).ravel()
-    cand = np.append(starts, n_views * rows)
-    total = n_views * rows
+    cand = np.unique(np.append(starts, total))
+    if cost is None:
+        cum = cand.astype(np.float64)
+    else:
+        c = np.concatenate([[0.0], np.cumsum(np.asarray(cost, dtype=np.float64))])
+        cum = c[cand]
     b = [0]
     for r in range(1, world):
-        t = r * total / world
-        i = int(np.searchsorted(cand, t))
-        lo = cand[max(i - 1, 0)]
-        hi = cand[min(i, len(cand) - 1)]
-        pick = lo if (t - lo) <= (hi - t) else hi
+        t = r * cum[-1] / world
+        i = int(np.searchsorted(cum, t))
+        lo, hi = max(i - 1, 0), min(i, len(cand) - 1)
+        pick = cand[lo] if (t - cum[lo]) <= (cum[hi] - t) else cand[hi]
         b.append(max(int(pick), b[-1]))
     b.append(total)
     return np.asarray(b, dtype=np.int64)
@@ -137,6 +144,12 @@ class GpuEngine:
     def row_tile(self) -> int:
         return self.eng.row_tile()
 
+    def row_costs(self, views):
+        """FP cost per flattened detector row of a view batch: its in-support
+        samples plus a per-ray setup allowance (~8 samples per pixel)."""
+        return (self.eng.row_samples(np.asarray(views)).ravel().astype(np.float64)
+                + 8.0 * self.eng.cols)
+
     def scratch(self, n_slots: int):
         torch = self.D.torch_mod()
         s = self.eng.residual_scratch(n_slots)
@@ -173,7 +186,8 @@ class _RowShard:
     def __init__(self, views, rows, rank, world, tile, engine):
         self.views = np.asarray(views)
         self.n = len(self.views)
-        self.bounds = row_bounds(self.n, rows, world, tile)
+        cost = engine.row_costs(self.views) if (world > 1 and self.n) else None
+        self.bounds = row_bounds(self.n, rows, world, tile, cost)
         self.lo, self.hi = int(self.bounds[rank]), int(self.bounds[rank + 1])
         self.sizes = np.diff(self.bounds)
         self.chunk = int(self.sizes.max()) if self.n else 0
@@ -343,7 +357,11 @@ class ShardedSartRun:
         wall = time.perf_counter() - t0
         res = ([math.sqrt(float(x)) for x in self.resid.cpu().numpy()]
                if self.cfg.compute_residuals else [])
-        mu = self.mu if self.ps.on_device else self.mu.cpu().numpy()
+        if self.ps.on_device:
+            mu = self.mu
+        else:
+            from . import _device as D
+            mu = D.to_host(self.mu, pinned=True) if self.mu.is_cuda else self.mu.numpy()
         return (_volume_cls(self.grid)._trusted(self.grid, mu),
                 ReconReport(residuals=res, wall_time=wall, config=_config_echo(self.cfg)))
 

@@ -150,6 +150,19 @@ class SartEngine:
                D.ptr(out), D.stream_handle())
         return D.to_host(out)
 
+    def row_samples(self, views) -> np.ndarray:
+        """In-support samples per detector row of the given views, shape
+        (len(views), rows) int64 (geometry only, no march)."""
+        torch = D.torch_mod()
+        n = len(views)
+        out = torch.zeros(n * self.rows, dtype=torch.int64, device=self.device)
+        slots = D.upload_i32(views)
+        b = D.batch_c(n, self.rows, self.cols, slots)
+        fn = "ct_row_samples_cyl" if self.cyl else "ct_row_samples_cart"
+        N.call(fn, C.byref(self.gc), D.ptr(self.fp_views), C.byref(b), C.byref(self.samp),
+               D.ptr(out), D.stream_handle())
+        return D.to_host(out).reshape(n, self.rows)
+
     def prepare_thresholds(self, order_slots=None) -> np.ndarray:
         """Row maxima -> skip thresholds; EmptyView for the first empty view."""
         max_row = self.row_max()

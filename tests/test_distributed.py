@@ -58,6 +58,15 @@ class OracleEngine:
     def row_tile(self):
         return self.TILE
 
+    def row_costs(self, views):
+        """samples per detector row (the oracle's row sums w are counts * step)"""
+        out = []
+        for v in views:
+            _, w = self.o.forward(np.zeros(self.o.grid_shape(self.grid)), self.grid,
+                                  self.ps.geom, int(v))
+            out.append(w.sum(axis=1))
+        return np.concatenate(out) + 1e-3
+
     def scratch(self, n_slots):
         return self.torch.zeros(n_slots * self.H, dtype=self.torch.float64)
 
@@ -183,6 +192,12 @@ def test_shard_helpers():
         if n_views * rows >= world * tile:
             assert np.abs(np.diff(b) - n_views * rows / world).max() <= tile
     assert np.array_equal(PD.row_bounds(45, 512, 8, 8), np.arange(9) * 2880)
+    # cost-weighted: rows 0..9 of one view cost 10x the rest
+    cost = np.ones(40)
+    cost[:10] = 10.0
+    b = PD.row_bounds(1, 40, 2, 2, cost)
+    assert b[1] == 6                       # 60 of 130 left, 70 right (tile 2)
+    assert np.array_equal(PD.row_bounds(1, 40, 2, 2, np.ones(40)), PD.row_bounds(1, 40, 2, 2))
     n = 1001
     ranges = [PD.shard_range(n, r, 4) for r in range(4)]
     covered = sum(c for _, c, _ in ranges)

@@ -270,3 +270,23 @@ def test_sharded_kernels_split_bit_identical(world):
         off, cnt, _ = PD.shard_range(nvox, r, world)
         e.bp_update_range(full, slots, n, upd, off, cnt, quads)
     assert torch.equal(got, ref)
+
+
+def test_row_samples_match_row_sums():
+    """ct_row_samples_*: per detector row, the in-support sample counts that
+    the FP's row sums w = count * step / ss^2 carry (exact integers)."""
+    from paper_2005_11976_b200.recon import SartEngine
+    geom = P.ScanGeometry(400.0, 200.0, 40, 36, 0.2, (19.5, 17.5), P.full_turn_angles(5))
+    for grid in (P.CylGrid(12, 24, 10, 4.0, 6.0, P.Pose.tilt(0.3, 0.05, [0.3, 0.1, 0.0])),
+                 P.CartGrid.centered(10, 12, 8, 0.6)):
+        samp = P.RaySamplingConfig(supersample=2)
+        eng = SartEngine(grid, geom, samp)
+        got = eng.row_samples(np.arange(geom.n_proj))
+        mu = torch.zeros(grid.shape, device="cuda")
+        vol = (P.CylVolume if isinstance(grid, P.CylGrid) else P.CartVolume)(grid, mu)
+        step = samp.step_for(grid)
+        for i in range(geom.n_proj):
+            _, w = P.forward_project(vol, geom, i, samp, return_weights=True)
+            counts = np.rint(np.asarray(w.cpu() if hasattr(w, "cpu") else w, np.float64)
+                             * 4 / step).sum(axis=1)
+            assert np.array_equal(got[i], counts.astype(np.int64))
