@@ -359,16 +359,72 @@ __host__ __device__ inline unsigned gather_layer_stride(unsigned rows, unsigned 
   return ks + (256u - (ks + js + 1u) % 256u) % 256u;
 }
 
+// CT_POW2_CELLS (A/B): power-of-two row and layer strides (js >= 256), so the
+// cell index is (kb << lk) + (jb << lj) + ib on the ALU pipe instead of two
+// IMADs on the FMA pipe; the magic bias then leaves a constant B (B << l == 0
+// mod 2^32 for l >= 8), folded into the base pointer.  Memory: up to 4x the
+// cells (padding is never written or read).
+#ifndef CT_POW2_CELLS
+#define CT_POW2_CELLS 0
+#endif
+struct CellStrides {
+  unsigned js, ks, lj, lk;
+};
+__host__ __device__ inline unsigned ct_next_pow2(unsigned x) {
+  unsigned p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+__host__ __device__ inline unsigned ct_ilog2(unsigned x) {
+  unsigned l = 0;
+  while ((1u << l) < x) ++l;
+  return l;
+}
+// gather-layout base pointer for gather_index's cell numbers: `one_on` cells
+// on (the cylindrical r floor bits carry index - 1), and B cells back with
+// CT_POW2_CELLS (the index then carries the bias B; u32 index + B < 2^31)
+__host__ inline const float4* cell_base(const float* gather, bool quad, int one_on) {
+  const uintptr_t cb = quad ? 16u : 32u;
+  uintptr_t p = reinterpret_cast<uintptr_t>(gather) + cb * (uintptr_t)one_on;
+#if CT_POW2_CELLS
+  p -= cb * (uintptr_t)kMagicBits;
+#endif
+  return reinterpret_cast<const float4*>(p);
+}
+// signed cell offset of a gather_index value
+__device__ __forceinline__ ptrdiff_t cell_off(unsigned idx) {
+#if CT_POW2_CELLS
+  return (ptrdiff_t)(size_t)idx;
+#else
+  return (ptrdiff_t)(int)idx;   // the first cylindrical cell is -1
+#endif
+}
+// rows x ncols real cells per layer
+__host__ __device__ inline CellStrides cell_strides(unsigned rows, unsigned ncols) {
+  CellStrides c;
+#if CT_POW2_CELLS
+  c.js = ct_next_pow2(ncols < 256u ? 256u : ncols);
+  c.ks = ct_next_pow2(rows * c.js);
+  c.lj = ct_ilog2(c.js);
+  c.lk = ct_ilog2(c.ks);
+#else
+  c.js = ncols;
+  c.ks = gather_layer_stride(rows, ncols);
+  c.lj = c.lk = 0;
+#endif
+  return c;
+}
+
 // Large volumes use 16-byte per-layer bilinear cells (GL_QUAD) instead of the
 // 32-byte trilinear cells: half the bytes per h layer, so more of the band of
 // layers a wave of rays works on stays in L2, for one more load and two f32x2
 // subtractions per cell entered.  Measured (A/B): C5 -23.5 %, C4-cyl equal,
 // C4-cart (8.4 MB layers) +22 %, C2 (4.2 MB layers) +15 %; hence layers above
 // 10 MB.  CT_GATHER_QUAD=0/1 overrides.
-inline bool gather_quad(unsigned ks) {
+inline bool gather_quad(double cells_per_layer) {
   const char* e = getenv("CT_GATHER_QUAD");
   if (e && *e) return e[0] == '1';
-  return 32.0 * ks > 10.0e6;
+  return 32.0 * cells_per_layer > 10.0e6;
 }
 
 struct CylGeo {
@@ -381,7 +437,8 @@ struct CylGeo {
   float inv_dr, inv_dth, inv_dh, h_off, h_off1, nr_m1, nh_m1;
   float tc[8];   // 2 atan polynomial coefficients times n_theta / (2 pi)
   // gather layout: cells (nh+1, nt+1, nr+1), strides (ks, js, 1)
-  unsigned cell_kstride, cell_jstride, jb_wrap;
+  unsigned cell_kstride, cell_jstride, jb_wrap, cell_lj, cell_lk;
+  double cells_layer;   // real cells per layer (rows x columns)
 
   __host__ void init(const float* m, const float* gather, const ct_cyl_grid& g) {
     mu = m;
@@ -397,11 +454,16 @@ struct CylGeo {
     nh_m1 = (float)(g.n_h - 1);
     h_off1 = h_off + 1.0f;
     const unsigned B = kMagicBits;
-    cell_jstride = (unsigned)g.n_r + 1u;
-    cell_kstride = gather_layer_stride((unsigned)gather_rows(g.n_theta), cell_jstride);
-    quad = gather_quad(cell_kstride);
+    const CellStrides cs = cell_strides((unsigned)gather_rows(g.n_theta), (unsigned)g.n_r + 1u);
+    cell_jstride = cs.js;
+    cell_kstride = cs.ks;
+    cell_lj = cs.lj;
+    cell_lk = cs.lk;
+    cells_layer = (double)gather_rows(g.n_theta) * (g.n_r + 1);
+    quad = gather_quad(cells_layer);
     // the r floor bits carry index - 1 (kRMagic): the base is one cell on
-    oct = gather ? reinterpret_cast<const float4*>(gather) + (quad ? 1 : 2) : nullptr;
+    // (CT_POW2_CELLS: and B cells back, see cell_strides)
+    oct = gather ? cell_base(gather, quad, 1) : nullptr;
     jb_wrap = B + (unsigned)g.n_theta;
   }
   // theta rows of the gather layout: indices -1 .. n_theta - 1 (see RayF)
@@ -549,11 +611,15 @@ struct CylGeo {
 
   // gather-layout cell index (modular uint32; one constant for all offsets)
   template <bool WRAP>
-  __device__ __forceinline__ int gather_index(const Cell& c) const {
+  __device__ __forceinline__ unsigned gather_index(const Cell& c) const {
     // WRAP (rays crossing theta = 2 pi): rows past n_theta wrap onto the
     // primary rows (integer ops)
     const unsigned jb = (WRAP && c.jb > jb_wrap) ? c.jb - (unsigned)nt : c.jb;
-    return (int)(c.kb * cell_kstride + jb * cell_jstride + c.ib);
+#if CT_POW2_CELLS
+    return (c.kb << cell_lk) + (jb << cell_lj) + c.ib;
+#else
+    return c.kb * cell_kstride + jb * cell_jstride + c.ib;
+#endif
   }
 
   // the same 8 values from the plain mu layout (r/h clamp, theta modulo n_theta)
@@ -592,10 +658,12 @@ struct CartGeo {
   double vs, lo[3], hi[3];
   float inv_vs, off[3], off1[3], nx_m1, ny_m1, nz_m1;
   unsigned cell_kstride, cell_jstride;   // gather layout (nz+1, ny+1, nx+1), strides (ks, js, 1)
+  unsigned cell_lj, cell_lk;
+  double cells_layer;
 
   __host__ void init(const float* m, const float* gather, const ct_cart_grid& g) {
     mu = m;
-    oct = reinterpret_cast<const float4*>(gather);
+    oct = nullptr;
     nz = g.n_z; ny = g.n_y; nx = g.n_x;
     vs = g.voxel_size;
     for (int a = 0; a < 3; ++a) lo[a] = g.origin[a];
@@ -606,9 +674,14 @@ struct CartGeo {
     for (int a = 0; a < 3; ++a) off[a] = (float)(-g.origin[a] / g.voxel_size - 0.5);
     nx_m1 = (float)(nx - 1); ny_m1 = (float)(ny - 1); nz_m1 = (float)(nz - 1);
     for (int a = 0; a < 3; ++a) off1[a] = off[a] + 1.0f;
-    cell_jstride = (unsigned)nx + 1u;
-    cell_kstride = gather_layer_stride((unsigned)ny + 1u, cell_jstride);
-    quad = gather_quad(cell_kstride);
+    const CellStrides cs = cell_strides((unsigned)ny + 1u, (unsigned)nx + 1u);
+    cell_jstride = cs.js;
+    cell_kstride = cs.ks;
+    cell_lj = cs.lj;
+    cell_lk = cs.lk;
+    cells_layer = (double)(ny + 1) * (nx + 1);
+    quad = gather_quad(cells_layer);
+    oct = gather ? cell_base(gather, quad, 0) : nullptr;
   }
 
   // _kernels.py:207-231
@@ -702,8 +775,12 @@ struct CartGeo {
   }
 
   template <bool WRAP>
-  __device__ __forceinline__ int gather_index(const Cell& c) const {
-    return (int)(c.kb * cell_kstride + c.jb * cell_jstride + c.ib);
+  __device__ __forceinline__ unsigned gather_index(const Cell& c) const {
+#if CT_POW2_CELLS
+    return (c.kb << cell_lk) + (c.jb << cell_lj) + c.ib;
+#else
+    return c.kb * cell_kstride + c.jb * cell_jstride + c.ib;
+#endif
   }
 
   __device__ __forceinline__ void fetch_plain(const Cell& c, float4& a, float4& b) const {

@@ -107,25 +107,25 @@ __device__ __forceinline__ float march_linear(const Geo& geo, const RayF& ry, in
   // flight together (a single chain serialises load -> evaluate -> next load
   // through its cell registers), and one f32x2 locate serves two chains.
   struct Chain {
-    int prev = INT_MIN;   // no cell (indices are >= -1)
+    unsigned prev = 0x80000000u;   // no cell (indices are >= -1, or >= B - 1 < 2^31)
     float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pb = make_float4(0.f, 0.f, 0.f, 0.f);
     float sum = 0.0f;
   };
   auto value = [&](Chain& ch, const Cell& c) -> float {
     if (OCT == GL_OCT) {
-      const int idx = geo.template gather_index<WRAP>(c);
+      const unsigned idx = geo.template gather_index<WRAP>(c);
       // signed: the cylindrical r bits make the first cell's index -1 (kRMagic)
-      if (idx != ch.prev) ld_cell(geo.oct + 2 * (ptrdiff_t)idx, ch.pa, ch.pb);
+      if (idx != ch.prev) ld_cell(geo.oct + 2 * cell_off(idx), ch.pa, ch.pb);
       ch.prev = idx;   // (unconditional: equal when not reloaded; no predicated move)
       return trilinear_eval(ch.pa, ch.pb, c.w0, c.w1, c.w2);
     }
     if (OCT == GL_QUAD) {
       // bilinear layers k, k+1 of the cell; the h terms are their
       // difference (two f32x2 subtractions)
-      const int idx = geo.template gather_index<WRAP>(c);
+      const unsigned idx = geo.template gather_index<WRAP>(c);
       if (idx != ch.prev) {
-        const float4 a = ld_vquad(geo.oct + (ptrdiff_t)idx);
-        const float4 b = ld_vquad(geo.oct + (ptrdiff_t)idx + geo.cell_kstride);
+        const float4 a = ld_vquad(geo.oct + cell_off(idx));
+        const float4 b = ld_vquad(geo.oct + cell_off(idx) + geo.cell_kstride);
         ch.pa = a;
         float x0, x1, y0, y1;
         upk(sub2(pk(b.x, b.y), pk(a.x, a.y)), x0, x1);
@@ -448,7 +448,7 @@ int launch_fp(const Geo& geo, const ct_ray_view* views, const ct_batch& b, const
     fp_kernel<Geo, EPI, false, GL_QUAD><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
   else if (EPI != EPI_ROWMAX && EPI != EPI_ROWCOUNT && geo.oct)
   {
-    if (32.0 * geo.cell_kstride <= CT_FP_SMALL_LAYER_BYTES)
+    if (32.0 * geo.cells_layer <= CT_FP_SMALL_LAYER_BYTES)
       fp_kernel_small<Geo, EPI, false, GL_OCT><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
     else
       fp_kernel<Geo, EPI, false, GL_OCT><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
@@ -467,19 +467,16 @@ int launch_fp(const Geo& geo, const ct_ray_view* views, const ct_batch& b, const
 // one h-layer (blockIdx.y = kc) per grid row; cells past the layer's rows are
 // the stride padding (zeroed, never read)
 __global__ void pack_gather_cyl_kernel(const float* __restrict__ mu, int nh, int nt, int nr,
-                                       unsigned ks, float4* __restrict__ oct) {
+                                       unsigned ks, unsigned js, float4* __restrict__ oct) {
   // cells (kc, jc, ic), kc in [0, nh], jc in [0, nt], ic in [0, nr]: corner
-  // (kc-1, jc-1, ic-1); index -1 is a halo (r/h: copy of 0; theta: row nt-1)
+  // (kc-1, jc-1, ic-1); index -1 is a halo (r/h: copy of 0; theta: row nt-1).
+  // Only real cells are written (the stride padding is never read).
   const unsigned rem = blockIdx.x * blockDim.x + threadIdx.x;
-  if (rem >= ks) return;
+  const unsigned nc = (unsigned)nr + 1u;
+  if (rem >= (unsigned)(nt + 1) * nc) return;
   const int kc = blockIdx.y;
-  const size_t m = (size_t)kc * ks + rem;
-  const unsigned js = (unsigned)nr + 1u;
-  const int jc = (int)(rem / js), ic = (int)(rem % js);
-  if (jc > nt) {
-    oct[2 * m] = oct[2 * m + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
-    return;
-  }
+  const int jc = (int)(rem / nc), ic = (int)(rem % nc);
+  const size_t m = (size_t)kc * ks + (size_t)jc * js + ic;
   const int i = max(ic - 1, 0), i1 = min(ic, nr - 1);
   const int k = max(kc - 1, 0), k1 = min(kc, nh - 1);
   const int j = (jc == 0) ? nt - 1 : jc - 1, j1 = (jc == nt) ? 0 : jc;
@@ -492,18 +489,14 @@ __global__ void pack_gather_cyl_kernel(const float* __restrict__ mu, int nh, int
 }
 
 __global__ void pack_gather_cart_kernel(const float* __restrict__ mu, int nz, int ny, int nx,
-                                        unsigned ks, float4* __restrict__ oct) {
+                                        unsigned ks, unsigned js, float4* __restrict__ oct) {
   // cells (kc, jc, ic) in [0, n] per axis: corner (kc-1, jc-1, ic-1)
   const unsigned rem = blockIdx.x * blockDim.x + threadIdx.x;
-  if (rem >= ks) return;
+  const unsigned nc = (unsigned)nx + 1u;
+  if (rem >= (unsigned)(ny + 1) * nc) return;
   const int kc = blockIdx.y;
-  const size_t m = (size_t)kc * ks + rem;
-  const unsigned js = (unsigned)nx + 1u;
-  const int jc = (int)(rem / js), ic = (int)(rem % js);
-  if (jc > ny) {
-    oct[2 * m] = oct[2 * m + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
-    return;
-  }
+  const int jc = (int)(rem / nc), ic = (int)(rem % nc);
+  const size_t m = (size_t)kc * ks + (size_t)jc * js + ic;
   const int i = max(ic - 1, 0), i1 = min(ic, nx - 1);
   const int j = max(jc - 1, 0), j1 = min(jc, ny - 1);
   const int k = max(kc - 1, 0), k1 = min(kc, nz - 1);
@@ -522,17 +515,13 @@ __global__ void pack_gather_cart_kernel(const float* __restrict__ mu, int nz, in
 // trilinear_coeffs, so GL_QUAD, GL_OCT and the plain path agree bit for bit.
 template <bool CYL>
 __global__ void pack_vquad_kernel(const float* __restrict__ mu, int nk, int nj, int ni,
-                                  unsigned ks, float4* __restrict__ q) {
+                                  unsigned ks, unsigned js, float4* __restrict__ q) {
   const unsigned rem = blockIdx.x * blockDim.x + threadIdx.x;
-  if (rem >= ks) return;
+  const unsigned nc = (unsigned)ni + 1u;
+  if (rem >= (unsigned)(nj + 1) * nc) return;
   const int kc = blockIdx.y;
-  const size_t m = (size_t)kc * ks + rem;
-  const unsigned js = (unsigned)ni + 1u;
-  const int jc = (int)(rem / js), ic = (int)(rem % js);
-  if (jc > nj) {
-    q[m] = make_float4(0.f, 0.f, 0.f, 0.f);
-    return;
-  }
+  const int jc = (int)(rem / nc), ic = (int)(rem % nc);
+  const size_t m = (size_t)kc * ks + (size_t)jc * js + ic;
   const int k = min(max(kc - 1, 0), nk - 1);
   const int i = max(ic - 1, 0), i1 = min(ic, ni - 1);
   int j, j1;
@@ -551,20 +540,26 @@ __global__ void pack_vquad_kernel(const float* __restrict__ mu, int nk, int nj, 
   q[m] = make_float4(a0, dr0, a2 - a0, dr1 - dr0);
 }
 
-unsigned gather_ks_cyl(const ct_cyl_grid& g) {
-  return gather_layer_stride((unsigned)CylGeo::gather_rows(g.n_theta), (unsigned)g.n_r + 1u);
+CellStrides gather_strides_cyl(const ct_cyl_grid& g) {
+  return cell_strides((unsigned)CylGeo::gather_rows(g.n_theta), (unsigned)g.n_r + 1u);
 }
-unsigned gather_ks_cart(const ct_cart_grid& g) {
-  return gather_layer_stride((unsigned)g.n_y + 1u, (unsigned)g.n_x + 1u);
+CellStrides gather_strides_cart(const ct_cart_grid& g) {
+  return cell_strides((unsigned)g.n_y + 1u, (unsigned)g.n_x + 1u);
 }
+double cells_layer_cyl(const ct_cyl_grid& g) {
+  return (double)CylGeo::gather_rows(g.n_theta) * (g.n_r + 1);
+}
+double cells_layer_cart(const ct_cart_grid& g) { return (double)(g.n_y + 1) * (g.n_x + 1); }
 // gather buffer length in floats: (n+1) layers x 8 floats, or GL_QUAD (n+2) x 4
 int64_t gather_floats_cyl(const ct_cyl_grid& g) {
-  const unsigned ks = gather_ks_cyl(g);
-  return gather_quad(ks) ? 4 * (int64_t)(g.n_h + 2) * ks : 8 * (int64_t)(g.n_h + 1) * ks;
+  const unsigned ks = gather_strides_cyl(g).ks;
+  return gather_quad(cells_layer_cyl(g)) ? 4 * (int64_t)(g.n_h + 2) * ks
+                                         : 8 * (int64_t)(g.n_h + 1) * ks;
 }
 int64_t gather_floats_cart(const ct_cart_grid& g) {
-  const unsigned ks = gather_ks_cart(g);
-  return gather_quad(ks) ? 4 * (int64_t)(g.n_z + 2) * ks : 8 * (int64_t)(g.n_z + 1) * ks;
+  const unsigned ks = gather_strides_cart(g).ks;
+  return gather_quad(cells_layer_cart(g)) ? 4 * (int64_t)(g.n_z + 2) * ks
+                                          : 8 * (int64_t)(g.n_z + 1) * ks;
 }
 
 
@@ -828,14 +823,18 @@ int ct_pack_gather_cyl(const float* mu, const ct_cyl_grid* grid, float* gather,
   if (!mu || !gather) return set_err(CT_ERR_ARG, "null mu/gather");
   if (reinterpret_cast<uintptr_t>(gather) % 16) return set_err(CT_ERR_ARG, "gather not 16B-aligned");
   if (grid->n_h + 2 > 65535) return set_err(CT_ERR_ARG, "gather layout: n_h + 2 > 65535");
-  const unsigned ks = gather_ks_cyl(*grid);
-  if (gather_quad(ks)) {
-    pack_vquad_kernel<true><<<dim3(blocks_for(ks, 256), grid->n_h + 2), 256, 0, CT_STREAM(stream)>>>(
-        mu, grid->n_h, grid->n_theta, grid->n_r, ks, reinterpret_cast<float4*>(gather));
+  const CellStrides cs = gather_strides_cyl(*grid);
+  const double cells = cells_layer_cyl(*grid);
+  if (CT_POW2_CELLS && (double)(grid->n_h + 2) * cs.ks + kMagicBits >= 2147483648.0)
+    return set_err(CT_ERR_ARG, "gather layout too large for power-of-two strides");
+  const unsigned nb = blocks_for((int64_t)cells, 256);
+  if (gather_quad(cells)) {
+    pack_vquad_kernel<true><<<dim3(nb, grid->n_h + 2), 256, 0, CT_STREAM(stream)>>>(
+        mu, grid->n_h, grid->n_theta, grid->n_r, cs.ks, cs.js, reinterpret_cast<float4*>(gather));
     return check_launch("pack_vquad_kernel");
   }
-  pack_gather_cyl_kernel<<<dim3(blocks_for(ks, 256), grid->n_h + 1), 256, 0, CT_STREAM(stream)>>>(
-      mu, grid->n_h, grid->n_theta, grid->n_r, ks, reinterpret_cast<float4*>(gather));
+  pack_gather_cyl_kernel<<<dim3(nb, grid->n_h + 1), 256, 0, CT_STREAM(stream)>>>(
+      mu, grid->n_h, grid->n_theta, grid->n_r, cs.ks, cs.js, reinterpret_cast<float4*>(gather));
   return check_launch("pack_gather_cyl_kernel");
 }
 
@@ -846,14 +845,18 @@ int ct_pack_gather_cart(const float* mu, const ct_cart_grid* grid, float* gather
   if (!mu || !gather) return set_err(CT_ERR_ARG, "null mu/gather");
   if (reinterpret_cast<uintptr_t>(gather) % 16) return set_err(CT_ERR_ARG, "gather not 16B-aligned");
   if (grid->n_z + 2 > 65535) return set_err(CT_ERR_ARG, "gather layout: n_z + 2 > 65535");
-  const unsigned ks = gather_ks_cart(*grid);
-  if (gather_quad(ks)) {
-    pack_vquad_kernel<false><<<dim3(blocks_for(ks, 256), grid->n_z + 2), 256, 0, CT_STREAM(stream)>>>(
-        mu, grid->n_z, grid->n_y, grid->n_x, ks, reinterpret_cast<float4*>(gather));
+  const CellStrides cs = gather_strides_cart(*grid);
+  const double cells = cells_layer_cart(*grid);
+  if (CT_POW2_CELLS && (double)(grid->n_z + 2) * cs.ks + kMagicBits >= 2147483648.0)
+    return set_err(CT_ERR_ARG, "gather layout too large for power-of-two strides");
+  const unsigned nb = blocks_for((int64_t)cells, 256);
+  if (gather_quad(cells)) {
+    pack_vquad_kernel<false><<<dim3(nb, grid->n_z + 2), 256, 0, CT_STREAM(stream)>>>(
+        mu, grid->n_z, grid->n_y, grid->n_x, cs.ks, cs.js, reinterpret_cast<float4*>(gather));
     return check_launch("pack_vquad_kernel");
   }
-  pack_gather_cart_kernel<<<dim3(blocks_for(ks, 256), grid->n_z + 1), 256, 0, CT_STREAM(stream)>>>(
-      mu, grid->n_z, grid->n_y, grid->n_x, ks, reinterpret_cast<float4*>(gather));
+  pack_gather_cart_kernel<<<dim3(nb, grid->n_z + 1), 256, 0, CT_STREAM(stream)>>>(
+      mu, grid->n_z, grid->n_y, grid->n_x, cs.ks, cs.js, reinterpret_cast<float4*>(gather));
   return check_launch("pack_gather_cart_kernel");
 }
 
