@@ -122,10 +122,17 @@ __device__ __forceinline__ float march_linear(const Geo& geo, const RayF& ry, in
     if (OCT == GL_QUAD) {
       // bilinear layers k, k+1 of the cell; the h terms are their
       // difference (two f32x2 subtractions)
+#if CT_QUAD_BRICK
+      const unsigned idx = geo.template quad_cell<WRAP>(c, 0u);
+      if (idx != ch.prev) {
+        const float4 a = ld_vquad(geo.qraw + idx);
+        const float4 b = ld_vquad(geo.qraw + geo.template quad_cell<WRAP>(c, 1u));
+#else
       const unsigned idx = geo.template gather_index<WRAP>(c);
       if (idx != ch.prev) {
         const float4 a = ld_vquad(geo.oct + cell_off(idx));
         const float4 b = ld_vquad(geo.oct + cell_off(idx) + geo.cell_kstride);
+#endif
         ch.pa = a;
         float x0, x1, y0, y1;
         upk(sub2(pk(b.x, b.y), pk(a.x, a.y)), x0, x1);
@@ -521,7 +528,12 @@ __global__ void pack_vquad_kernel(const float* __restrict__ mu, int nk, int nj, 
   if (rem >= (unsigned)(nj + 1) * nc) return;
   const int kc = blockIdx.y;
   const int jc = (int)(rem / nc), ic = (int)(rem % nc);
+#if CT_QUAD_BRICK
+  const size_t m = quad_brick_index((unsigned)kc, (unsigned)jc, (unsigned)ic,
+                                    ((unsigned)nj + 2u) / 2u, (nc + 1u) / 2u);
+#else
   const size_t m = (size_t)kc * ks + (size_t)jc * js + ic;
+#endif
   const int k = min(max(kc - 1, 0), nk - 1);
   const int i = max(ic - 1, 0), i1 = min(ic, ni - 1);
   int j, j1;
@@ -551,12 +563,20 @@ double cells_layer_cyl(const ct_cyl_grid& g) {
 }
 double cells_layer_cart(const ct_cart_grid& g) { return (double)(g.n_y + 1) * (g.n_x + 1); }
 // gather buffer length in floats: (n+1) layers x 8 floats, or GL_QUAD (n+2) x 4
+// bricked GL_QUAD: ceil(layers/2) x ceil(rows/2) x ceil(cols/2) bricks of 8 cells
+int64_t quad_brick_floats(int64_t layers, int64_t rows, int64_t cols) {
+  return 32 * ((layers + 1) / 2) * ((rows + 1) / 2) * ((cols + 1) / 2);
+}
 int64_t gather_floats_cyl(const ct_cyl_grid& g) {
+  if (CT_QUAD_BRICK && gather_quad(cells_layer_cyl(g)))
+    return quad_brick_floats(g.n_h + 2, CylGeo::gather_rows(g.n_theta), g.n_r + 1);
   const unsigned ks = gather_strides_cyl(g).ks;
   return gather_quad(cells_layer_cyl(g)) ? 4 * (int64_t)(g.n_h + 2) * ks
                                          : 8 * (int64_t)(g.n_h + 1) * ks;
 }
 int64_t gather_floats_cart(const ct_cart_grid& g) {
+  if (CT_QUAD_BRICK && gather_quad(cells_layer_cart(g)))
+    return quad_brick_floats(g.n_z + 2, g.n_y + 1, g.n_x + 1);
   const unsigned ks = gather_strides_cart(g).ks;
   return gather_quad(cells_layer_cart(g)) ? 4 * (int64_t)(g.n_z + 2) * ks
                                           : 8 * (int64_t)(g.n_z + 1) * ks;
@@ -827,6 +847,9 @@ int ct_pack_gather_cyl(const float* mu, const ct_cyl_grid* grid, float* gather,
   const double cells = cells_layer_cyl(*grid);
   if (CT_POW2_CELLS && (double)(grid->n_h + 2) * cs.ks + kMagicBits >= 2147483648.0)
     return set_err(CT_ERR_ARG, "gather layout too large for power-of-two strides");
+  if (CT_QUAD_BRICK && gather_quad(cells) &&
+      quad_brick_floats(grid->n_h + 2, grid->n_theta + 1, grid->n_r + 1) / 4 >= 2147483648LL)
+    return set_err(CT_ERR_ARG, "gather layout too large for 32-bit brick indices");
   const unsigned nb = blocks_for((int64_t)cells, 256);
   if (gather_quad(cells)) {
     pack_vquad_kernel<true><<<dim3(nb, grid->n_h + 2), 256, 0, CT_STREAM(stream)>>>(
@@ -849,6 +872,9 @@ int ct_pack_gather_cart(const float* mu, const ct_cart_grid* grid, float* gather
   const double cells = cells_layer_cart(*grid);
   if (CT_POW2_CELLS && (double)(grid->n_z + 2) * cs.ks + kMagicBits >= 2147483648.0)
     return set_err(CT_ERR_ARG, "gather layout too large for power-of-two strides");
+  if (CT_QUAD_BRICK && gather_quad(cells) &&
+      quad_brick_floats(grid->n_z + 2, grid->n_y + 1, grid->n_x + 1) / 4 >= 2147483648LL)
+    return set_err(CT_ERR_ARG, "gather layout too large for 32-bit brick indices");
   const unsigned nb = blocks_for((int64_t)cells, 256);
   if (gather_quad(cells)) {
     pack_vquad_kernel<false><<<dim3(nb, grid->n_z + 2), 256, 0, CT_STREAM(stream)>>>(
