@@ -412,6 +412,13 @@ __host__ __device__ __forceinline__ unsigned quad_brick_index(unsigned kc, unsig
   return ((((kc >> 1) * jbr + (jc >> 1)) * ibr + (ic >> 1)) << 3) | ((kc & 1u) << 2) |
          ((jc & 1u) << 1) | (ic & 1u);
 }
+// GL_OCTB: GL_OCT cells in 2x2 (row, column) bricks per layer, one 128-byte
+// line each (gather_obrick)
+__host__ __device__ __forceinline__ unsigned oct_brick_index(unsigned kc, unsigned jc,
+                                                             unsigned ic, unsigned jbr,
+                                                             unsigned ibr) {
+  return (((kc * jbr + (jc >> 1)) * ibr + (ic >> 1)) << 2) | ((jc & 1u) << 1) | (ic & 1u);
+}
 // rows x ncols real cells per layer
 __host__ __device__ inline CellStrides cell_strides(unsigned rows, unsigned ncols) {
   CellStrides c;
@@ -439,11 +446,24 @@ inline bool gather_quad(double cells_per_layer) {
   if (e && *e) return e[0] == '1';
   return 32.0 * cells_per_layer > 10.0e6;
 }
+// 32-byte cells in 2x2 bricks (GL_OCTB) when the layers exceed the
+// small-layer bound of the FP (CT_FP_SMALL_LAYER_BYTES; A/B: C4-cart -6 %,
+// C2 +15 %).  CT_GATHER_OBRICK=0/1 overrides.
+#ifndef CT_FP_SMALL_LAYER_BYTES
+#define CT_FP_SMALL_LAYER_BYTES 6.0e6
+#endif
+inline bool gather_obrick(double cells_per_layer) {
+  if (gather_quad(cells_per_layer)) return false;
+  const char* e = getenv("CT_GATHER_OBRICK");
+  if (e && *e) return e[0] == '1';
+  return 32.0 * cells_per_layer > CT_FP_SMALL_LAYER_BYTES;
+}
 
 struct CylGeo {
   const float* __restrict__ mu;
   const float4* __restrict__ oct;  // gather layout (ct_pack_gather_cyl) or null
   bool quad;                       // oct holds GL_QUAD corner quads
+  bool obrick;                     // oct holds GL_OCTB bricked 32-byte cells
   int nh, nt, nr;
   double radius, half_h;
   // fp32 sampling constants
@@ -476,6 +496,7 @@ struct CylGeo {
     cell_lk = cs.lk;
     cells_layer = (double)gather_rows(g.n_theta) * (g.n_r + 1);
     quad = gather_quad(cells_layer);
+    obrick = gather_obrick(cells_layer);
     // the r floor bits carry index - 1 (kRMagic): the base is one cell on
     // (CT_POW2_CELLS: and B cells back, see cell_strides)
     oct = gather ? cell_base(gather, quad, 1) : nullptr;
@@ -647,6 +668,12 @@ struct CylGeo {
     return quad_brick_index(c.kb - kMagicBits + dk, jb - kMagicBits, c.ib - kMagicBits + 1u,
                             brick_j, brick_i);
   }
+  template <bool WRAP>
+  __device__ __forceinline__ unsigned oct_cell(const Cell& c) const {
+    const unsigned jb = (WRAP && c.jb > jb_wrap) ? c.jb - (unsigned)nt : c.jb;
+    return oct_brick_index(c.kb - kMagicBits, jb - kMagicBits, c.ib - kMagicBits + 1u,
+                           brick_j, brick_i);
+  }
 
   // the same 8 values from the plain mu layout (r/h clamp, theta modulo n_theta)
   __device__ __forceinline__ void fetch_plain(const Cell& c, float4& a, float4& b) const {
@@ -680,6 +707,7 @@ struct CartGeo {
   const float* __restrict__ mu;
   const float4* __restrict__ oct;  // gather layout (ct_pack_gather_cart) or null
   bool quad;                       // oct holds GL_QUAD corner quads
+  bool obrick;                     // oct holds GL_OCTB bricked 32-byte cells
   int nz, ny, nx;
   double vs, lo[3], hi[3];
   float inv_vs, off[3], off1[3], nx_m1, ny_m1, nz_m1;
@@ -709,6 +737,7 @@ struct CartGeo {
     cell_lk = cs.lk;
     cells_layer = (double)(ny + 1) * (nx + 1);
     quad = gather_quad(cells_layer);
+    obrick = gather_obrick(cells_layer);
     oct = gather ? cell_base(gather, quad, 0) : nullptr;
     qraw = reinterpret_cast<const float4*>(gather);
     brick_j = ((unsigned)ny + 2u) / 2u;
@@ -817,6 +846,11 @@ struct CartGeo {
   __device__ __forceinline__ unsigned quad_cell(const Cell& c, unsigned dk) const {
     return quad_brick_index(c.kb - kMagicBits + dk, c.jb - kMagicBits, c.ib - kMagicBits,
                             brick_j, brick_i);
+  }
+  template <bool WRAP>
+  __device__ __forceinline__ unsigned oct_cell(const Cell& c) const {
+    return oct_brick_index(c.kb - kMagicBits, c.jb - kMagicBits, c.ib - kMagicBits, brick_j,
+                           brick_i);
   }
 
   __device__ __forceinline__ void fetch_plain(const Cell& c, float4& a, float4& b) const {

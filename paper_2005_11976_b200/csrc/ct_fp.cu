@@ -17,7 +17,9 @@ enum FpEpi { EPI_PROJECT = 0, EPI_CORR = 1, EPI_RESID = 2, EPI_ROWMAX = 3, EPI_C
 
 // FP volume layouts: plain mu, the 32-byte polynomial cells (ct_pack_gather_*),
 // or 16-byte corner quads per h layer (large volumes; see gather_quad())
-enum FpLayout { GL_PLAIN = 0, GL_OCT = 1, GL_QUAD = 2 };
+// GL_OCTB: the 32-byte cells in 2x2 (row, column) bricks per 128-byte line, for
+// volumes whose layers exceed the small-layer bound (A/B: C4-cart FP -6 %; C2 +15 %)
+enum FpLayout { GL_PLAIN = 0, GL_OCT = 1, GL_QUAD = 2, GL_OCTB = 3 };
 
 // block = FP_WX x FP_WY warps, each warp a pixel patch (tile_ww x tile_wh rays)
 #ifndef CT_FP_WX
@@ -40,9 +42,6 @@ enum FpLayout { GL_PLAIN = 0, GL_OCT = 1, GL_QUAD = 2 };
 // lose 3 % with it, the GL_QUAD path 11 % (C5)
 #ifndef CT_FP_MAXREG_SMALL
 #define CT_FP_MAXREG_SMALL 56
-#endif
-#ifndef CT_FP_SMALL_LAYER_BYTES
-#define CT_FP_SMALL_LAYER_BYTES 6.0e6
 #endif
 #ifndef CT_FP_WW1
 #define CT_FP_WW1 4              // warp patch width at one lane per ray
@@ -112,6 +111,12 @@ __device__ __forceinline__ float march_linear(const Geo& geo, const RayF& ry, in
     float sum = 0.0f;
   };
   auto value = [&](Chain& ch, const Cell& c) -> float {
+    if (OCT == GL_OCTB) {
+      const unsigned idx = geo.template oct_cell<WRAP>(c);
+      if (idx != ch.prev) ld_cell(geo.qraw + 2 * (size_t)idx, ch.pa, ch.pb);
+      ch.prev = idx;
+      return trilinear_eval(ch.pa, ch.pb, c.w0, c.w1, c.w2);
+    }
     if (OCT == GL_OCT) {
       const unsigned idx = geo.template gather_index<WRAP>(c);
       // signed: the cylindrical r bits make the first cell's index -1 (kRMagic)
@@ -453,6 +458,8 @@ int launch_fp(const Geo& geo, const ct_ray_view* views, const ct_batch& b, const
     fp_kernel<Geo, EPI, true, GL_PLAIN><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
   else if (EPI != EPI_ROWMAX && EPI != EPI_ROWCOUNT && geo.oct && geo.quad)
     fp_kernel<Geo, EPI, false, GL_QUAD><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
+  else if (EPI != EPI_ROWMAX && EPI != EPI_ROWCOUNT && geo.oct && geo.obrick)
+    fp_kernel<Geo, EPI, false, GL_OCTB><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
   else if (EPI != EPI_ROWMAX && EPI != EPI_ROWCOUNT && geo.oct)
   {
     if (32.0 * geo.cells_layer <= CT_FP_SMALL_LAYER_BYTES)
@@ -473,6 +480,7 @@ int launch_fp(const Geo& geo, const ct_ray_view* views, const ct_batch& b, const
 // ---------------------------------------------------------------------------
 // one h-layer (blockIdx.y = kc) per grid row; cells past the layer's rows are
 // the stride padding (zeroed, never read)
+template <bool BRICK>
 __global__ void pack_gather_cyl_kernel(const float* __restrict__ mu, int nh, int nt, int nr,
                                        unsigned ks, unsigned js, float4* __restrict__ oct) {
   // cells (kc, jc, ic), kc in [0, nh], jc in [0, nt], ic in [0, nr]: corner
@@ -483,7 +491,9 @@ __global__ void pack_gather_cyl_kernel(const float* __restrict__ mu, int nh, int
   if (rem >= (unsigned)(nt + 1) * nc) return;
   const int kc = blockIdx.y;
   const int jc = (int)(rem / nc), ic = (int)(rem % nc);
-  const size_t m = (size_t)kc * ks + (size_t)jc * js + ic;
+  const size_t m = BRICK ? (size_t)oct_brick_index((unsigned)kc, (unsigned)jc, (unsigned)ic,
+                                                   ((unsigned)nt + 2u) / 2u, (nc + 1u) / 2u)
+                         : (size_t)kc * ks + (size_t)jc * js + ic;
   const int i = max(ic - 1, 0), i1 = min(ic, nr - 1);
   const int k = max(kc - 1, 0), k1 = min(kc, nh - 1);
   const int j = (jc == 0) ? nt - 1 : jc - 1, j1 = (jc == nt) ? 0 : jc;
@@ -495,6 +505,7 @@ __global__ void pack_gather_cyl_kernel(const float* __restrict__ mu, int nh, int
   oct[2 * m + 1] = cb;
 }
 
+template <bool BRICK>
 __global__ void pack_gather_cart_kernel(const float* __restrict__ mu, int nz, int ny, int nx,
                                         unsigned ks, unsigned js, float4* __restrict__ oct) {
   // cells (kc, jc, ic) in [0, n] per axis: corner (kc-1, jc-1, ic-1)
@@ -503,7 +514,9 @@ __global__ void pack_gather_cart_kernel(const float* __restrict__ mu, int nz, in
   if (rem >= (unsigned)(ny + 1) * nc) return;
   const int kc = blockIdx.y;
   const int jc = (int)(rem / nc), ic = (int)(rem % nc);
-  const size_t m = (size_t)kc * ks + (size_t)jc * js + ic;
+  const size_t m = BRICK ? (size_t)oct_brick_index((unsigned)kc, (unsigned)jc, (unsigned)ic,
+                                                   ((unsigned)ny + 2u) / 2u, (nc + 1u) / 2u)
+                         : (size_t)kc * ks + (size_t)jc * js + ic;
   const int i = max(ic - 1, 0), i1 = min(ic, nx - 1);
   const int j = max(jc - 1, 0), j1 = min(jc, ny - 1);
   const int k = max(kc - 1, 0), k1 = min(kc, nz - 1);
@@ -570,6 +583,9 @@ int64_t quad_brick_floats(int64_t layers, int64_t rows, int64_t cols) {
 int64_t gather_floats_cyl(const ct_cyl_grid& g) {
   if (CT_QUAD_BRICK && gather_quad(cells_layer_cyl(g)))
     return quad_brick_floats(g.n_h + 2, CylGeo::gather_rows(g.n_theta), g.n_r + 1);
+  if (gather_obrick(cells_layer_cyl(g)))
+    return 32 * (int64_t)(g.n_h + 1) * ((CylGeo::gather_rows(g.n_theta) + 1) / 2) *
+           ((g.n_r + 2) / 2);
   const unsigned ks = gather_strides_cyl(g).ks;
   return gather_quad(cells_layer_cyl(g)) ? 4 * (int64_t)(g.n_h + 2) * ks
                                          : 8 * (int64_t)(g.n_h + 1) * ks;
@@ -577,6 +593,8 @@ int64_t gather_floats_cyl(const ct_cyl_grid& g) {
 int64_t gather_floats_cart(const ct_cart_grid& g) {
   if (CT_QUAD_BRICK && gather_quad(cells_layer_cart(g)))
     return quad_brick_floats(g.n_z + 2, g.n_y + 1, g.n_x + 1);
+  if (gather_obrick(cells_layer_cart(g)))
+    return 32 * (int64_t)(g.n_z + 1) * ((g.n_y + 2) / 2) * ((g.n_x + 2) / 2);
   const unsigned ks = gather_strides_cart(g).ks;
   return gather_quad(cells_layer_cart(g)) ? 4 * (int64_t)(g.n_z + 2) * ks
                                           : 8 * (int64_t)(g.n_z + 1) * ks;
@@ -856,8 +874,12 @@ int ct_pack_gather_cyl(const float* mu, const ct_cyl_grid* grid, float* gather,
         mu, grid->n_h, grid->n_theta, grid->n_r, cs.ks, cs.js, reinterpret_cast<float4*>(gather));
     return check_launch("pack_vquad_kernel");
   }
-  pack_gather_cyl_kernel<<<dim3(nb, grid->n_h + 1), 256, 0, CT_STREAM(stream)>>>(
-      mu, grid->n_h, grid->n_theta, grid->n_r, cs.ks, cs.js, reinterpret_cast<float4*>(gather));
+  if (gather_obrick(cells))
+    pack_gather_cyl_kernel<true><<<dim3(nb, grid->n_h + 1), 256, 0, CT_STREAM(stream)>>>(
+        mu, grid->n_h, grid->n_theta, grid->n_r, cs.ks, cs.js, reinterpret_cast<float4*>(gather));
+  else
+    pack_gather_cyl_kernel<false><<<dim3(nb, grid->n_h + 1), 256, 0, CT_STREAM(stream)>>>(
+        mu, grid->n_h, grid->n_theta, grid->n_r, cs.ks, cs.js, reinterpret_cast<float4*>(gather));
   return check_launch("pack_gather_cyl_kernel");
 }
 
@@ -881,8 +903,12 @@ int ct_pack_gather_cart(const float* mu, const ct_cart_grid* grid, float* gather
         mu, grid->n_z, grid->n_y, grid->n_x, cs.ks, cs.js, reinterpret_cast<float4*>(gather));
     return check_launch("pack_vquad_kernel");
   }
-  pack_gather_cart_kernel<<<dim3(nb, grid->n_z + 1), 256, 0, CT_STREAM(stream)>>>(
-      mu, grid->n_z, grid->n_y, grid->n_x, cs.ks, cs.js, reinterpret_cast<float4*>(gather));
+  if (gather_obrick(cells))
+    pack_gather_cart_kernel<true><<<dim3(nb, grid->n_z + 1), 256, 0, CT_STREAM(stream)>>>(
+        mu, grid->n_z, grid->n_y, grid->n_x, cs.ks, cs.js, reinterpret_cast<float4*>(gather));
+  else
+    pack_gather_cart_kernel<false><<<dim3(nb, grid->n_z + 1), 256, 0, CT_STREAM(stream)>>>(
+        mu, grid->n_z, grid->n_y, grid->n_x, cs.ks, cs.js, reinterpret_cast<float4*>(gather));
   return check_launch("pack_gather_cart_kernel");
 }
 

@@ -365,15 +365,17 @@ def test_deferred_residual_cartesian_and_mixed_passes(monkeypatch):
     assert out[0][1][0] > 0 and out[0][1][1] == 0 and out[0][1][3] > 0
 
 
-@pytest.mark.parametrize("quad", ["0", "1"])
+@pytest.mark.parametrize("quad", ["0", "1", "b"])
 @pytest.mark.parametrize("kind", ["cyl", "cyl_coarse", "cart"])
 def test_gather_layout_matches_plain_path(rng, kind, quad, monkeypatch):
-    """The gather layouts (GL_OCT: 32-byte polynomial cells; GL_QUAD: 16-byte
-    per-layer bilinear cells, forced with CT_GATHER_QUAD=1) change the loads,
-    not the result: bit-identical to the plain path.  cyl_coarse (2x4x2 cells)
-    puts many samples into the first cell of the layout (bottom h halo, theta
-    row 0, axis r halo), whose index is -1 with the r floor magic."""
-    monkeypatch.setenv("CT_GATHER_QUAD", quad)
+    """The gather layouts (GL_OCT: 32-byte polynomial cells; GL_OCTB: the same
+    in 2x2 bricks, forced with CT_GATHER_OBRICK=1; GL_QUAD: 16-byte per-layer
+    bilinear cells in 2x2x2 bricks, forced with CT_GATHER_QUAD=1) change the
+    loads, not the result: bit-identical to the plain path.  cyl_coarse (2x4x2
+    cells) puts many samples into the first cell of the layout (bottom h halo,
+    theta row 0, axis r halo), whose index is -1 with the r floor magic."""
+    monkeypatch.setenv("CT_GATHER_QUAD", "1" if quad == "1" else "0")
+    monkeypatch.setenv("CT_GATHER_OBRICK", "1" if quad == "b" else "0")
     import ctypes as C
     import torch
     from paper_2005_11976_b200 import _device as D, _native as N
@@ -449,9 +451,11 @@ def test_quad_layout_sart_bit_identical(small_cyl_setup, monkeypatch):
     grid, vol, ps = small_cyl_setup
     cfg = SartConfig(n_iterations=2, n_subsets=3, relaxation=0.6)
     out = []
-    for quad in ("0", "1"):
+    for quad, obrick in (("0", "0"), ("1", "0"), ("0", "1")):
         monkeypatch.setenv("CT_GATHER_QUAD", quad)
+        monkeypatch.setenv("CT_GATHER_OBRICK", obrick)
         v, r = sart_run(ps, grid, cfg)
         out.append((v.mu, r.residuals))
-    assert np.array_equal(out[0][0], out[1][0])
-    assert out[0][1] == out[1][1]
+    for o in out[1:]:
+        assert np.array_equal(out[0][0], o[0])
+        assert out[0][1] == o[1]
