@@ -406,11 +406,20 @@ __device__ __forceinline__ ptrdiff_t cell_off(unsigned idx) {
 #ifndef CT_QUAD_BRICK
 #define CT_QUAD_BRICK 1
 #endif
+#ifndef CT_QB_LK
+#define CT_QB_LK 1               // log2 layers per GL_QUAD brick
+#endif
+#ifndef CT_QB_LJ
+#define CT_QB_LJ 1               // log2 rows per GL_QUAD brick (columns: the rest of 8 cells)
+#endif
+constexpr unsigned QB_LK = CT_QB_LK, QB_LJ = CT_QB_LJ, QB_LI = 3 - CT_QB_LK - CT_QB_LJ;
+__host__ __device__ inline unsigned qbricks(unsigned n, unsigned l) { return (n + (1u << l) - 1u) >> l; }
 __host__ __device__ __forceinline__ unsigned quad_brick_index(unsigned kc, unsigned jc,
                                                               unsigned ic, unsigned jbr,
                                                               unsigned ibr) {
-  return ((((kc >> 1) * jbr + (jc >> 1)) * ibr + (ic >> 1)) << 3) | ((kc & 1u) << 2) |
-         ((jc & 1u) << 1) | (ic & 1u);
+  return ((((kc >> QB_LK) * jbr + (jc >> QB_LJ)) * ibr + (ic >> QB_LI)) << 3) |
+         ((kc & ((1u << QB_LK) - 1u)) << (QB_LJ + QB_LI)) |
+         ((jc & ((1u << QB_LJ) - 1u)) << QB_LI) | (ic & ((1u << QB_LI) - 1u));
 }
 // GL_OCTB: GL_OCT cells in 2x2 (row, column) bricks per layer, one 128-byte
 // line each (gather_obrick)
@@ -473,7 +482,8 @@ struct CylGeo {
   unsigned cell_kstride, cell_jstride, jb_wrap, cell_lj, cell_lk;
   double cells_layer;   // real cells per layer (rows x columns)
   const float4* __restrict__ qraw;   // GL_QUAD bricked layout (CT_QUAD_BRICK)
-  unsigned brick_j, brick_i;         // bricks per layer pair: rows / 2, columns / 2
+  unsigned brick_j, brick_i;         // GL_OCTB bricks per layer: rows / 2, columns / 2
+  unsigned qbrick_j, qbrick_i;       // GL_QUAD bricks per layer pair
 
   __host__ void init(const float* m, const float* gather, const ct_cyl_grid& g) {
     mu = m;
@@ -503,6 +513,8 @@ struct CylGeo {
     qraw = reinterpret_cast<const float4*>(gather);
     brick_j = ((unsigned)gather_rows(g.n_theta) + 1u) / 2u;
     brick_i = ((unsigned)g.n_r + 2u) / 2u;
+    qbrick_j = qbricks((unsigned)gather_rows(g.n_theta), QB_LJ);
+    qbrick_i = qbricks((unsigned)g.n_r + 1u, QB_LI);
     jb_wrap = B + (unsigned)g.n_theta;
   }
   // theta rows of the gather layout: indices -1 .. n_theta - 1 (see RayF)
@@ -666,7 +678,7 @@ struct CylGeo {
   __device__ __forceinline__ unsigned quad_cell(const Cell& c, unsigned dk) const {
     const unsigned jb = (WRAP && c.jb > jb_wrap) ? c.jb - (unsigned)nt : c.jb;
     return quad_brick_index(c.kb - kMagicBits + dk, jb - kMagicBits, c.ib - kMagicBits + 1u,
-                            brick_j, brick_i);
+                            qbrick_j, qbrick_i);
   }
   template <bool WRAP>
   __device__ __forceinline__ unsigned oct_cell(const Cell& c) const {
@@ -715,7 +727,7 @@ struct CartGeo {
   unsigned cell_lj, cell_lk;
   double cells_layer;
   const float4* __restrict__ qraw;
-  unsigned brick_j, brick_i;
+  unsigned brick_j, brick_i, qbrick_j, qbrick_i;
 
   __host__ void init(const float* m, const float* gather, const ct_cart_grid& g) {
     mu = m;
@@ -742,6 +754,8 @@ struct CartGeo {
     qraw = reinterpret_cast<const float4*>(gather);
     brick_j = ((unsigned)ny + 2u) / 2u;
     brick_i = ((unsigned)nx + 2u) / 2u;
+    qbrick_j = qbricks((unsigned)ny + 1u, QB_LJ);
+    qbrick_i = qbricks((unsigned)nx + 1u, QB_LI);
   }
 
   // _kernels.py:207-231
@@ -845,7 +859,7 @@ struct CartGeo {
   template <bool WRAP>
   __device__ __forceinline__ unsigned quad_cell(const Cell& c, unsigned dk) const {
     return quad_brick_index(c.kb - kMagicBits + dk, c.jb - kMagicBits, c.ib - kMagicBits,
-                            brick_j, brick_i);
+                            qbrick_j, qbrick_i);
   }
   template <bool WRAP>
   __device__ __forceinline__ unsigned oct_cell(const Cell& c) const {

@@ -543,7 +543,7 @@ __global__ void pack_vquad_kernel(const float* __restrict__ mu, int nk, int nj, 
   const int jc = (int)(rem / nc), ic = (int)(rem % nc);
 #if CT_QUAD_BRICK
   const size_t m = quad_brick_index((unsigned)kc, (unsigned)jc, (unsigned)ic,
-                                    ((unsigned)nj + 2u) / 2u, (nc + 1u) / 2u);
+                                    qbricks((unsigned)nj + 1u, QB_LJ), qbricks(nc, QB_LI));
 #else
   const size_t m = (size_t)kc * ks + (size_t)jc * js + ic;
 #endif
@@ -578,7 +578,8 @@ double cells_layer_cart(const ct_cart_grid& g) { return (double)(g.n_y + 1) * (g
 // gather buffer length in floats: (n+1) layers x 8 floats, or GL_QUAD (n+2) x 4
 // bricked GL_QUAD: ceil(layers/2) x ceil(rows/2) x ceil(cols/2) bricks of 8 cells
 int64_t quad_brick_floats(int64_t layers, int64_t rows, int64_t cols) {
-  return 32 * ((layers + 1) / 2) * ((rows + 1) / 2) * ((cols + 1) / 2);
+  return 32 * (int64_t)qbricks((unsigned)layers, QB_LK) * (int64_t)qbricks((unsigned)rows, QB_LJ) *
+         (int64_t)qbricks((unsigned)cols, QB_LI);
 }
 int64_t gather_floats_cyl(const ct_cyl_grid& g) {
   if (CT_QUAD_BRICK && gather_quad(cells_layer_cyl(g)))
