@@ -359,46 +359,16 @@ __host__ __device__ inline unsigned gather_layer_stride(unsigned rows, unsigned 
   return ks + (256u - (ks + js + 1u) % 256u) % 256u;
 }
 
-// CT_POW2_CELLS (A/B): power-of-two row and layer strides (js >= 256), so the
-// cell index is (kb << lk) + (jb << lj) + ib on the ALU pipe instead of two
-// IMADs on the FMA pipe; the magic bias then leaves a constant B (B << l == 0
-// mod 2^32 for l >= 8), folded into the base pointer.  Memory: up to 4x the
-// cells (padding is never written or read).
-#ifndef CT_POW2_CELLS
-#define CT_POW2_CELLS 0
-#endif
 struct CellStrides {
-  unsigned js, ks, lj, lk;
+  unsigned js, ks;
 };
-__host__ __device__ inline unsigned ct_next_pow2(unsigned x) {
-  unsigned p = 1;
-  while (p < x) p <<= 1;
-  return p;
-}
-__host__ __device__ inline unsigned ct_ilog2(unsigned x) {
-  unsigned l = 0;
-  while ((1u << l) < x) ++l;
-  return l;
-}
 // gather-layout base pointer for gather_index's cell numbers: `one_on` cells
-// on (the cylindrical r floor bits carry index - 1), and B cells back with
-// CT_POW2_CELLS (the index then carries the bias B; u32 index + B < 2^31)
+// on (the cylindrical r floor bits carry index - 1)
 __host__ inline const float4* cell_base(const float* gather, bool quad, int one_on) {
-  const uintptr_t cb = quad ? 16u : 32u;
-  uintptr_t p = reinterpret_cast<uintptr_t>(gather) + cb * (uintptr_t)one_on;
-#if CT_POW2_CELLS
-  p -= cb * (uintptr_t)kMagicBits;
-#endif
-  return reinterpret_cast<const float4*>(p);
+  return reinterpret_cast<const float4*>(gather) + (quad ? 1 : 2) * one_on;
 }
-// signed cell offset of a gather_index value
-__device__ __forceinline__ ptrdiff_t cell_off(unsigned idx) {
-#if CT_POW2_CELLS
-  return (ptrdiff_t)(size_t)idx;
-#else
-  return (ptrdiff_t)(int)idx;   // the first cylindrical cell is -1
-#endif
-}
+// signed cell offset of a gather_index value (the first cylindrical cell is -1)
+__device__ __forceinline__ ptrdiff_t cell_off(unsigned idx) { return (ptrdiff_t)(int)idx; }
 // CT_QUAD_BRICK: GL_QUAD cells stored in 2x2x2 (layer, row, column) bricks,
 // one 128-byte line each: the two layers of a trilinear cell share a line for
 // even layers, and neighbouring rays' cells share lines in theta as well as r
@@ -431,16 +401,8 @@ __host__ __device__ __forceinline__ unsigned oct_brick_index(unsigned kc, unsign
 // rows x ncols real cells per layer
 __host__ __device__ inline CellStrides cell_strides(unsigned rows, unsigned ncols) {
   CellStrides c;
-#if CT_POW2_CELLS
-  c.js = ct_next_pow2(ncols < 256u ? 256u : ncols);
-  c.ks = ct_next_pow2(rows * c.js);
-  c.lj = ct_ilog2(c.js);
-  c.lk = ct_ilog2(c.ks);
-#else
   c.js = ncols;
   c.ks = gather_layer_stride(rows, ncols);
-  c.lj = c.lk = 0;
-#endif
   return c;
 }
 
@@ -479,7 +441,7 @@ struct CylGeo {
   float inv_dr, inv_dth, inv_dh, h_off, h_off1, nr_m1, nh_m1;
   float tc[8];   // 2 atan polynomial coefficients times n_theta / (2 pi)
   // gather layout: cells (nh+1, nt+1, nr+1), strides (ks, js, 1)
-  unsigned cell_kstride, cell_jstride, jb_wrap, cell_lj, cell_lk;
+  unsigned cell_kstride, cell_jstride, jb_wrap;
   double cells_layer;   // real cells per layer (rows x columns)
   const float4* __restrict__ qraw;   // GL_QUAD bricked layout (CT_QUAD_BRICK)
   unsigned brick_j, brick_i;         // GL_OCTB bricks per layer: rows / 2, columns / 2
@@ -502,13 +464,10 @@ struct CylGeo {
     const CellStrides cs = cell_strides((unsigned)gather_rows(g.n_theta), (unsigned)g.n_r + 1u);
     cell_jstride = cs.js;
     cell_kstride = cs.ks;
-    cell_lj = cs.lj;
-    cell_lk = cs.lk;
     cells_layer = (double)gather_rows(g.n_theta) * (g.n_r + 1);
     quad = gather_quad(cells_layer);
     obrick = gather_obrick(cells_layer);
     // the r floor bits carry index - 1 (kRMagic): the base is one cell on
-    // (CT_POW2_CELLS: and B cells back, see cell_strides)
     oct = gather ? cell_base(gather, quad, 1) : nullptr;
     qraw = reinterpret_cast<const float4*>(gather);
     brick_j = ((unsigned)gather_rows(g.n_theta) + 1u) / 2u;
@@ -666,11 +625,7 @@ struct CylGeo {
     // WRAP (rays crossing theta = 2 pi): rows past n_theta wrap onto the
     // primary rows (integer ops)
     const unsigned jb = (WRAP && c.jb > jb_wrap) ? c.jb - (unsigned)nt : c.jb;
-#if CT_POW2_CELLS
-    return (c.kb << cell_lk) + (jb << cell_lj) + c.ib;
-#else
     return c.kb * cell_kstride + jb * cell_jstride + c.ib;
-#endif
   }
 
   // bricked GL_QUAD cell of layer kc + dk (the r floor bits carry index - 1)
@@ -724,7 +679,6 @@ struct CartGeo {
   double vs, lo[3], hi[3];
   float inv_vs, off[3], off1[3], nx_m1, ny_m1, nz_m1;
   unsigned cell_kstride, cell_jstride;   // gather layout (nz+1, ny+1, nx+1), strides (ks, js, 1)
-  unsigned cell_lj, cell_lk;
   double cells_layer;
   const float4* __restrict__ qraw;
   unsigned brick_j, brick_i, qbrick_j, qbrick_i;
@@ -745,8 +699,6 @@ struct CartGeo {
     const CellStrides cs = cell_strides((unsigned)ny + 1u, (unsigned)nx + 1u);
     cell_jstride = cs.js;
     cell_kstride = cs.ks;
-    cell_lj = cs.lj;
-    cell_lk = cs.lk;
     cells_layer = (double)(ny + 1) * (nx + 1);
     quad = gather_quad(cells_layer);
     obrick = gather_obrick(cells_layer);
@@ -850,11 +802,7 @@ struct CartGeo {
 
   template <bool WRAP>
   __device__ __forceinline__ unsigned gather_index(const Cell& c) const {
-#if CT_POW2_CELLS
-    return (c.kb << cell_lk) + (c.jb << cell_lj) + c.ib;
-#else
     return c.kb * cell_kstride + c.jb * cell_jstride + c.ib;
-#endif
   }
   template <bool WRAP>
   __device__ __forceinline__ unsigned quad_cell(const Cell& c, unsigned dk) const {

@@ -864,8 +864,6 @@ int ct_pack_gather_cyl(const float* mu, const ct_cyl_grid* grid, float* gather,
   if (grid->n_h + 2 > 65535) return set_err(CT_ERR_ARG, "gather layout: n_h + 2 > 65535");
   const CellStrides cs = gather_strides_cyl(*grid);
   const double cells = cells_layer_cyl(*grid);
-  if (CT_POW2_CELLS && (double)(grid->n_h + 2) * cs.ks + kMagicBits >= 2147483648.0)
-    return set_err(CT_ERR_ARG, "gather layout too large for power-of-two strides");
   if (CT_QUAD_BRICK && gather_quad(cells) &&
       quad_brick_floats(grid->n_h + 2, grid->n_theta + 1, grid->n_r + 1) / 4 >= 2147483648LL)
     return set_err(CT_ERR_ARG, "gather layout too large for 32-bit brick indices");
@@ -893,8 +891,6 @@ int ct_pack_gather_cart(const float* mu, const ct_cart_grid* grid, float* gather
   if (grid->n_z + 2 > 65535) return set_err(CT_ERR_ARG, "gather layout: n_z + 2 > 65535");
   const CellStrides cs = gather_strides_cart(*grid);
   const double cells = cells_layer_cart(*grid);
-  if (CT_POW2_CELLS && (double)(grid->n_z + 2) * cs.ks + kMagicBits >= 2147483648.0)
-    return set_err(CT_ERR_ARG, "gather layout too large for power-of-two strides");
   if (CT_QUAD_BRICK && gather_quad(cells) &&
       quad_brick_floats(grid->n_z + 2, grid->n_y + 1, grid->n_x + 1) / 4 >= 2147483648LL)
     return set_err(CT_ERR_ARG, "gather layout too large for 32-bit brick indices");
