@@ -275,6 +275,10 @@ __global__ void __launch_bounds__(BP_THREADS, BP_MIN_BLOCKS) bp_kernel(const __g
         const unsigned oa = tv.x * (unsigned)a.cols + tu.x + co.x;
         const unsigned ob = tv.y * (unsigned)a.cols + tu.y + co.y;
         if (QUADS) {
+#if defined(CT_DEBUG_BOUNDS) && CT_DEBUG_BOUNDS
+          assert((long long)oa < (long long)a.n_batch * npix &&
+                 (long long)ob < (long long)a.n_batch * npix);
+#endif
           // one 16-byte footprint per view; lerp-form bilinear per lane
           const float4 qa = ld_quad(a.quads + oa), qb = ld_quad(a.quads + ob);
           float fua, fub, fva, fvb;

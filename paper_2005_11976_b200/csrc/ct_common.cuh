@@ -26,6 +26,7 @@
 #include "cyltomo_b200.h"
 
 #include <cuda_runtime.h>
+#include <cassert>
 #include <limits.h>
 #include <math.h>
 #include <stdint.h>
@@ -435,6 +436,7 @@ struct CylGeo {
   const float4* __restrict__ oct;  // gather layout (ct_pack_gather_cyl) or null
   bool quad;                       // oct holds GL_QUAD corner quads
   bool obrick;                     // oct holds GL_OCTB bricked 32-byte cells
+  long long dbg_floats = 0;        // CT_DEBUG_BOUNDS: gather buffer length (floats)
   int nh, nt, nr;
   double radius, half_h;
   // fp32 sampling constants
@@ -675,6 +677,7 @@ struct CartGeo {
   const float4* __restrict__ oct;  // gather layout (ct_pack_gather_cart) or null
   bool quad;                       // oct holds GL_QUAD corner quads
   bool obrick;                     // oct holds GL_OCTB bricked 32-byte cells
+  long long dbg_floats = 0;        // CT_DEBUG_BOUNDS: gather buffer length (floats)
   int nz, ny, nx;
   double vs, lo[3], hi[3];
   float inv_vs, off[3], off1[3], nx_m1, ny_m1, nz_m1;

@@ -22,6 +22,9 @@ enum FpEpi { EPI_PROJECT = 0, EPI_CORR = 1, EPI_RESID = 2, EPI_ROWMAX = 3, EPI_C
 enum FpLayout { GL_PLAIN = 0, GL_OCT = 1, GL_QUAD = 2, GL_OCTB = 3 };
 
 // block = FP_WX x FP_WY warps, each warp a pixel patch (tile_ww x tile_wh rays)
+#ifndef CT_DEBUG_BOUNDS
+#define CT_DEBUG_BOUNDS 0        // device asserts on every gather-layout cell address (tests)
+#endif
 #ifndef CT_FP_WX
 #define CT_FP_WX 4
 #endif
@@ -113,12 +116,21 @@ __device__ __forceinline__ float march_linear(const Geo& geo, const RayF& ry, in
   auto value = [&](Chain& ch, const Cell& c) -> float {
     if (OCT == GL_OCTB) {
       const unsigned idx = geo.template oct_cell<WRAP>(c);
+#if CT_DEBUG_BOUNDS
+      assert(8LL * ((long long)idx + 1) <= geo.dbg_floats);
+#endif
       if (idx != ch.prev) ld_cell(geo.qraw + 2 * (size_t)idx, ch.pa, ch.pb);
       ch.prev = idx;
       return trilinear_eval(ch.pa, ch.pb, c.w0, c.w1, c.w2);
     }
     if (OCT == GL_OCT) {
       const unsigned idx = geo.template gather_index<WRAP>(c);
+#if CT_DEBUG_BOUNDS
+      {
+        const long long cell = (long long)(geo.oct - geo.qraw) / 2 + cell_off(idx);
+        assert(cell >= 0 && 8LL * (cell + 1) <= geo.dbg_floats);
+      }
+#endif
       // signed: the cylindrical r bits make the first cell's index -1 (kRMagic)
       if (idx != ch.prev) ld_cell(geo.oct + 2 * cell_off(idx), ch.pa, ch.pb);
       ch.prev = idx;   // (unconditional: equal when not reloaded; no predicated move)
@@ -129,6 +141,10 @@ __device__ __forceinline__ float march_linear(const Geo& geo, const RayF& ry, in
       // difference (two f32x2 subtractions)
 #if CT_QUAD_BRICK
       const unsigned idx = geo.template quad_cell<WRAP>(c, 0u);
+#if CT_DEBUG_BOUNDS
+      assert(4LL * ((long long)geo.template quad_cell<WRAP>(c, 1u) + 1) <= geo.dbg_floats &&
+             4LL * ((long long)idx + 1) <= geo.dbg_floats);
+#endif
       if (idx != ch.prev) {
         const float4 a = ld_vquad(geo.qraw + idx);
         const float4 b = ld_vquad(geo.qraw + geo.template quad_cell<WRAP>(c, 1u));
@@ -432,16 +448,35 @@ int check_batch(const ct_batch* b, const void* views, const ct_sampling* s) {
   return CT_OK;
 }
 
+int64_t gather_floats_cyl(const ct_cyl_grid& g);
+int64_t gather_floats_cart(const ct_cart_grid& g);
+inline int64_t gather_floats_of(const CylGeo& g) {
+  ct_cyl_grid c{};
+  c.n_h = g.nh; c.n_theta = g.nt; c.n_r = g.nr;
+  return gather_floats_cyl(c);
+}
+inline int64_t gather_floats_of(const CartGeo& g) {
+  ct_cart_grid c{};
+  c.n_z = g.nz; c.n_y = g.ny; c.n_x = g.nx;
+  return gather_floats_cart(c);
+}
+
 template <class Geo, int EPI>
 int launch_fp(const Geo& geo, const ct_ray_view* views, const ct_batch& b, const ct_sampling& s,
               const float* p_meas, const double* thr, float* o0, float* o1, double* red,
               cudaStream_t st, int red_rows = 0, int64_t frow_lo = 0,
               int64_t frow_hi = INT64_MAX) {
   FpArgs<Geo> a;
+#if CT_DEBUG_BOUNDS
+  a.geo = geo;
+  a.geo.dbg_floats = gather_floats_of(geo);
+#endif
   a.red_rows = red_rows;
   a.frow_lo = frow_lo;
   a.frow_hi = frow_hi;
+#if !CT_DEBUG_BOUNDS
   a.geo = geo;
+#endif
   a.views = views;
   a.view_ids = b.view_ids;
   a.rows = b.det_rows;
