@@ -124,7 +124,9 @@ class GpuEngine:
         self.D = D
         self.eng = SartEngine(grid, ps.geom, cfg.sampling)
         self.device = self.eng.device
-        self.p_meas = D.to_device(ps.images, device=self.device)
+        self.ps = ps
+        self.p_meas = None          # upload_rows(): only the rows this rank marches
+        self._row_samples = None
         self.weights = _device_weights(cfg, grid.shape, self.device)
         self.cfg = cfg
         self.gather = self.eng.alloc_gather()
@@ -146,9 +148,26 @@ class GpuEngine:
 
     def row_costs(self, views):
         """FP cost per flattened detector row of a view batch: its in-support
-        samples plus a per-ray setup allowance (~8 samples per pixel)."""
-        return (self.eng.row_samples(np.asarray(views)).ravel().astype(np.float64)
+        samples plus a per-ray setup allowance (~8 samples per pixel).  One
+        count launch for all views, cached."""
+        if self._row_samples is None:
+            self._row_samples = self.eng.row_samples(np.arange(self.ps.geom.n_proj))
+        return (self._row_samples[np.asarray(views)].ravel().astype(np.float64)
                 + 8.0 * self.eng.cols)
+
+    def upload_rows(self, ranges):
+        """Measured projections to the device, only the (view, row range)
+        pieces this rank's FP launches read (the kernels index p_meas by
+        global view and row; other rows are never read).  ranges=None: all."""
+        D, torch = self.D, self.D.torch_mod()
+        imgs = self.ps.images
+        if D.is_device_array(imgs) or ranges is None:
+            self.p_meas = D.to_device(imgs, device=self.device)
+            return
+        host = torch.from_numpy(np.ascontiguousarray(imgs, dtype=np.float32))
+        self.p_meas = torch.empty(tuple(host.shape), dtype=torch.float32, device=self.device)
+        for v, r0, r1 in ranges:
+            self.p_meas[v, r0:r1].copy_(host[v, r0:r1], non_blocking=True)
 
     def scratch(self, n_slots: int):
         torch = self.D.torch_mod()
@@ -240,6 +259,8 @@ class ShardedSartRun:
         rest = np.setdiff1d(np.arange(n_proj), self.subsets[0])
         self.rest = _RowShard(rest, rows, self.rank, self.world, tile, self.e) \
             if len(rest) else None
+        if hasattr(self.e, "upload_rows"):
+            self.e.upload_rows(None if self.world == 1 else self._my_rows())
         self.scratch = self.e.scratch(n_proj)       # this rank's residual slot partials
         self.red = self.e.scratch(n_proj)           # their all-reduced copy
         self.resid = self.e.tensor(cfg.n_iterations, "float64")
@@ -248,6 +269,16 @@ class ShardedSartRun:
         self._pending = None
         self._packed = False
         self.launch_log = None
+
+    def _my_rows(self):
+        """(view, row0, row1) pieces of the detector this rank's FPs read."""
+        out = []
+        for sh in self.shards + ([self.rest] if self.rest is not None else []):
+            for f0 in range(sh.lo - sh.lo % self.rows, sh.hi, self.rows):
+                a, b = max(f0, sh.lo), min(f0 + self.rows, sh.hi)
+                if b > a:
+                    out.append((int(sh.views[f0 // self.rows]), a - f0, b - f0))
+        return out
 
     # views of subset s this rank marches (tests / accounting)
     @property
