@@ -403,8 +403,7 @@ class _StreamedUpload:
     upload overlaps the first subsets' compute: subset k's views are copied
     (one async copy per view from page-locked memory) while subset k-1
     computes, and the compute stream waits on subset k's event just before
-    its first use.  Only for page-locked host arrays (SartRun uploads pageable
-    ones in one synchronous copy: staging them would cost a host memcpy)."""
+    its first use.  For page-locked host arrays (pageable ones: _StagedUpload)."""
 
     @staticmethod
     def applies(images) -> bool:
@@ -458,6 +457,53 @@ class _StreamedUpload:
         return all(self.waited)
 
 
+_STAGE_POOL = None
+
+
+def _stage_pool():
+    global _STAGE_POOL
+    if _STAGE_POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _STAGE_POOL = ThreadPoolExecutor(max_workers=max(1, min(8, (os.cpu_count() or 2) // 2)))
+    return _STAGE_POOL
+
+
+class _StagedUpload(_StreamedUpload):
+    """Pageable host projections: worker threads copy the views, in subset
+    order, into a page-locked staging array (numpy copies release the GIL, so
+    the host memcpy runs on several cores), and each subset's views go up
+    asynchronously on the copy stream as soon as they are staged -- the
+    staging of view i+1 overlaps the DMA of view i, and both overlap the
+    compute of earlier subsets.  The staging array comes from torch's caching
+    host allocator (reused by the next call)."""
+
+    @staticmethod
+    def applies(images) -> bool:
+        arr = np.asarray(images)
+        return (os.environ.get("CT_STAGED_UPLOAD", "1") != "0" and arr.ndim == 3
+                and arr.dtype == np.float32 and arr.nbytes >= (16 << 20))
+
+    def __init__(self, images, subsets, device):
+        torch = D.torch_mod()
+        src = np.asarray(images)
+        pinned = torch.empty(src.shape, dtype=torch.float32, pin_memory=True)
+        dst = pinned.numpy()
+        pool = _stage_pool()
+        self.futures = {}
+        for sub in subsets:
+            for v in sub:
+                v = int(v)
+                self.futures[v] = pool.submit(np.copyto, dst[v], src[v])
+        super().__init__(dst, subsets, device)
+
+    def issue(self, k: int) -> None:
+        # the subset's views must be staged before their DMA is queued
+        for kk in range(self.issued, min(k, len(self.subsets) - 1) + 1):
+            for v in self.subsets[kk]:
+                self.futures[int(v)].result()
+        super().issue(k)
+
+
 class SartRun:
     """A prepared (OS-)SART reconstruction: tables, thresholds, buffers.
 
@@ -482,12 +528,18 @@ class SartRun:
         self._max_row, self._max_row_ev = self.eng.prepare_thresholds_async()
         self._empty_checked = False
         self.weights = _device_weights(cfg, grid.shape, dev)
-        if ps.on_device or not _StreamedUpload.applies(ps.images):
+        if ps.on_device:
             self._p_meas = D.to_device(ps.images, device=dev)
             self._upload = None
-        else:
+        elif _StreamedUpload.applies(ps.images):
             self._upload = _StreamedUpload(ps.images, self.subsets, dev)
             self._p_meas = self._upload.dev
+        elif _StagedUpload.applies(ps.images):
+            self._upload = _StagedUpload(ps.images, self.subsets, dev)
+            self._p_meas = self._upload.dev
+        else:
+            self._p_meas = D.to_device(ps.images, device=dev)
+            self._upload = None
         self.subset_slots = [D.upload_i32(s) for s in self.subsets]
         self.all_slots = D.upload_i32(np.arange(ps.geom.n_proj))
         nmax = max(len(s) for s in self.subsets)

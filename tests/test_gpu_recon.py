@@ -308,6 +308,30 @@ def test_pinned_host_run_matches_device(small_cyl_setup, n_subsets):
     assert ra.residuals == rb.residuals == rc.residuals
 
 
+@pytest.mark.parametrize("n_subsets", [2, 21])
+def test_staged_pageable_upload_matches_device(small_cyl_setup, monkeypatch, n_subsets):
+    """Pageable host projections staged through page-locked memory by worker
+    threads (recon._StagedUpload, forced here for a small stack) give the
+    device-resident run's bits, eager (2 subsets) and graph-captured (21)."""
+    import torch
+    from paper_2005_11976_b200 import recon as R
+    grid, vol, ps = small_cyl_setup
+    cfg = SartConfig(n_iterations=2, n_subsets=n_subsets, relaxation=0.7)
+    used = []
+    orig = R._StagedUpload.__init__
+
+    def spy(self, *a, **k):
+        used.append(1)
+        orig(self, *a, **k)
+    monkeypatch.setattr(R._StagedUpload, "applies", staticmethod(lambda images: True))
+    monkeypatch.setattr(R._StagedUpload, "__init__", spy)
+    a, ra = sart_run(ps, grid, cfg)                       # pageable host arrays
+    assert used
+    b, rb = sart_run(ProjectionSet(ps.geom, torch.as_tensor(ps.images, device="cuda")), grid, cfg)
+    assert np.array_equal(a.mu, b.mu.cpu().numpy())
+    assert ra.residuals == rb.residuals
+
+
 def test_graph_replay_bit_identical(small_cyl_setup):
     """A pass captured as a CUDA graph replays the same kernels: same bits."""
     from paper_2005_11976_b200.recon import SartRun
