@@ -448,6 +448,7 @@ int check_batch(const ct_batch* b, const void* views, const ct_sampling* s) {
   return CT_OK;
 }
 
+#if CT_DEBUG_BOUNDS
 int64_t gather_floats_cyl(const ct_cyl_grid& g);
 int64_t gather_floats_cart(const ct_cart_grid& g);
 inline int64_t gather_floats_of(const CylGeo& g) {
@@ -460,6 +461,7 @@ inline int64_t gather_floats_of(const CartGeo& g) {
   c.n_z = g.nz; c.n_y = g.ny; c.n_x = g.nx;
   return gather_floats_cart(c);
 }
+#endif
 
 template <class Geo, int EPI>
 int launch_fp(const Geo& geo, const ct_ray_view* views, const ct_batch& b, const ct_sampling& s,
