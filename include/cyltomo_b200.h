@@ -91,6 +91,14 @@ typedef struct ct_update {
     int32_t nonneg;
     const float *weights;
     float *mu;
+    /* (ABI v6) peer-store all-gather fused into the update: when n_peers > 0,
+     * every updated voxel is also stored into each of the n_peers replica
+     * volumes mu_peers[p] (device array of device pointers, e.g. the
+     * symmetric-memory buffers of the ranks, NVLink P2P stores) instead of
+     * only into mu. */
+    float *const *mu_peers;
+    int32_t n_peers;
+    int32_t _pad;
 } ct_update;
 
 /* Detector / batch description shared by the batched calls:
@@ -171,7 +179,10 @@ int ct_fp_cart_residual(const float *mu, const float *gather, const ct_cart_grid
  *  - ct_fp_*_correction_rows: the correction epilogue of ct_fp_*_correction;
  *    with a scratch also the residual partials of the same simulation (the
  *    residual FP of pass k and the first subset's correction FP of pass k+1
- *    read the same mu, recon.py:171-181 / PAPER.md:182-187);
+ *    read the same mu, recon.py:171-181 / PAPER.md:182-187); with
+ *    n_peers > 0 each correction is stored at corr_peers[p][peer_offset +
+ *    (f - row_lo) * det_cols + col] for every p instead of into corr (the
+ *    all-gather of the corrections fused into the FP: NVLink P2P stores);
  *  - ct_fp_*_residual_rows: residual partials only (no sum);
  *  - ct_residual_sum: *accum += fixed-order sum of scratch[0..n);
  *  - ct_fp_row_tile: rows per FP block for this detector. */
@@ -180,12 +191,16 @@ int ct_fp_cyl_correction_rows(const float *mu, const float *gather, const ct_cyl
                               const ct_ray_view *views, const ct_batch *batch,
                               const ct_sampling *sampling, const float *p_meas,
                               const double *row_thr, float *corr, int64_t row_lo,
-                              int64_t row_hi, int n_slots, double *scratch, ct_stream_t stream);
+                              int64_t row_hi, int n_slots, double *scratch,
+                              float *const *corr_peers, int n_peers, int64_t peer_offset,
+                              ct_stream_t stream);
 int ct_fp_cart_correction_rows(const float *mu, const float *gather, const ct_cart_grid *grid,
                                const ct_ray_view *views, const ct_batch *batch,
                                const ct_sampling *sampling, const float *p_meas,
                                const double *row_thr, float *corr, int64_t row_lo,
-                               int64_t row_hi, int n_slots, double *scratch, ct_stream_t stream);
+                               int64_t row_hi, int n_slots, double *scratch,
+                               float *const *corr_peers, int n_peers, int64_t peer_offset,
+                               ct_stream_t stream);
 int ct_fp_cyl_residual_rows(const float *mu, const float *gather, const ct_cyl_grid *grid,
                             const ct_ray_view *views, const ct_batch *batch,
                             const ct_sampling *sampling, const float *p_meas, int64_t row_lo,

@@ -51,7 +51,8 @@ class SamplingC(C.Structure):
 
 class UpdateC(C.Structure):
     _fields_ = [("relaxation", C.c_float), ("nonneg", C.c_int32),
-                ("weights", C.c_void_p), ("mu", C.c_void_p)]
+                ("weights", C.c_void_p), ("mu", C.c_void_p),
+                ("mu_peers", C.c_void_p), ("n_peers", C.c_int32), ("_pad", C.c_int32)]
 
 
 class BatchC(C.Structure):
@@ -80,10 +81,10 @@ _SIGNATURES = {
     "ct_fp_row_tile": (C.c_int, [C.POINTER(BatchC)]),
     "ct_fp_cyl_correction_rows": (C.c_int, [P, P, C.POINTER(CylGridC), P, C.POINTER(BatchC),
                                             C.POINTER(SamplingC), P, P, P, C.c_int64,
-                                            C.c_int64, C.c_int, P, P]),
+                                            C.c_int64, C.c_int, P, P, C.c_int, C.c_int64, P]),
     "ct_fp_cart_correction_rows": (C.c_int, [P, P, C.POINTER(CartGridC), P, C.POINTER(BatchC),
                                              C.POINTER(SamplingC), P, P, P, C.c_int64,
-                                             C.c_int64, C.c_int, P, P]),
+                                             C.c_int64, C.c_int, P, P, C.c_int, C.c_int64, P]),
     "ct_fp_cyl_residual_rows": (C.c_int, [P, P, C.POINTER(CylGridC), P, C.POINTER(BatchC),
                                           C.POINTER(SamplingC), P, C.c_int64, C.c_int64,
                                           C.c_int, P, P]),

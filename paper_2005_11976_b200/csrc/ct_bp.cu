@@ -379,7 +379,13 @@ __global__ void __launch_bounds__(BP_THREADS, BP_MIN_BLOCKS) bp_kernel(const __g
       const float delta = (lw * num) / den;
       float mu = a.upd.mu[m] + delta;
       if (a.upd.nonneg) mu = fmaxf(mu, 0.0f);
-      a.upd.mu[m] = mu;
+      if (a.upd.n_peers > 0) {
+        // all-gather of the updated shard fused into the update: every
+        // rank's replica gets the voxel (NVLink peer stores)
+        for (int p = 0; p < a.upd.n_peers; ++p) a.upd.mu_peers[p][m] = mu;
+      } else {
+        a.upd.mu[m] = mu;
+      }
     }
   }
 }

@@ -76,7 +76,23 @@ struct FpArgs {
   // f = b * rows + row in [frow_lo, frow_hi) are marched, and the correction
   // of row f lands at out0[(f - frow_lo) * cols + col].  Defaults: all rows.
   int64_t frow_lo, frow_hi;
+  // peer-store all-gather of the corrections (distributed.py, fused comm):
+  // with n_peers > 0 every correction goes to peers[p][peer_off + out index]
+  float* const* __restrict__ peers;
+  int n_peers;
+  int64_t peer_off;
 };
+
+// A correction value: local output, or (fused all-gather) every rank's copy
+// of the gathered stack over NVLink peer stores.
+template <class Geo>
+__device__ __forceinline__ void store_corr(const FpArgs<Geo>& a, size_t oidx, float c) {
+  if (a.n_peers > 0) {
+    for (int p = 0; p < a.n_peers; ++p) a.peers[p][a.peer_off + (int64_t)oidx] = c;
+  } else {
+    a.out0[oidx] = c;
+  }
+}
 
 // Lanes per ray.  Small detectors cannot fill 148 SMs with one thread per
 // ray, so each ray's samples are split into K contiguous chunks on K adjacent
@@ -371,7 +387,7 @@ __device__ __forceinline__ void fp_body(const FpArgs<Geo>& a) {
         const float pm = a.p_meas[(size_t)vid * npix + pix];
         c = (pm - (float)p64) / (float)w64;
       }
-      a.out0[oidx] = c;
+      store_corr(a, oidx, c);
     }
   } else {
     double x = 0.0;
@@ -382,7 +398,7 @@ __device__ __forceinline__ void fp_body(const FpArgs<Geo>& a) {
         const float pm = a.p_meas[(size_t)vid * npix + pix];
         float c = 0.0f;
         if (w64 > a.row_thr[vid]) c = (pm - (float)p64) / (float)w64;
-        a.out0[oidx] = c;
+        store_corr(a, oidx, c);
         const double r = (double)pm - (double)(float)p64;
         x = r * r;
       } else if (EPI == EPI_RESID) {
@@ -467,8 +483,12 @@ template <class Geo, int EPI>
 int launch_fp(const Geo& geo, const ct_ray_view* views, const ct_batch& b, const ct_sampling& s,
               const float* p_meas, const double* thr, float* o0, float* o1, double* red,
               cudaStream_t st, int red_rows = 0, int64_t frow_lo = 0,
-              int64_t frow_hi = INT64_MAX) {
+              int64_t frow_hi = INT64_MAX, float* const* peers = nullptr, int n_peers = 0,
+              int64_t peer_off = 0) {
   FpArgs<Geo> a;
+  a.peers = peers;
+  a.n_peers = n_peers;
+  a.peer_off = peer_off;
 #if CT_DEBUG_BOUNDS
   a.geo = geo;
   a.geo.dbg_floats = gather_floats_of(geo);
@@ -658,16 +678,20 @@ int check_slots(const ct_batch* batch, int n_slots, const double* scratch) {
 template <class Geo>
 int fp_rows(const Geo& geo, const ct_ray_view* views, const ct_batch* batch,
             const ct_sampling* s, const float* p_meas, const double* row_thr, float* corr,
-            int64_t row_lo, int64_t row_hi, int n_slots, double* scratch, ct_stream_t stream) {
+            int64_t row_lo, int64_t row_hi, int n_slots, double* scratch, ct_stream_t stream,
+            float* const* peers = nullptr, int n_peers = 0, int64_t peer_off = 0) {
   int rc = check_rows(batch, row_lo, row_hi);
   if (rc) return rc;
+  if (n_peers < 0 || (n_peers > 0 && !peers)) return set_err(CT_ERR_ARG, "bad peer list");
   if (corr && !scratch)
     return launch_fp<Geo, EPI_CORR>(geo, views, *batch, *s, p_meas, row_thr, corr, nullptr,
-                                    nullptr, CT_STREAM(stream), 0, row_lo, row_hi);
+                                    nullptr, CT_STREAM(stream), 0, row_lo, row_hi, peers,
+                                    n_peers, peer_off);
   if ((rc = check_slots(batch, n_slots, scratch))) return rc;
   if (corr)
     return launch_fp<Geo, EPI_CORR_RESID>(geo, views, *batch, *s, p_meas, row_thr, corr, nullptr,
-                                          scratch, CT_STREAM(stream), n_slots, row_lo, row_hi);
+                                          scratch, CT_STREAM(stream), n_slots, row_lo, row_hi,
+                                          peers, n_peers, peer_off);
   return launch_fp<Geo, EPI_RESID>(geo, views, *batch, *s, p_meas, nullptr, nullptr, nullptr,
                                    scratch, CT_STREAM(stream), n_slots, row_lo, row_hi);
 }
@@ -782,28 +806,30 @@ int ct_fp_cyl_correction_rows(const float* mu, const float* gather, const ct_cyl
                               const ct_ray_view* views, const ct_batch* batch,
                               const ct_sampling* s, const float* p_meas, const double* row_thr,
                               float* corr, int64_t row_lo, int64_t row_hi, int n_slots,
-                              double* scratch, ct_stream_t stream) {
+                              double* scratch, float* const* corr_peers, int n_peers,
+                              int64_t peer_offset, ct_stream_t stream) {
   int rc = check_batch(batch, views, s);
   if (rc || (rc = check_cyl(grid))) return rc;
   if (!mu || !p_meas || !row_thr || !corr) return set_err(CT_ERR_ARG, "null pointer");
   CylGeo geo;
   geo.init(mu, gather, *grid);
   return fp_rows(geo, views, batch, s, p_meas, row_thr, corr, row_lo, row_hi, n_slots, scratch,
-                 stream);
+                 stream, corr_peers, n_peers, peer_offset);
 }
 
 int ct_fp_cart_correction_rows(const float* mu, const float* gather, const ct_cart_grid* grid,
                                const ct_ray_view* views, const ct_batch* batch,
                                const ct_sampling* s, const float* p_meas, const double* row_thr,
                                float* corr, int64_t row_lo, int64_t row_hi, int n_slots,
-                               double* scratch, ct_stream_t stream) {
+                               double* scratch, float* const* corr_peers, int n_peers,
+                              int64_t peer_offset, ct_stream_t stream) {
   int rc = check_batch(batch, views, s);
   if (rc || (rc = check_cart(grid))) return rc;
   if (!mu || !p_meas || !row_thr || !corr) return set_err(CT_ERR_ARG, "null pointer");
   CartGeo geo;
   geo.init(mu, gather, *grid);
   return fp_rows(geo, views, batch, s, p_meas, row_thr, corr, row_lo, row_hi, n_slots, scratch,
-                 stream);
+                 stream, corr_peers, n_peers, peer_offset);
 }
 
 int ct_fp_cyl_residual_rows(const float* mu, const float* gather, const ct_cyl_grid* grid,

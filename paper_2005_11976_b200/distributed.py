@@ -177,9 +177,12 @@ class GpuEngine:
     def pack(self, mu) -> None:
         self.eng.pack(mu, self.gather)
 
-    def correction_rows(self, mu, slots, n, out, lo, hi, n_slots, scratch):
+    def correction_rows(self, mu, slots, n, out, lo, hi, n_slots, scratch, peers=None):
+        """peers = (device pointer array, count, element offset): fused
+        all-gather by peer stores."""
+        pp, npeer, off = peers if peers else (None, 0, 0)
         self.eng.correction_rows(mu, self.p_meas, slots, n, out, lo, hi, n_slots, scratch,
-                                 self.gather)
+                                 self.gather, pp, npeer, off)
 
     def residual_rows(self, mu, slots, n, lo, hi, n_slots, scratch):
         self.eng.residual_rows(mu, self.p_meas, slots, n, n_slots, scratch, lo, hi, self.gather)
@@ -187,11 +190,13 @@ class GpuEngine:
     def residual_sum(self, scratch, acc):
         self.eng.residual_sum(scratch, acc)
 
-    def bp_update_range(self, corr, slots, n, offset, count, mu):
+    def bp_update_range(self, corr, slots, n, offset, count, mu, peers=None):
         if self.quads is None or self.quads.numel() < 4 * corr[:n].numel():
             self.quads = self.eng.alloc_quads(n)
         if self._upd is None:
             self._upd = make_update(mu, self.weights, self.cfg)
+            if peers:
+                self._upd.mu_peers, self._upd.n_peers = int(peers[0]), int(peers[1])
         self.eng.pack_quads(corr, n, self.quads)
         self.eng.bp_update_range(corr, slots, n, self._upd, offset, count, self.quads)
 
@@ -236,8 +241,16 @@ class ShardedSartRun:
         self.nvox = n
         self.offset, self.count, self.chunk = shard_range(n, self.rank, self.world)
         pad = self.chunk * self.world
+        # fused communication (opt-in, CT_FUSED_COMM=1, NCCL groups): the
+        # correction stack and mu live in symmetric memory; the FP stores its
+        # corrections and the update its voxels straight into every rank's
+        # copy over NVLink, and a symmetric-memory barrier replaces each
+        # all-gather
+        self.fused = (os.environ.get("CT_FUSED_COMM", "0") == "1" and engine is None
+                      and dist.get_backend(group) == "nccl")
+        self._symm = None
         # mu lives in a padded flat buffer so all-gather chunks are equal-sized
-        self.mu_flat = self.e.tensor(pad)
+        self.mu_flat = self._symm_tensor(pad) if self.fused else self.e.tensor(pad)
         self.mu = self.mu_flat[:n].view(grid.shape)
         init = _initial_mu(grid, cfg, self.mu.device) if cfg.initial is not None else None
         if init is not None:
@@ -253,7 +266,11 @@ class ShardedSartRun:
         self.subset_slots = [self.e.slots(s) for s in self.subsets]
         nmax = max(len(s) for s in self.subsets)
         cmax = max(sh.chunk for sh in self.shards)
-        self.corr_all = self.e.tensor(self.world * cmax * cols)      # gather target
+        self.corr_all = (self._symm_tensor(self.world * cmax * cols) if self.fused
+                         else self.e.tensor(self.world * cmax * cols))  # gather target
+        if self.fused:
+            self._h_corr = self._rendezvous(self.corr_all)
+            self._h_mu = self._rendezvous(self.mu_flat)
         self.corr = self.e.tensor((nmax, rows, cols))                 # compacted stack
         n_proj = ps.geom.n_proj
         rest = np.setdiff1d(np.arange(n_proj), self.subsets[0])
@@ -269,6 +286,18 @@ class ShardedSartRun:
         self._pending = None
         self._packed = False
         self.launch_log = None
+
+    def _symm_tensor(self, n):
+        import torch
+        import torch.distributed._symmetric_memory as symm_mem
+        t = symm_mem.empty(n, dtype=torch.float32, device=self.e.device)
+        t.zero_()
+        return t
+
+    def _rendezvous(self, t):
+        import torch.distributed._symmetric_memory as symm_mem
+        g = self.group if self.group is not None else _dist().group.WORLD
+        return symm_mem.rendezvous(t, g)
 
     def _my_rows(self):
         """(view, row0, row1) pieces of the detector this rank's FPs read."""
@@ -322,17 +351,22 @@ class ShardedSartRun:
         self._pack(s)
         mine = self.corr_all[self.rank * sh.chunk * cols:(self.rank + 1) * sh.chunk * cols]
         fused = s == 0 and self._pending is not None
+        peers = ((self._h_corr.buffer_ptrs_dev, self.world, self.rank * sh.chunk * cols),
+                 ) if self.fused else ()
         if sh.nb:
             if fused:
                 self._timed("fp_correction_resid", s, self.e.correction_rows, self.mu,
-                            sh.slots, sh.nb, mine, sh.rlo, sh.rhi, n_proj, self.scratch)
+                            sh.slots, sh.nb, mine, sh.rlo, sh.rhi, n_proj, self.scratch, *peers)
             else:
                 self._timed("fp_correction", s, self.e.correction_rows, self.mu, sh.slots,
-                            sh.nb, mine, sh.rlo, sh.rhi, 0, None)
+                            sh.nb, mine, sh.rlo, sh.rhi, 0, None, *peers)
         if fused:
             self._finish_residual()
         full = self.corr_all[:self.world * sh.chunk * cols]
-        self._timed("all_gather_corr", s, _all_gather, full, mine, self.group)
+        if self.fused:            # every rank's stores into every copy are done
+            self._timed("barrier_corr", s, self._h_corr.barrier)
+        else:
+            self._timed("all_gather_corr", s, _all_gather, full, mine, self.group)
         npix_rows = sh.n * self.rows
         if sh.equal and self.world * sh.chunk == npix_rows:
             stack = full.view(-1)[:npix_rows * cols].view(sh.n, self.rows, cols)
@@ -344,12 +378,16 @@ class ShardedSartRun:
                     flat[a * cols:b * cols].copy_(full[r * sh.chunk * cols:
                                                        (r * sh.chunk + b - a) * cols])
             stack = self.corr[:sh.n]
+        mu_peers = ((self._h_mu.buffer_ptrs_dev, self.world),) if self.fused else ()
         if self.count:
             self._timed("bp_update", s, self.e.bp_update_range, stack, self.subset_slots[s],
-                        sh.n, self.offset, self.count, self.mu)
-        self._timed("all_gather", s, _all_gather, self.mu_flat,
-                    self.mu_flat[self.rank * self.chunk:(self.rank + 1) * self.chunk],
-                    self.group)
+                        sh.n, self.offset, self.count, self.mu, *mu_peers)
+        if self.fused:            # every rank's shard is in every replica
+            self._timed("barrier_mu", s, self._h_mu.barrier)
+        else:
+            self._timed("all_gather", s, _all_gather, self.mu_flat,
+                        self.mu_flat[self.rank * self.chunk:(self.rank + 1) * self.chunk],
+                        self.group)
         self._packed = False
 
     def run_pass(self, residual: bool | None = None) -> None:

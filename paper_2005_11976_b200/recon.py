@@ -275,7 +275,8 @@ class SartEngine:
 
     def correction_rows(self, mu, p_meas, slots, n: int, corr, row_lo: int = 0,
                         row_hi: int | None = None, n_slots: int = 0, scratch=None,
-                        gather=None) -> None:
+                        gather=None, peers=None, n_peers: int = 0,
+                        peer_off: int = 0) -> None:
         """Correction FP over flattened rows [row_lo, row_hi) of an n-view batch
         (corr holds rows from row_lo); with a scratch also the residual
         partials of the same simulation at the views' slots of an
@@ -285,7 +286,9 @@ class SartEngine:
         fn = "ct_fp_cyl_correction_rows" if self.cyl else "ct_fp_cart_correction_rows"
         N.call(fn, D.ptr(mu), D.ptr(gather), C.byref(self.gc), D.ptr(self.fp_views),
                C.byref(b), C.byref(self.samp), D.ptr(p_meas), D.ptr(self.row_thr), D.ptr(corr),
-               int(row_lo), int(hi), int(n_slots), D.ptr(scratch), D.stream_handle())
+               int(row_lo), int(hi), int(n_slots), D.ptr(scratch),
+               C.c_void_p(int(peers) if peers else 0), int(n_peers), int(peer_off),
+               D.stream_handle())
 
     def residual_rows(self, mu, p_meas, slots, n: int, n_slots: int, scratch, row_lo: int = 0,
                       row_hi: int | None = None, gather=None) -> None:

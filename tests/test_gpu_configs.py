@@ -169,9 +169,13 @@ def test_c5_object_views_vs_oracle(oracle):
                           rtol=1e-6)
 
 
-def test_sharded_run_on_one_rank_group_matches_single_gpu():
-    """The angle-sharded driver (reduce-scatter / update shard / all-gather)
-    on a 1-rank NCCL group gives the single-GPU result."""
+@pytest.mark.parametrize("fused", ["0", "1"])
+def test_sharded_run_on_one_rank_group_matches_single_gpu(monkeypatch, fused):
+    """The angle-sharded driver on a 1-rank NCCL group gives the single-GPU
+    result; fused="1": the symmetric-memory path (corrections and voxels
+    stored into the replicas by the kernels, barriers instead of
+    all-gathers)."""
+    monkeypatch.setenv("CT_FUSED_COMM", fused)
     import os
     import socket
     import torch.distributed as dist
@@ -192,7 +196,9 @@ def test_sharded_run_on_one_rank_group_matches_single_gpu():
         truth = (rng.random(grid.shape) * 0.05).astype(np.float32)
         ps = P.forward_project_all(P.CylVolume(grid, dev(truth)), geom)
         cfg = P.SartConfig(relaxation=0.4, n_iterations=2, n_subsets=3)
-        a, ra = PD.ShardedSartRun(ps, grid, cfg).run()
+        srun = PD.ShardedSartRun(ps, grid, cfg)
+        assert srun.fused == (fused == "1")
+        a, ra = srun.run()
         b, rb = SartRun(ps, grid, cfg).run()
         # every correction / voxel update / residual partial is the 1-GPU one
         assert torch.equal(a.mu, b.mu)
