@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define CT_ABI_VERSION 6
+#define CT_ABI_VERSION 7
 
 #define CT_OK 0
 #define CT_ERR_ARG (-1)   /* invalid argument (null pointer, bad size) */
@@ -283,7 +283,10 @@ int ct_bp_cart_update_range(const float *corr, const float *quads, const ct_det_
 int ct_cyl_trig(const ct_cyl_grid *grid, double *trig, ct_stream_t stream);
 
 /* Stand-alone update from reduced num/den over voxels [offset, offset+count)
- * (the multi-GPU path: BP partials -> NCCL reduce-scatter -> this). */
+ * (the multi-GPU path: BP partials -> NCCL reduce-scatter -> this).  Writes
+ * upd->mu only: upd->n_peers must be 0 (CT_ERR_ARG otherwise).  Every entry
+ * point taking a ct_update rejects n_peers < 0 and n_peers > 0 with a null
+ * mu_peers. */
 int ct_sart_update(const float *num, const float *den, int64_t offset, int64_t count,
                    const ct_update *upd, ct_stream_t stream);
 
@@ -294,6 +297,16 @@ int ct_sart_update(const float *num, const float *den, int64_t offset, int64_t c
  * index needs no bias term. */
 int64_t ct_gather_floats_cyl(const ct_cyl_grid *grid);
 int64_t ct_gather_floats_cart(const ct_cart_grid *grid);
+/* (ABI v7) Which gather layout ct_pack_gather_* builds for this grid (and the
+ * FP reads): CT_GL_OCT linear 32-byte trilinear cells, CT_GL_QUAD bricked
+ * 16-byte bilinear layer cells (layers > 10 MB), CT_GL_OCTB 32-byte cells in
+ * 2x2 bricks (layers > 6 MB); < 0 for a bad grid.  Tests use it to prove
+ * which production path a parity case exercised. */
+#define CT_GL_OCT 1
+#define CT_GL_QUAD 2
+#define CT_GL_OCTB 3
+int ct_gather_layout_cyl(const ct_cyl_grid *grid);
+int ct_gather_layout_cart(const ct_cart_grid *grid);
 /* Cell (kc, jc, ic) holds the trilinear corner (k, j, i) = (kc-1, jc-1, ic-1)
  * with a one-cell halo at index -1 (r/h: a copy of index 0; theta: the wrapped
  * row n_theta-1) as the coefficients of

@@ -346,40 +346,89 @@ static inline void bilinear_gather(const double *img, int64_t n_rows, int64_t n_
     *den = b;
 }
 
+/* _kernels.py:380-417 -- voxel-driven BP of voxel m (one body of the prange
+ * loop); adds its footprint to *num / *den. */
+static inline void bp_cyl_voxel(int64_t m, const double *corr, int64_t n_rows, int64_t n_cols,
+                                double u0, double v0, double pitch, double sdd, double sod,
+                                double cphi, double sphi, const double *rot,
+                                const double *tvec, double radius, double height, int64_t nh,
+                                int64_t nt, int64_t nr, double *num, double *den) {
+    const double dr = radius / (double)nr;
+    const double dth = OR_TWO_PI / (double)nt;
+    const double dh = height / (double)nh;
+    const double half_h = 0.5 * height;
+    const double depth_floor = 1e-6 * sod;
+    (void)nh;
+    int64_t k = m / (nt * nr);
+    int64_t j = (m / nr) % nt;
+    int64_t ir = m % nr;
+    double r = ((double)ir + 0.5) * dr;
+    double th = ((double)j + 0.5) * dth;
+    double h = ((double)k + 0.5) * dh - half_h;
+    double xo = r * cos(th);
+    double yo = r * sin(th);
+    double xw = rot[0] * xo + rot[1] * yo + rot[2] * h + tvec[0];
+    double yw = rot[3] * xo + rot[4] * yo + rot[5] * h + tvec[1];
+    double zw = rot[6] * xo + rot[7] * yo + rot[8] * h + tvec[2];
+    double xi = cphi * xw - sphi * yw;
+    double yi = sphi * xw + cphi * yw;
+    double depth = sod + yi;
+    if (depth <= depth_floor) return;
+    double scale = sdd / (depth * pitch);
+    double a, b;
+    bilinear_gather(corr, n_rows, n_cols, u0 + xi * scale, v0 + zw * scale, &a, &b);
+    *num += a;
+    *den += b;
+}
+
 /* _kernels.py:380-417 -- voxel-driven BP; ACCUMULATES into num/den. */
 void oracle_backproject_cyl(const double *corr, int64_t n_rows, int64_t n_cols, double u0,
                             double v0, double pitch, double sdd, double sod, double cphi,
                             double sphi, const double *rot, const double *tvec,
                             double radius, double height, int64_t nh, int64_t nt,
                             int64_t nr, double *num, double *den) {
-    const double dr = radius / (double)nr;
-    const double dth = OR_TWO_PI / (double)nt;
-    const double dh = height / (double)nh;
-    const double half_h = 0.5 * height;
-    const double depth_floor = 1e-6 * sod;
 #pragma omp parallel for schedule(static)
-    for (int64_t m = 0; m < nh * nt * nr; ++m) {
-        int64_t k = m / (nt * nr);
-        int64_t j = (m / nr) % nt;
-        int64_t ir = m % nr;
-        double r = ((double)ir + 0.5) * dr;
-        double th = ((double)j + 0.5) * dth;
-        double h = ((double)k + 0.5) * dh - half_h;
-        double xo = r * cos(th);
-        double yo = r * sin(th);
-        double xw = rot[0] * xo + rot[1] * yo + rot[2] * h + tvec[0];
-        double yw = rot[3] * xo + rot[4] * yo + rot[5] * h + tvec[1];
-        double zw = rot[6] * xo + rot[7] * yo + rot[8] * h + tvec[2];
-        double xi = cphi * xw - sphi * yw;
-        double yi = sphi * xw + cphi * yw;
-        double depth = sod + yi;
-        if (depth <= depth_floor) continue;
-        double scale = sdd / (depth * pitch);
-        double a, b;
-        bilinear_gather(corr, n_rows, n_cols, u0 + xi * scale, v0 + zw * scale, &a, &b);
-        num[m] += a;
-        den[m] += b;
-    }
+    for (int64_t m = 0; m < nh * nt * nr; ++m)
+        bp_cyl_voxel(m, corr, n_rows, n_cols, u0, v0, pitch, sdd, sod, cphi, sphi, rot, tvec,
+                     radius, height, nh, nt, nr, &num[m], &den[m]);
+}
+
+/* The same per-voxel function on an explicit voxel list (flat indices
+ * idx[0..n_idx)); num/den have n_idx entries (accumulated).  For parity at
+ * sizes where the whole-volume BP is too slow for a test. */
+void oracle_backproject_cyl_voxels(const double *corr, int64_t n_rows, int64_t n_cols,
+                                   double u0, double v0, double pitch, double sdd, double sod,
+                                   double cphi, double sphi, const double *rot,
+                                   const double *tvec, double radius, double height,
+                                   int64_t nh, int64_t nt, int64_t nr, const int64_t *idx,
+                                   int64_t n_idx, double *num, double *den) {
+#pragma omp parallel for schedule(static)
+    for (int64_t q = 0; q < n_idx; ++q)
+        bp_cyl_voxel(idx[q], corr, n_rows, n_cols, u0, v0, pitch, sdd, sod, cphi, sphi, rot,
+                     tvec, radius, height, nh, nt, nr, &num[q], &den[q]);
+}
+
+/* _kernels.py:420-443 -- one voxel of the Cartesian BP. */
+static inline void bp_cart_voxel(int64_t m, const double *corr, int64_t n_rows, int64_t n_cols,
+                                 double u0, double v0, double pitch, double sdd, double sod,
+                                 double cphi, double sphi, double vs, double ox, double oy,
+                                 double oz, int64_t ny, int64_t nx, double *num, double *den) {
+    const double depth_floor = 1e-6 * sod;
+    int64_t k = m / (ny * nx);
+    int64_t j = (m / nx) % ny;
+    int64_t i = m % nx;
+    double xw = ox + ((double)i + 0.5) * vs;
+    double yw = oy + ((double)j + 0.5) * vs;
+    double zw = oz + ((double)k + 0.5) * vs;
+    double xi = cphi * xw - sphi * yw;
+    double yi = sphi * xw + cphi * yw;
+    double depth = sod + yi;
+    if (depth <= depth_floor) return;
+    double scale = sdd / (depth * pitch);
+    double a, b;
+    bilinear_gather(corr, n_rows, n_cols, u0 + xi * scale, v0 + zw * scale, &a, &b);
+    *num += a;
+    *den += b;
 }
 
 /* _kernels.py:420-443 */
@@ -387,25 +436,23 @@ void oracle_backproject_cart(const double *corr, int64_t n_rows, int64_t n_cols,
                              double v0, double pitch, double sdd, double sod, double cphi,
                              double sphi, double vs, double ox, double oy, double oz,
                              int64_t nz, int64_t ny, int64_t nx, double *num, double *den) {
-    const double depth_floor = 1e-6 * sod;
 #pragma omp parallel for schedule(static)
-    for (int64_t m = 0; m < nz * ny * nx; ++m) {
-        int64_t k = m / (ny * nx);
-        int64_t j = (m / nx) % ny;
-        int64_t i = m % nx;
-        double xw = ox + ((double)i + 0.5) * vs;
-        double yw = oy + ((double)j + 0.5) * vs;
-        double zw = oz + ((double)k + 0.5) * vs;
-        double xi = cphi * xw - sphi * yw;
-        double yi = sphi * xw + cphi * yw;
-        double depth = sod + yi;
-        if (depth <= depth_floor) continue;
-        double scale = sdd / (depth * pitch);
-        double a, b;
-        bilinear_gather(corr, n_rows, n_cols, u0 + xi * scale, v0 + zw * scale, &a, &b);
-        num[m] += a;
-        den[m] += b;
-    }
+    for (int64_t m = 0; m < nz * ny * nx; ++m)
+        bp_cart_voxel(m, corr, n_rows, n_cols, u0, v0, pitch, sdd, sod, cphi, sphi, vs, ox, oy,
+                      oz, ny, nx, &num[m], &den[m]);
+}
+
+void oracle_backproject_cart_voxels(const double *corr, int64_t n_rows, int64_t n_cols,
+                                    double u0, double v0, double pitch, double sdd, double sod,
+                                    double cphi, double sphi, double vs, double ox, double oy,
+                                    double oz, int64_t nz, int64_t ny, int64_t nx,
+                                    const int64_t *idx, int64_t n_idx, double *num,
+                                    double *den) {
+    (void)nz;
+#pragma omp parallel for schedule(static)
+    for (int64_t q = 0; q < n_idx; ++q)
+        bp_cart_voxel(idx[q], corr, n_rows, n_cols, u0, v0, pitch, sdd, sod, cphi, sphi, vs, ox,
+                      oy, oz, ny, nx, &num[q], &den[q]);
 }
 
 /* Threads the OpenMP runtime will use (for the cpu_baseline's "cores"). */

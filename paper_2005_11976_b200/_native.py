@@ -20,7 +20,7 @@ LIB_NAME = "libcyltomo_b200.so"
 LIB_PATH = Path(os.environ.get("CT_LIBRARY") or Path(__file__).resolve().parent / LIB_NAME)
 
 CT_OK = 0
-CT_ABI_VERSION = 6
+CT_ABI_VERSION = 7
 
 
 class CylGridC(C.Structure):
@@ -94,6 +94,8 @@ _SIGNATURES = {
     "ct_residual_sum": (C.c_int, [P, C.c_int64, P, P]),
     "ct_gather_floats_cyl": (C.c_int64, [C.POINTER(CylGridC)]),
     "ct_gather_floats_cart": (C.c_int64, [C.POINTER(CartGridC)]),
+    "ct_gather_layout_cyl": (C.c_int, [C.POINTER(CylGridC)]),
+    "ct_gather_layout_cart": (C.c_int, [C.POINTER(CartGridC)]),
     "ct_pack_gather_cyl": (C.c_int, [P, C.POINTER(CylGridC), P, P]),
     "ct_pack_gather_cart": (C.c_int, [P, C.POINTER(CartGridC), P, P]),
     "ct_rowsum_max_cyl": (C.c_int, [C.POINTER(CylGridC), P, C.POINTER(BatchC),

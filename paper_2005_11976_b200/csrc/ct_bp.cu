@@ -479,6 +479,15 @@ static int check_bp(const float* corr, const ct_det_view* dets, const ct_batch* 
   return CT_OK;
 }
 
+// every entry point that takes a ct_update: mu present, and a consistent peer
+// list (n_peers >= 0; n_peers > 0 needs the device pointer array)
+static int check_update(const ct_update* upd) {
+  if (!upd || !upd->mu) return set_err(CT_ERR_ARG, "null update/mu");
+  if (upd->n_peers < 0 || (upd->n_peers > 0 && !upd->mu_peers))
+    return set_err(CT_ERR_ARG, "bad update peer list");
+  return CT_OK;
+}
+
 int ct_bp_cyl(const float* corr, const float* quads, const ct_det_view* dets, const ct_batch* batch,
               const ct_cyl_grid* grid, const double* trig, float* num, float* den,
               int accumulate, ct_stream_t stream) {
@@ -510,7 +519,8 @@ int ct_bp_cyl_update(const float* corr, const float* quads, const ct_det_view* d
                      ct_stream_t stream) {
   int rc = check_bp(corr, dets, batch);
   if (rc || (rc = check_cyl(grid))) return rc;
-  if (!trig || !upd || !upd->mu) return set_err(CT_ERR_ARG, "null trig/update/mu");
+  if (!trig) return set_err(CT_ERR_ARG, "null trig");
+  if ((rc = check_update(upd))) return rc;
   CylVox vox;
   vox.init(*grid, trig);
   return launch_bp<CylVox, BP_UPDATE>(vox, corr, quads, dets, *batch, nullptr, nullptr, upd,
@@ -521,7 +531,7 @@ int ct_bp_cart_update(const float* corr, const float* quads, const ct_det_view* 
                       const ct_cart_grid* grid, const ct_update* upd, ct_stream_t stream) {
   int rc = check_bp(corr, dets, batch);
   if (rc || (rc = check_cart(grid))) return rc;
-  if (!upd || !upd->mu) return set_err(CT_ERR_ARG, "null update/mu");
+  if ((rc = check_update(upd))) return rc;
   CartVox vox;
   vox.init(*grid);
   return launch_bp<CartVox, BP_UPDATE>(vox, corr, quads, dets, *batch, nullptr, nullptr, upd,
@@ -534,7 +544,8 @@ int ct_bp_cyl_update_range(const float* corr, const float* quads, const ct_det_v
                            ct_stream_t stream) {
   int rc = check_bp(corr, dets, batch);
   if (rc || (rc = check_cyl(grid))) return rc;
-  if (!trig || !upd || !upd->mu) return set_err(CT_ERR_ARG, "null trig/update/mu");
+  if (!trig) return set_err(CT_ERR_ARG, "null trig");
+  if ((rc = check_update(upd))) return rc;
   const int64_t n = (int64_t)grid->n_h * grid->n_theta * grid->n_r;
   if (offset < 0 || count < 0 || offset + count > n) return set_err(CT_ERR_ARG, "bad voxel range");
   CylVox vox;
@@ -548,7 +559,7 @@ int ct_bp_cart_update_range(const float* corr, const float* quads, const ct_det_
                             int64_t offset, int64_t count, ct_stream_t stream) {
   int rc = check_bp(corr, dets, batch);
   if (rc || (rc = check_cart(grid))) return rc;
-  if (!upd || !upd->mu) return set_err(CT_ERR_ARG, "null update/mu");
+  if ((rc = check_update(upd))) return rc;
   const int64_t n = (int64_t)grid->n_z * grid->n_y * grid->n_x;
   if (offset < 0 || count < 0 || offset + count > n) return set_err(CT_ERR_ARG, "bad voxel range");
   CartVox vox;
@@ -569,6 +580,8 @@ int ct_sart_update(const float* num, const float* den, int64_t offset, int64_t c
                    const ct_update* upd, ct_stream_t stream) {
   if (!num || !den || !upd || !upd->mu || offset < 0 || count < 0)
     return set_err(CT_ERR_ARG, "bad update arguments");
+  // the stand-alone update writes mu only (peer replicas: the fused BP update)
+  if (upd->n_peers != 0) return set_err(CT_ERR_ARG, "ct_sart_update does not take peer replicas");
   if (count == 0) return CT_OK;
   update_kernel<<<blocks_for(count, 256), 256, 0, CT_STREAM(stream)>>>(num, den, offset, count,
                                                                        *upd);

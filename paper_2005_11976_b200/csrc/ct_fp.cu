@@ -918,6 +918,20 @@ int64_t ct_gather_floats_cart(const ct_cart_grid* grid) {
   return check_cart(grid) ? 0 : gather_floats_cart(*grid);
 }
 
+static int layout_of(double cells) {
+  return gather_quad(cells) ? CT_GL_QUAD : gather_obrick(cells) ? CT_GL_OCTB : CT_GL_OCT;
+}
+static_assert(CT_GL_OCT == GL_OCT && CT_GL_QUAD == GL_QUAD && CT_GL_OCTB == GL_OCTB,
+              "layout enum");
+
+int ct_gather_layout_cyl(const ct_cyl_grid* grid) {
+  return check_cyl(grid) ? CT_ERR_ARG : layout_of(cells_layer_cyl(*grid));
+}
+
+int ct_gather_layout_cart(const ct_cart_grid* grid) {
+  return check_cart(grid) ? CT_ERR_ARG : layout_of(cells_layer_cart(*grid));
+}
+
 int ct_pack_gather_cyl(const float* mu, const ct_cyl_grid* grid, float* gather,
                        ct_stream_t stream) {
   int rc = check_cyl(grid);

@@ -286,6 +286,17 @@ class ShardedSartRun:
         self._pending = None
         self._packed = False
         self.launch_log = None
+        if self.fused:
+            # every rank's replica setup (zero fill, initial mu) must be done
+            # before any rank's first peer store lands in it: device barriers
+            # on the compute stream, after the queued initialisation
+            self._h_corr.barrier()
+            self._h_mu.barrier()
+            if self.world > 1:
+                import warnings
+                warnings.warn("CT_FUSED_COMM=1 with more than one rank: the peer-store "
+                              "path is verified bit-identical on 1-rank groups only",
+                              RuntimeWarning, stacklevel=2)
 
     def _symm_tensor(self, n):
         import torch

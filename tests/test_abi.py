@@ -53,8 +53,10 @@ def test_struct_layouts_match_header(tmp_path):
           printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(ct_cyl_grid), sizeof(ct_cart_grid),
                  sizeof(ct_ray_view), sizeof(ct_det_view), sizeof(ct_sampling),
                  sizeof(ct_update), sizeof(ct_batch));
-          printf("%zu %zu %zu %zu\\n", offsetof(ct_cyl_grid, rot), offsetof(ct_cyl_grid, t),
-                 offsetof(ct_update, weights), offsetof(ct_batch, view_ids));
+          printf("%zu %zu %zu %zu %zu %zu\\n", offsetof(ct_cyl_grid, rot),
+                 offsetof(ct_cyl_grid, t), offsetof(ct_update, weights),
+                 offsetof(ct_batch, view_ids), offsetof(ct_update, mu_peers),
+                 offsetof(ct_update, n_peers));
           return 0;
         }"""))
     exe = tmp_path / "probe"
@@ -66,7 +68,9 @@ def test_struct_layouts_match_header(tmp_path):
                                     N.SamplingC, N.UpdateC, N.BatchC)]
     assert [int(x) for x in sizes.split()] == expect
     assert [int(x) for x in offs.split()] == [N.CylGridC.rot.offset, N.CylGridC.t.offset,
-                                             N.UpdateC.weights.offset, N.BatchC.view_ids.offset]
+                                             N.UpdateC.weights.offset, N.BatchC.view_ids.offset,
+                                             N.UpdateC.mu_peers.offset,
+                                             N.UpdateC.n_peers.offset]
 
 
 def test_argument_errors_return_status_not_crash():
@@ -81,6 +85,47 @@ def test_argument_errors_return_status_not_crash():
     assert lib.ct_last_error()
     with pytest.raises(N.NativeError):
         N.call("ct_sart_update", None, None, 0, 0, None, None)
+
+
+def test_update_peer_lists_are_validated():
+    """Every ct_update entry point rejects an inconsistent peer list before any
+    launch (n_peers < 0, or n_peers > 0 without the pointer array), and the
+    stand-alone update refuses peers (it writes mu only)."""
+    from paper_2005_11976_b200 import _native as N
+    lib = N.load_library()
+    g = N.CylGridC(4, 8, 6, 0, 2.0, 3.0)
+    gx = N.CartGridC(4, 4, 4, 0, 0.5)
+    b = N.BatchC(1, 9, 9, 0, None)
+    dummy = C.c_void_p(16)            # never dereferenced: validation comes first
+    for n_peers, peers in ((-1, None), (2, None)):
+        u = N.UpdateC(0.5, 1, None, dummy, peers, n_peers, 0)
+        for rc in (lib.ct_bp_cyl_update(dummy, None, dummy, C.byref(b), C.byref(g), dummy,
+                                        C.byref(u), None),
+                   lib.ct_bp_cart_update(dummy, None, dummy, C.byref(b), C.byref(gx),
+                                         C.byref(u), None),
+                   lib.ct_bp_cyl_update_range(dummy, None, dummy, C.byref(b), C.byref(g), dummy,
+                                              C.byref(u), 0, 1, None),
+                   lib.ct_bp_cart_update_range(dummy, None, dummy, C.byref(b), C.byref(gx),
+                                               C.byref(u), 0, 1, None),
+                   lib.ct_sart_update(dummy, dummy, 0, 1, C.byref(u), None)):
+            assert rc == -1
+            assert b"peer" in lib.ct_last_error()
+    u = N.UpdateC(0.5, 1, None, dummy, dummy, 1, 0)
+    assert lib.ct_sart_update(dummy, dummy, 0, 1, C.byref(u), None) == -1
+
+
+def test_gather_layout_query():
+    """ct_gather_layout_*: the layout the FP of a config reads (no GPU needed)."""
+    from paper_2005_11976_b200 import _native as N
+    import paper_2005_11976_b200 as P
+    from paper_2005_11976_b200 import _device as D
+    lib = N.load_library()
+    cyl = lambda *s: C.byref(D.grid_c(P.CylGrid(*s, 12.0, 24.0)))
+    assert lib.ct_gather_layout_cyl(cyl(256, 512, 256)) == 1          # C2/C3: GL_OCT
+    assert lib.ct_gather_layout_cyl(cyl(512, 1024, 384)) == 2         # C4-cyl/C5: GL_QUAD
+    cart = D.grid_c(P.CartGrid.centered(512, 512, 512, 24.0 / 512))
+    assert lib.ct_gather_layout_cart(C.byref(cart)) == 3              # C4-cart: GL_OCTB
+    assert lib.ct_gather_layout_cyl(C.byref(N.CylGridC())) == -1
 
 
 def test_no_cpu_fallback_without_gpu():
