@@ -24,8 +24,9 @@ bytes:
   so an all-reduce of the slot scratch (x + 0 + ... = x) and one fixed-order
   sum give the single-GPU residual bit for bit.
 * **object sharding** -- independent objects (config C5 batches) are
-  assigned round-robin, no collective on the data path
-  (:func:`reconstruct_batch`).
+  assigned round-robin, no collective on the data path; composed with angle
+  sharding as G = G_obj x G_ang (:class:`BatchPlan`,
+  :func:`reconstruct_batch`).
 
 The compute engine is injectable so the host logic (row / voxel
 partitioning, collective sequence, residual slots) is testable on CPU with
@@ -456,16 +457,72 @@ def assign_objects(n_objects: int, rank: int, world: int):
     return list(range(rank, n_objects, world))
 
 
-def reconstruct_batch(items, cfg: SartConfig, rank: int = 0, world: int = 1):
-    """Object-sharded batch reconstruction (no data-path collective).
+class BatchPlan:
+    """G = G_obj x G_ang decomposition of the ranks for an object batch
+    (config C5): ranks [g*G_ang, (g+1)*G_ang) form object group
+    g; objects go round-robin to the G_obj groups (no collective between
+    groups), and each object's OS-SART subsets are angle-sharded over the
+    G_ang ranks of its group (ShardedSartRun).  G_ang = 1 is pure object
+    sharding, G_ang = G pure angle sharding."""
 
-    items: sequence of (ProjectionSet, grid[, SartConfig]) for every object; the
-    rank reconstructs its own objects and returns {index: (volume, report)}.
+    def __init__(self, rank: int, world: int, g_ang: int = 1):
+        if g_ang < 1 or world % g_ang:
+            raise ConfigError(f"angle-group size {g_ang} does not divide {world} ranks")
+        self.rank, self.world, self.g_ang = int(rank), int(world), int(g_ang)
+        self.n_groups = self.world // self.g_ang
+        self.group_index = self.rank // self.g_ang
+        self.group_rank = self.rank % self.g_ang
+
+    def group_ranks(self, g: int) -> list:
+        return list(range(g * self.g_ang, (g + 1) * self.g_ang))
+
+    def objects(self, n_objects: int) -> list:
+        """This rank's objects (every rank of a group gets the group's)."""
+        return assign_objects(n_objects, self.group_index, self.n_groups)
+
+    def make_group(self):
+        """This rank's object group as a process group (collective: every rank
+        creates every group, in order).  None for G_ang = 1 (no exchange)."""
+        if self.g_ang == 1:
+            return None
+        dist = _dist()
+        mine = None
+        for g in range(self.n_groups):
+            pg = dist.new_group(self.group_ranks(g))
+            if g == self.group_index:
+                mine = pg
+        return mine
+
+
+def _default_runner(ps, grid, cfg, group):
+    if group is None:
+        from .recon import SartRun
+        return SartRun(ps, grid, cfg).run()
+    return ShardedSartRun(ps, grid, cfg, group).run()
+
+
+def reconstruct_batch(items, cfg: SartConfig, rank: int | None = None,
+                      world: int | None = None, g_ang: int = 1, runner=None):
+    """Batch reconstruction over G = G_obj x G_ang ranks (BatchPlan).
+
+    items: sequence of (ProjectionSet, grid[, SartConfig]) for every object.
+    Objects are independent (no data-path collective between object groups);
+    with g_ang > 1 each object's subsets are angle-sharded over its group.
+    Returns {index: (volume, report)} for this rank's objects (every rank of
+    an object group holds the group's results).  runner(ps, grid, cfg,
+    group) overrides the per-object driver (tests: an oracle engine).
     """
-    from .recon import SartRun
+    if rank is None or world is None:
+        dist = _dist()
+        on = dist.is_available() and dist.is_initialized()
+        rank = dist.get_rank() if on else 0
+        world = dist.get_world_size() if on else 1
+    plan = BatchPlan(rank, world, g_ang)
+    group = plan.make_group()
+    run = runner or _default_runner
     out = {}
-    for idx in assign_objects(len(items), rank, world):
+    for idx in plan.objects(len(items)):
         it = items[idx]
         c = it[2] if len(it) > 2 else cfg
-        out[idx] = SartRun(it[0], it[1], c).run()
+        out[idx] = run(it[0], it[1], c, group)
     return out

@@ -203,3 +203,103 @@ def test_shard_helpers():
     covered = sum(c for _, c, _ in ranges)
     assert covered == n and ranges[0][0] == 0 and ranges[-1][0] + ranges[-1][1] == n
     assert PD.assign_objects(10, 1, 4) == [1, 5, 9]
+
+
+# ---------------------------------------------------------------------------
+# object batches: G = G_obj x G_ang (BatchPlan / reconstruct_batch)
+# ---------------------------------------------------------------------------
+def _batch_items(P, orc, geom, grid_base, n_objects):
+    """n seeded objects with their own poses (config C5 in miniature)."""
+    items, truths = [], []
+    for k in range(n_objects):
+        rng = np.random.default_rng(50 + k)
+        grid = P.CylGrid(grid_base.n_h, grid_base.n_theta, grid_base.n_r, grid_base.radius,
+                         grid_base.height,
+                         P.Pose.tilt(float(rng.uniform(0, 3)), float(rng.uniform(0, 0.15)),
+                                     list(rng.uniform(-0.3, 0.3, 2)) + [0.0]))
+        truth = rng.random(grid.shape) * 0.05
+        images = np.stack([orc.forward(truth, grid, geom, i)[0] for i in range(geom.n_proj)])
+        items.append((P.ProjectionSet(geom, images.astype(np.float32)), grid))
+        truths.append(truth)
+    return items
+
+
+def _batch_worker(rank, world, port, outdir, g_ang, n_objects):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    sys.path.insert(0, str(ROOT))
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import torch.distributed as dist
+    import oracle as orc
+    from paper_2005_11976_b200 import distributed as PD
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    P, geom, grid, _, _ = _problem()
+    items = _batch_items(P, orc, geom, grid, n_objects)
+    cfg = P.SartConfig(relaxation=0.4, n_iterations=2, n_subsets=3)
+    sizes = {}
+
+    def runner(ps, g, c, group):
+        # every object through the angle-sharded driver on its group (a
+        # 1-rank group for G_ang = 1), with the oracle engine
+        sizes[id(ps)] = 1 if group is None else dist.get_world_size(group)
+        grp = group if group is not None else dist.new_group([rank])
+        run = PD.ShardedSartRun(ps, g, c, group=grp, engine=OracleEngine(orc, ps, g, c))
+        return run.run()
+
+    if g_ang == 1:
+        # G_ang = 1 has no group; give each rank a 1-rank group (collective creation)
+        solo = [dist.new_group([r]) for r in range(world)]
+        runner_1 = lambda ps, g, c, group: runner(ps, g, c, solo[rank])  # noqa: E731
+        out = PD.reconstruct_batch(items, cfg, rank, world, g_ang=1, runner=runner_1)
+    else:
+        out = PD.reconstruct_batch(items, cfg, rank, world, g_ang=g_ang, runner=runner)
+    np.savez(Path(outdir) / f"b{rank}.npz", idx=np.array(sorted(out)),
+             mu=np.stack([np.asarray(out[i][0].mu) for i in sorted(out)]),
+             res=np.array([out[i][1].residuals for i in sorted(out)]),
+             group_size=max(sizes.values()) if sizes else 0)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,g_ang", [(2, 1), (2, 2), (4, 2)])
+def test_batch_reconstruction_object_and_angle_groups(oracle, tmp_path, world, g_ang):
+    """reconstruct_batch over G = G_obj x G_ang gloo ranks: every object is
+    reconstructed by exactly one object group, all ranks of a group hold the
+    same volume, and each equals the single-process OS-SART oracle."""
+    import torch.multiprocessing as mp
+    n_objects = 3
+    mp.start_processes(_batch_worker, args=(world, _free_port(), str(tmp_path), g_ang,
+                                            n_objects),
+                       nprocs=world, start_method="spawn", join=True)
+    P, geom, grid, _, _ = _problem()
+    items = _batch_items(P, oracle, geom, grid, n_objects)
+    rs = [np.load(tmp_path / f"b{r}.npz") for r in range(world)]
+    n_groups = world // g_ang
+    seen = {}
+    for r, d in enumerate(rs):
+        g = r // g_ang
+        assert list(d["idx"]) == list(range(g, n_objects, n_groups))
+        for k, i in enumerate(d["idx"]):
+            if int(i) in seen:                           # same group: identical replicas
+                assert seen[int(i)][0] == g
+                assert np.array_equal(seen[int(i)][1], d["mu"][k])
+            seen[int(i)] = (g, d["mu"][k], d["res"][k])
+    assert sorted(seen) == list(range(n_objects))
+    for i, (ps, g) in enumerate(items):
+        mu_ref, res_ref = oracle.sart(ps.images, g, geom, relaxation=0.4, n_iterations=2,
+                                      n_subsets=3)
+        _, mu, res = seen[i]
+        assert np.abs(mu - mu_ref).max() <= 1e-12 * np.abs(mu_ref).max()
+        assert np.allclose(res, res_ref, rtol=1e-12)
+
+
+def test_batch_plan():
+    from paper_2005_11976_b200 import distributed as PD
+    from paper_2005_11976_b200.errors import ConfigError
+    p = PD.BatchPlan(5, 8, 2)
+    assert (p.n_groups, p.group_index, p.group_rank) == (4, 2, 1)
+    assert p.group_ranks(2) == [4, 5]
+    assert p.objects(64) == list(range(2, 64, 4))
+    assert PD.BatchPlan(3, 8, 1).objects(10) == [3]
+    assert PD.BatchPlan(0, 8, 8).objects(3) == [0, 1, 2]
+    with pytest.raises(ConfigError):
+        PD.BatchPlan(0, 8, 3)

@@ -191,8 +191,14 @@ def test_c5_os_subset_update_production_path_vs_oracle(oracle, c5_run):
         sims_o.append(sim_o[valid])
     assert rel_l2(np.concatenate(sims), np.concatenate(sims_o)) < PROJ_TOL
     # (b) the fused update at sampled voxels: oracle BP sums of the same
-    # correction images + the reference update rule
-    idx = sample_voxels(wl.grid, 20000, 5)
+    # correction images + the reference update rule.  The update from the
+    # template is sparse (rays through the added / missing inclusions), so
+    # half the samples are drawn among the voxels the subset changed.
+    changed = torch.nonzero((run.mu != mu0).view(-1)).view(-1).cpu().numpy()
+    assert changed.size > 10000
+    rng = np.random.default_rng(5)
+    idx = np.unique(np.concatenate([sample_voxels(wl.grid, 10000, 5),
+                                    rng.choice(changed, 10000, replace=False)]))
     num = np.zeros(idx.size)
     den = np.zeros(idx.size)
     for b, i in enumerate(s):
@@ -206,7 +212,7 @@ def test_c5_os_subset_update_production_path_vs_oracle(oracle, c5_run):
     assert np.array_equal(start, f32(mu_start))
     assert (den > 0).mean() > 0.99
     delta_o = mu_o - mu_start
-    assert np.linalg.norm(delta_o) > 1e-3 * np.linalg.norm(mu_start)   # a real update
+    assert np.count_nonzero(delta_o) > 0.4 * idx.size                  # a real update
     assert rel_l2(got - start, delta_o) < RECON_TOL
 
 
