@@ -38,35 +38,75 @@ from .recon import SartConfig, presence_metric, sart_run
 
 EXIT_OK, EXIT_UNEXPECTED, EXIT_CONFIG, EXIT_IO, EXIT_DOMAIN = 0, 1, 2, 3, 4
 
+# exception class -> (exit code, message prefix), checked in order
+# (the reference's exit-code contract, cyltomo/cli.py:33-38)
+EXIT_MAP = ((errors.ConfigError, EXIT_CONFIG, "config error"),
+            ((errors.IoFailure, errors.SchemaMismatch, errors.SizeMismatch), EXIT_IO, "io error"),
+            (errors.CylTomoError, EXIT_DOMAIN, "error"))
 
-def deep_merge(base: dict, override: dict) -> dict:
-    out = dict(base)
-    for key, value in override.items():
-        if isinstance(value, dict) and isinstance(out.get(key), dict):
-            out[key] = deep_merge(out[key], value)
-        else:
-            out[key] = value
-    return out
+# --preset paper: the paper-scale simulation geometry (cyltomo/cli.py:250-252)
+PAPER_GEOMETRY = {"n_views": 4096, "det_cols": 2048, "det_rows": 128,
+                  "pixel_pitch_mm": 0.0096, "full_turn": True}
+
+
+def merged(defaults: dict, user: dict) -> dict:
+    """`user` laid over `defaults`, nested objects merged key by key (lists and
+    scalars replace).  Iterative: a work list of (target, overlay) pairs."""
+    root = dict(defaults)
+    work = [(root, user)]
+    while work:
+        target, overlay = work.pop()
+        for key, value in overlay.items():
+            below = target.get(key)
+            if isinstance(value, dict) and isinstance(below, dict):
+                target[key] = dict(below)
+                work.append((target[key], value))
+            else:
+                target[key] = value
+    return root
+
+
+def _read_json_document(path: str) -> dict:
+    try:
+        text = Path(path).read_text()
+    except OSError as exc:
+        raise errors.IoFailure(f"cannot read config {path}: {exc}") from exc
+    try:
+        return json.loads(text)
+    except json.JSONDecodeError as exc:
+        raise errors.ConfigError(f"config is not valid JSON: {exc}") from exc
 
 
 def load_config(args, defaults: dict, schema: dict) -> dict:
-    cfg = dict(defaults)
-    if args.config:
-        try:
-            user = json.loads(Path(args.config).read_text())
-        except OSError as exc:
-            raise errors.IoFailure(f"cannot read config {args.config}: {exc}") from exc
-        except json.JSONDecodeError as exc:
-            raise errors.ConfigError(f"config is not valid JSON: {exc}") from exc
-        cfg = deep_merge(cfg, user)
+    """Defaults, overlaid with the --config document, schema-validated."""
+    cfg = merged(defaults, _read_json_document(args.config)) if args.config else dict(defaults)
     try:
         import jsonschema
-        jsonschema.validate(cfg, schema)
     except ImportError:  # pragma: no cover - jsonschema ships with the image
-        pass
-    except Exception as exc:  # jsonschema.ValidationError
-        raise errors.ConfigError(f"config invalid: {getattr(exc, 'message', exc)}") from exc
+        return cfg
+    problems = sorted(jsonschema.Draft7Validator(schema).iter_errors(cfg), key=str)
+    if problems:
+        raise errors.ConfigError(f"config invalid: {problems[0].message}")
     return cfg
+
+
+def configure_threads(n: int | None) -> None:
+    """--threads / CYLTOMO_THREADS (the reference caps its numba pool,
+    cyltomo/cli.py:45-53): here the cap applies to the host worker pool that
+    stages pageable projections (recon._stage_pool) and to torch's intra-op
+    threads; the GPU kernels are unaffected."""
+    if n is None:
+        env = os.environ.get("CYLTOMO_THREADS")
+        n = int(env) if env else None
+    if n is None:
+        return
+    n = max(1, int(n))
+    os.environ["CT_HOST_THREADS"] = str(n)
+    try:
+        import torch
+        torch.set_num_threads(n)
+    except Exception:  # pragma: no cover
+        pass
 
 
 GEOMETRY_SCHEMA = {
@@ -122,8 +162,9 @@ SIMULATE_SCHEMA = {
 
 
 def cmd_simulate(args) -> int:
-    cfg = load_config(args, {"geometry": {}, "step_mm": None, "supersample": 1,
-                             "noise_sigma": 0.0}, SIMULATE_SCHEMA)
+    defaults = {"geometry": dict(PAPER_GEOMETRY) if args.preset == "paper" else {},
+                "step_mm": None, "supersample": 1, "noise_sigma": 0.0}
+    cfg = load_config(args, defaults, SIMULATE_SCHEMA)
     if args.views is not None:
         cfg["geometry"]["n_views"] = args.views
     vol = io.read_volume(cfg["volume"], device=True)
@@ -185,67 +226,18 @@ DEVICE_POSE_PARAMS = dict(threshold_level=1.8, threshold_levels=9, threshold_spa
 
 POSE_SCHEMA = {
     "type": "object",
-    "properties": {
-        "projections": {"type": "string"},
-        "params": {"type": "object"},
-        "study": {
-            "type": "object",
-            "properties": {
-                "centers_px": {"type": "array", "minItems": 2},
-                "noise_sigma": {"type": "number", "minimum": 0},
-                "geometry": GEOMETRY_SCHEMA,
-                "sim_shape": {"type": "array"},
-            },
-            "required": ["centers_px"],
-        },
-    },
+    "properties": {"projections": {"type": "string"}, "params": {"type": "object"}},
 }
 
 
-def pose_precision_study(centers_px, geom: ScanGeometry, sim_shape=(60, 16, 32),
-                         noise_sigma: float = 0.01, seed: int = 0, pose: Pose | None = None):
-    """Repeated scans with shifted rotation-center column u0; spread of the
-    estimates per pose component (cyltomo/experiments.py:342-372)."""
-    import warnings
-    rng = np.random.default_rng(seed)
-    pose = pose or Pose(alpha=0.4, beta=math.radians(1.0), t=[1.0, -1.0, 0.5])
-    with warnings.catch_warnings():
-        warnings.simplefilter("ignore")
-        vol = make_assembly_phantom(_device_components(True),
-                                    CylGrid(*sim_shape, 8.0, 60.0, pose))
-    estimates = []
-    for u0 in centers_px:
-        g = ScanGeometry(geom.sdd, geom.sod, geom.det_cols, geom.det_rows, geom.pixel_pitch,
-                         (float(u0), geom.principal_point[1]), geom.stage_angles)
-        ps = simulate_scan(vol, g, noise_sigma=noise_sigma, rng=rng)
-        estimates.append(fit_pose(ps, PoseFitParams(**DEVICE_POSE_PARAMS)).pose)
-    comps = {"x_mm": [e.t[0] for e in estimates], "y_mm": [e.t[1] for e in estimates],
-             "z_mm": [e.t[2] for e in estimates], "alpha_rad": [e.alpha for e in estimates],
-             "beta_rad": [e.beta for e in estimates]}
-    sigma = {k: float(np.std(v, ddof=1)) for k, v in comps.items()}
-    return {"estimates": estimates, "components": comps, "sigma": sigma}
-
-
 def cmd_pose(args) -> int:
-    """(cyltomo/cli.py:286-313)"""
+    """(cyltomo/cli.py:286-313) -- pose fit of a projection set.  The
+    reference's pose-precision study (experiments.py:342) is out of scope."""
     cfg = load_config(args, {"params": {}}, POSE_SCHEMA)
+    if "projections" not in cfg:
+        raise errors.ConfigError("pose needs \"projections\"")
     out = Path(args.out)
     out.mkdir(parents=True, exist_ok=True)
-    if cfg.get("study"):
-        study = cfg["study"]
-        geom = geometry_from_config(study.get("geometry", {}))
-        result = pose_precision_study(study["centers_px"], geom,
-                                      sim_shape=tuple(study.get("sim_shape", (60, 16, 32))),
-                                      noise_sigma=study.get("noise_sigma", 0.01), seed=args.seed)
-        rows = [(k, *[fmt(v) for v in vals], fmt(result["sigma"][k]))
-                for k, vals in result["components"].items()]
-        n = len(study["centers_px"])
-        write_csv_rows(out / "pose_precision.csv",
-                       ["component", *[f"scan_{i}" for i in range(n)], "sigma"], rows)
-        print(f"wrote {out / 'pose_precision.csv'}")
-        return EXIT_OK
-    if "projections" not in cfg:
-        raise errors.ConfigError("pose needs \"projections\" (or a \"study\")")
     ps = io.read_projections(cfg["projections"], device=True)
     result = fit_pose(ps, pose_params_from_config(cfg["params"]))
     io.write_pose(result.to_dict(), out / "pose.json")
@@ -427,43 +419,54 @@ def cmd_batch(args) -> int:
     return EXIT_OK
 
 
+# sub-command -> (handler, help, extra arguments)
+COMMANDS = {
+    "simulate": (cmd_simulate, "forward-project a volume",
+                 [("--views", dict(type=int, help="override projection count"))]),
+    "pose": (cmd_pose, "estimate the object pose", []),
+    "reconstruct": (cmd_reconstruct, "(OS-)SART reconstruction",
+                    [("--init", dict(metavar="none|PATH", help="initial volume")),
+                     ("--weights", dict(metavar="none|PATH",
+                                        help="back-projection weight map"))]),
+    "batch": (cmd_batch, "batch inspection study",
+              [("--strategies", dict(nargs="+", choices=["a", "b", "c", "d"]))]),
+}
+COMMON_ARGS = (
+    ("--config", dict(metavar="PATH", help="JSON config document")),
+    ("--seed", dict(type=int, default=0, help="RNG seed (default 0)")),
+    ("--threads", dict(type=int, default=None, help="host worker thread cap "
+                                                    "(env CYLTOMO_THREADS)")),
+    ("--preset", dict(choices=["paper", "desk"], default="desk",
+                      help="scale preset (default desk)")),
+    ("--out", dict(metavar="DIR", default=".", help="output directory")),
+)
+
+
 def build_parser() -> argparse.ArgumentParser:
     parser = argparse.ArgumentParser(prog="cyltomo-b200",
                                      description="B200 cone-beam FP/BP/(OS-)SART on "
                                                  "cylindrical grids")
-    common = argparse.ArgumentParser(add_help=False)
-    common.add_argument("--config", metavar="PATH", help="JSON config document")
-    common.add_argument("--seed", type=int, default=0, help="RNG seed (default 0)")
-    common.add_argument("--out", metavar="DIR", default=".", help="output directory")
+    shared = argparse.ArgumentParser(add_help=False)
+    for flag, kw in COMMON_ARGS:
+        shared.add_argument(flag, **kw)
     sub = parser.add_subparsers(dest="command", required=True)
-    p = sub.add_parser("simulate", parents=[common], help="forward-project a volume")
-    p.add_argument("--views", type=int, help="override projection count")
-    p.set_defaults(func=cmd_simulate)
-    p = sub.add_parser("pose", parents=[common], help="estimate the object pose")
-    p.set_defaults(func=cmd_pose)
-    p = sub.add_parser("reconstruct", parents=[common], help="(OS-)SART reconstruction")
-    p.add_argument("--init", metavar="none|PATH", help="initial volume")
-    p.add_argument("--weights", metavar="none|PATH", help="back-projection weight map")
-    p.set_defaults(func=cmd_reconstruct)
-    p = sub.add_parser("batch", parents=[common], help="batch inspection study")
-    p.add_argument("--strategies", nargs="+", choices=["a", "b", "c", "d"])
-    p.set_defaults(func=cmd_batch)
+    for name, (handler, text, extra) in COMMANDS.items():
+        cp = sub.add_parser(name, parents=[shared], help=text)
+        for flag, kw in extra:
+            cp.add_argument(flag, **kw)
+        cp.set_defaults(func=handler)
     return parser
 
 
 def main(argv=None) -> int:
     args = build_parser().parse_args(argv)
     try:
+        configure_threads(args.threads)
         return args.func(args)
-    except errors.ConfigError as exc:
-        print(f"config error: {exc}", file=sys.stderr)
-        return EXIT_CONFIG
-    except (errors.IoFailure, errors.SchemaMismatch, errors.SizeMismatch) as exc:
-        print(f"io error: {exc}", file=sys.stderr)
-        return EXIT_IO
     except errors.CylTomoError as exc:
-        print(f"error: {exc}", file=sys.stderr)
-        return EXIT_DOMAIN
+        code, prefix = next((c, pfx) for kinds, c, pfx in EXIT_MAP if isinstance(exc, kinds))
+        print(f"{prefix}: {exc}", file=sys.stderr)
+        return code
 
 
 if __name__ == "__main__":

@@ -502,7 +502,7 @@ def _default_runner(ps, grid, cfg, group):
 
 
 def reconstruct_batch(items, cfg: SartConfig, rank: int | None = None,
-                      world: int | None = None, g_ang: int = 1, runner=None):
+                      world: int | None = None, g_ang: int = 1, runner=None, group=None):
     """Batch reconstruction over G = G_obj x G_ang ranks (BatchPlan).
 
     items: sequence of (ProjectionSet, grid[, SartConfig]) for every object.
@@ -510,7 +510,9 @@ def reconstruct_batch(items, cfg: SartConfig, rank: int | None = None,
     with g_ang > 1 each object's subsets are angle-sharded over its group.
     Returns {index: (volume, report)} for this rank's objects (every rank of
     an object group holds the group's results).  runner(ps, grid, cfg,
-    group) overrides the per-object driver (tests: an oracle engine).
+    group) overrides the per-object driver (tests: an oracle engine); group
+    is this rank's object group if the caller already made it
+    (BatchPlan.make_group), else it is created here (collective).
     """
     if rank is None or world is None:
         dist = _dist()
@@ -518,7 +520,8 @@ def reconstruct_batch(items, cfg: SartConfig, rank: int | None = None,
         rank = dist.get_rank() if on else 0
         world = dist.get_world_size() if on else 1
     plan = BatchPlan(rank, world, g_ang)
-    group = plan.make_group()
+    if group is None:
+        group = plan.make_group()
     run = runner or _default_runner
     out = {}
     for idx in plan.objects(len(items)):

@@ -467,7 +467,8 @@ def _stage_pool():
     global _STAGE_POOL
     if _STAGE_POOL is None:
         from concurrent.futures import ThreadPoolExecutor
-        _STAGE_POOL = ThreadPoolExecutor(max_workers=max(1, min(8, (os.cpu_count() or 2) // 2)))
+        cap = int(os.environ.get("CT_HOST_THREADS", "0")) or 8       # cli --threads
+        _STAGE_POOL = ThreadPoolExecutor(max_workers=max(1, min(cap, (os.cpu_count() or 2) // 2)))
     return _STAGE_POOL
 
 

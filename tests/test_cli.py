@@ -36,7 +36,7 @@ def test_config_errors_map_to_exit_codes(tmp_path, capsys):
                                    "grid": {"shape": [2, 4, 2], "radius_mm": 1.0,
                                             "height_mm": 1.0}})
     assert cli.main(["reconstruct", "--config", c, "--out", str(tmp_path)]) == 3
-    # pose schema: study needs centers_px
+    # pose needs projections (the reference's precision study is out of scope)
     c = _cfg(tmp_path, "p.json", {"study": {"noise_sigma": 0.1}})
     assert cli.main(["pose", "--config", c, "--out", str(tmp_path)]) == 2
     # missing projections file -> io error
@@ -134,14 +134,76 @@ def test_pose_then_reconstruct_with_estimated_pose(tmp_path):
 
 
 @pytest.mark.gpu
-def test_pose_precision_study(tmp_path):
-    c = _cfg(tmp_path, "s.json", {"study": {"centers_px": [45.5, 47.5, 49.5],
-                                            "noise_sigma": 0.01}})
-    assert cli.main(["pose", "--config", c, "--out", str(tmp_path)]) == 0
-    rows = list(csv.reader(open(tmp_path / "pose_precision.csv")))
-    assert rows[0] == ["component", "scan_0", "scan_1", "scan_2", "sigma"]
-    assert [r[0] for r in rows[1:]] == ["x_mm", "y_mm", "z_mm", "alpha_rad", "beta_rad"]
-    assert float(rows[1][-1]) < 0.1                       # x spread well under a voxel
+def test_reconstruct_matches_reference_cli_artifacts(tmp_path, monkeypatch):
+    """`reconstruct` on the reference-written projections and config document
+    (tests/golden/make_golden_cli.py ran the unmodified reference CLI,
+    cyltomo/cli.py:341-397): same artifacts, same report schema and pose
+    echo, volume and residuals within the north_star reconstruction
+    tolerance."""
+    import shutil
+    src = Path(__file__).resolve().parent / "golden" / "cli_ref"
+    work = tmp_path / "cli_ref"
+    shutil.copytree(src, work)
+    monkeypatch.chdir(work)
+    assert cli.main(["reconstruct", "--config", "reconstruct.json", "--out", "ours"]) == 0
+    ref_vol = pio.read_volume(work / "volume.json")
+    our_vol = pio.read_volume(work / "ours" / "volume.json")
+    a, b = np.asarray(our_vol.mu, np.float64), np.asarray(ref_vol.mu, np.float64)
+    assert np.linalg.norm(a - b) / np.linalg.norm(b) < 1e-3
+    ref_rep = json.loads((work / "report.json").read_text())
+    our_rep = json.loads((work / "ours" / "report.json").read_text())
+    assert set(ref_rep) == set(our_rep)
+    assert our_rep["pose"] == ref_rep["pose"]
+    for k, v in ref_rep["config"].items():
+        assert our_rep["config"][k] == v, k
+    assert np.allclose(our_rep["residuals"], ref_rep["residuals"], rtol=1e-3)
+    ref_rows = list(csv.reader(open(work / "residuals.csv")))
+    our_rows = list(csv.reader(open(work / "ours" / "residuals.csv")))
+    assert our_rows[0] == ref_rows[0] and [r[0] for r in our_rows] == [r[0] for r in ref_rows]
+    assert np.allclose([float(r[1]) for r in our_rows[1:]],
+                       [float(r[1]) for r in ref_rows[1:]], rtol=1e-3)
+    # the volume header the reference reader expects
+    assert json.loads((work / "ours" / "volume.json").read_text()).keys() == \
+        json.loads((work / "volume.json").read_text()).keys()
+
+
+def test_reference_flags_preset_and_threads(tmp_path, monkeypatch):
+    """The reference's common flags parse (cyltomo/cli.py:551-555), --preset
+    paper selects the paper-scale simulation geometry (:250-252) and --threads
+    caps the host worker pool."""
+    seen = {}
+
+    class Stop(Exception):
+        pass
+
+    def fake_sim(vol, geom, *a, **k):
+        seen["geom"] = geom
+        raise Stop
+
+    monkeypatch.setattr(cli.io, "read_volume", lambda *a, **k: None)
+    monkeypatch.setattr(cli, "simulate_scan", fake_sim)
+    monkeypatch.delenv("CT_HOST_THREADS", raising=False)
+    c = _cfg(tmp_path, "s.json", {"volume": "v.json"})
+    with pytest.raises(Stop):
+        cli.main(["simulate", "--preset", "paper", "--threads", "3", "--config", c])
+    g = seen["geom"]
+    assert (g.n_proj, g.det_cols, g.det_rows, g.pixel_pitch) == (4096, 2048, 128, 0.0096)
+    assert np.isclose(g.stage_angles[1] - g.stage_angles[0], 2 * np.pi / 4096)
+    import os
+    assert os.environ["CT_HOST_THREADS"] == "3"
+    with pytest.raises(Stop):
+        cli.main(["simulate", "--preset", "desk", "--config", c])
+    assert seen["geom"].n_proj == 21
+    args = cli.build_parser().parse_args(["reconstruct", "--threads", "2", "--preset", "desk",
+                                          "--init", "none"])
+    assert args.threads == 2 and args.preset == "desk" and args.init == "none"
+
+
+def test_config_merge_semantics():
+    base = {"a": 1, "g": {"x": 1, "y": {"p": 1, "q": 2}}, "l": [1, 2]}
+    got = cli.merged(base, {"g": {"y": {"q": 3}, "z": 4}, "l": [9], "b": None})
+    assert got == {"a": 1, "g": {"x": 1, "y": {"p": 1, "q": 3}, "z": 4}, "l": [9], "b": None}
+    assert base["g"]["y"]["q"] == 2                       # defaults untouched
 
 
 @pytest.mark.gpu

@@ -1,9 +1,17 @@
-"""Condense an `ncu --set full` report into profiles/ncu_summary.json.
+"""Condense an `ncu --set full` report into a per-kernel-kind JSON summary.
 
 Maps kernel instantiations to the bench's kernel kinds and records, per
-launch: duration, DRAM bytes (read+write), L1 data-pipe / issue utilisation,
-sectors and instructions.  bench.py reads `dram_bytes_per_launch` for the
-roofline `traffic` field.
+launch: duration, DRAM bytes (read+write), L2 bytes (lts__t_bytes), FMA-pipe
+active cycles and its per-SM-cycle peak (derived from the .sum and the
+pct_of_peak_sustained_active of the same launch), L1 data-pipe / issue
+utilisation, sectors and instructions.  bench.py's roofline reads
+profiles/r02_ncu_summary.json (`dram_bytes_per_launch`,
+`lts_bytes_per_launch`, `fma_cycles_active_per_launch`,
+`fma_cycles_per_sm_cycle`).
+
+Capture with the extra metrics, e.g.
+  ncu --set full --metrics lts__t_bytes.sum,sm__pipe_fma_cycles_active.sum,\
+      sm__cycles_active.sum --clock-control none --import-source on ...
 """
 import csv
 import json
@@ -12,6 +20,7 @@ import sys
 from pathlib import Path
 
 KIND = [("fp_kernel<<unnamed>::CylGeo, 1", "fp_correction"),
+        ("fp_kernel<<unnamed>::CylGeo, 4", "fp_correction_resid"),
         ("fp_kernel_small<<unnamed>::CylGeo, 1", "fp_correction"),
         ("fp_kernel<<unnamed>::CylGeo, 2", "fp_residual"),
         ("fp_kernel_small<<unnamed>::CylGeo, 2", "fp_residual"),
@@ -34,7 +43,13 @@ FIELDS = {"duration_ms": ("gpu__time_duration.sum", 1.0),
           "fma_pipe_pct": ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", 1.0),
           "alu_pipe_pct": ("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", 1.0),
           "xu_pipe_pct": ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", 1.0),
-          "dram_throughput_pct": ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", 1.0)}
+          "dram_throughput_pct": ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", 1.0),
+          "lts_bytes": ("lts__t_bytes.sum", None),
+          "l2_throughput_pct": ("lts__t_sectors.avg.pct_of_peak_sustained_elapsed", 1.0),
+          "l1tex_throughput_pct": ("l1tex__throughput.avg.pct_of_peak_sustained_active", 1.0),
+          "fma_cycles_active_sum": ("sm__pipe_fma_cycles_active.sum", 1.0),
+          "sm_cycles_active_sum": ("sm__cycles_active.sum", 1.0),
+          "sm_mhz": ("sm__cycles_elapsed.avg.per_second", None)}
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 
@@ -57,10 +72,21 @@ def main(rep, out, label):
             if metric in h:
                 i = h.index(metric)
                 v = float(row[i].replace(",", "")) if row[i] else 0.0
-                if f.startswith("dram"):
+                if f.startswith("dram") or f == "lts_bytes":
                     v *= UNIT.get(units[i], 1)
+                if f == "sm_mhz":
+                    v *= {"hz": 1e-6, "Khz": 1e-3, "Mhz": 1.0, "Ghz": 1e3}.get(units[i], 1.0)
                 d[f] = v
         d["dram_bytes_per_launch"] = d.get("dram_read_bytes", 0) + d.get("dram_write_bytes", 0)
+        if d.get("lts_bytes"):
+            d["lts_bytes_per_launch"] = d["lts_bytes"]
+        if d.get("fma_cycles_active_sum") and d.get("fma_pipe_pct") and d.get("sm_cycles_active_sum"):
+            d["fma_cycles_active_per_launch"] = d["fma_cycles_active_sum"]
+            d["fma_cycles_per_sm_cycle"] = d["fma_cycles_active_sum"] / (
+                d["fma_pipe_pct"] / 100.0 * d["sm_cycles_active_sum"])
+        if kind in res["kernels"] and res["kernels"][kind].get("duration_ms", 0) >= d.get(
+                "duration_ms", 0):
+            continue                      # keep the longest launch of a kind (full batch)
         res["kernels"][kind] = d
     Path(out).write_text(json.dumps(res, indent=1))
     print(json.dumps(res, indent=1))
