@@ -54,8 +54,12 @@ UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 
 def main(rep, out, label):
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
+    if rep.endswith(".csv"):                 # the raw page already exported on the box
+        txt = Path(rep).read_text()
+    else:
+        txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
+    txt = txt[txt.index('"ID"'):] if '"ID"' in txt else txt
     r = list(csv.reader(txt.splitlines()))
     h, units, rows = r[0], r[1], r[2:]
     ki = h.index("Kernel Name")
