@@ -49,7 +49,11 @@ FIELDS = {"duration_ms": ("gpu__time_duration.sum", 1.0),
           "l1tex_throughput_pct": ("l1tex__throughput.avg.pct_of_peak_sustained_active", 1.0),
           "fma_cycles_active_sum": ("sm__pipe_fma_cycles_active.sum", 1.0),
           "sm_cycles_active_sum": ("sm__cycles_active.sum", 1.0),
-          "sm_mhz": ("sm__cycles_elapsed.avg.per_second", None)}
+          "sm_mhz": ("sm__cycles_elapsed.avg.per_second", None),
+          "sm_cycles_elapsed_avg": ("sm__cycles_elapsed.avg", 1.0),
+          "l1_wavefronts_avg_per_sm": ("l1tex__data_pipe_lsu_wavefronts.avg", 1.0),
+          "fmaheavy_pipe_pct": ("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
+                                1.0)}
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 
@@ -73,8 +77,10 @@ def main(rep, out, label):
             continue
         d = {"kernel": name[:120]}
         for f, (metric, _) in FIELDS.items():
-            if metric in h:
-                i = h.index(metric)
+            # some metrics carry a section prefix ("SM_A.TriageCompute.<metric>")
+            cands = [j for j, n in enumerate(h) if n == metric or n.endswith("." + metric)]
+            if cands:
+                i = cands[0]
                 v = float(row[i].replace(",", "")) if row[i] else 0.0
                 if f.startswith("dram") or f == "lts_bytes":
                     v *= UNIT.get(units[i], 1)
@@ -88,6 +94,12 @@ def main(rep, out, label):
             d["fma_cycles_active_per_launch"] = d["fma_cycles_active_sum"]
             d["fma_cycles_per_sm_cycle"] = d["fma_cycles_active_sum"] / (
                 d["fma_pipe_pct"] / 100.0 * d["sm_cycles_active_sum"])
+        if d.get("l1_wavefronts_avg_per_sm") and d.get("l1_data_pipe_pct") and \
+                d.get("sm_cycles_elapsed_avg"):
+            # data-pipe wavefronts per launch (all SMs) and the per-SM-cycle peak
+            d["l1_wavefronts_per_launch"] = 148 * d["l1_wavefronts_avg_per_sm"]
+            d["l1_wavefronts_per_sm_cycle"] = d["l1_wavefronts_avg_per_sm"] / (
+                d["l1_data_pipe_pct"] / 100.0 * d["sm_cycles_elapsed_avg"])
         if kind in res["kernels"] and res["kernels"][kind].get("duration_ms", 0) >= d.get(
                 "duration_ms", 0):
             continue                      # keep the longest launch of a kind (full batch)
