@@ -446,6 +446,7 @@ struct CylGeo {
   unsigned cell_kstride, cell_jstride, jb_wrap;
   double cells_layer;   // real cells per layer (rows x columns)
   const float4* __restrict__ qraw;   // GL_QUAD bricked layout (CT_QUAD_BRICK)
+  unsigned long long qtex = 0;       // CT_QUAD_TEX: texture object over qraw (A/B)
   unsigned brick_j, brick_i;         // GL_OCTB bricks per layer: rows / 2, columns / 2
   unsigned qbrick_j, qbrick_i;       // GL_QUAD bricks per layer pair
 
@@ -684,6 +685,7 @@ struct CartGeo {
   unsigned cell_kstride, cell_jstride;   // gather layout (nz+1, ny+1, nx+1), strides (ks, js, 1)
   double cells_layer;
   const float4* __restrict__ qraw;
+  unsigned long long qtex = 0;
   unsigned brick_j, brick_i, qbrick_j, qbrick_i;
 
   __host__ void init(const float* m, const float* gather, const ct_cart_grid& g) {

@@ -49,6 +49,26 @@ enum FpLayout { GL_PLAIN = 0, GL_OCT = 1, GL_QUAD = 2, GL_OCTB = 3 };
 #ifndef CT_FP_WW1
 #define CT_FP_WW1 4              // warp patch width at one lane per ray
 #endif
+// Depth-aligned march (A/B only, rejected): the lanes of a warp step through
+// their samples in lockstep by depth along the view direction instead of by
+// their own sample index, so that at every step the warp's 32 samples lie
+// near one plane across the rays -- the hypothesis being fewer distinct
+// 128-byte lines per quarter-warp load (L1TEX data-pipe wavefronts: one per
+// distinct line per 8 lanes, tools/microbench/l1_wavefronts.cu).  Measured
+// (C5 correction FP, ncu): 8.16 wavefronts per request either way (the lanes'
+// cells are one pixel apart, not misaligned in depth), +10 % instructions for
+// the per-sample validity: C5 0.276 -> 0.289 s (1 chain, =2) / 0.316 s (2
+// chains, =1), C2 192 -> 227 / 237 ms.
+#ifndef CT_FP_ALIGN
+#define CT_FP_ALIGN 0
+#endif
+// CT_QUAD_TEX (A/B): GL_QUAD cell loads through the texture pipe (a linear
+// float4 texture over the gather buffer) instead of LSU global loads -- 1: the
+// second layer of a cell only (splits the loads across the two L1TEX input
+// pipes), 2: both layers
+#ifndef CT_QUAD_TEX
+#define CT_QUAD_TEX 0
+#endif
 constexpr int FP_WX = CT_FP_WX, FP_WY = CT_FP_WY, FP_CHAINS = CT_FP_CHAINS, FP_UNROLL = CT_FP_UNROLL;
 static_assert(FP_CHAINS == 2 || FP_CHAINS == 4, "FP_CHAINS");
 constexpr int FP_THREADS = 32 * FP_WX * FP_WY;
@@ -162,8 +182,16 @@ __device__ __forceinline__ float march_linear(const Geo& geo, const RayF& ry, in
              4LL * ((long long)idx + 1) <= geo.dbg_floats);
 #endif
       if (idx != ch.prev) {
+#if CT_QUAD_TEX >= 2
+        const float4 a = tex1Dfetch<float4>(geo.qtex, (int)idx);
+#else
         const float4 a = ld_vquad(geo.qraw + idx);
+#endif
+#if CT_QUAD_TEX >= 1
+        const float4 b = tex1Dfetch<float4>(geo.qtex, (int)geo.template quad_cell<WRAP>(c, 1u));
+#else
         const float4 b = ld_vquad(geo.qraw + geo.template quad_cell<WRAP>(c, 1u));
+#endif
 #else
       const unsigned idx = geo.template gather_index<WRAP>(c);
       if (idx != ch.prev) {
@@ -237,18 +265,133 @@ __device__ __forceinline__ float march_linear(const Geo& geo, const RayF& ry, in
   return sum;
 }
 
+// Depth-aligned march of the interior samples [0, n_int) of a ray whose
+// first sample has global depth index D (CT_FP_ALIGN): the warp's depth range
+// [G0, G1) is split at Gm into two chains marched in lockstep (chain 0 covers
+// depths [G0, Gm), chain 1 [Gm, G1)); at iteration j chain c of this lane
+// holds its sample k = base_c - D + j, valid when 0 <= k < end_c.  Cells are
+// loaded only for valid samples that leave the chain's live cell; invalid
+// samples contribute nothing.  + the last sample k_last when with_last.
+template <class Geo, int OCT, bool WRAP>
+__device__ __forceinline__ float march_aligned(const Geo& geo, const RayF& ry, int D, int n_int,
+                                               int G0, int G1, bool with_last, float k_last) {
+  struct Chain {
+    unsigned prev = 0x80000000u;
+    float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pb = make_float4(0.f, 0.f, 0.f, 0.f);
+    float sum = 0.0f;
+  };
+  auto value = [&](Chain& ch, const Cell& c, bool valid) -> float {
+    unsigned idx;
+    if (OCT == GL_OCTB) {
+      idx = geo.template oct_cell<WRAP>(c);
+      if (valid && idx != ch.prev) ld_cell(geo.qraw + 2 * (size_t)idx, ch.pa, ch.pb);
+    } else if (OCT == GL_OCT) {
+      idx = geo.template gather_index<WRAP>(c);
+      if (valid && idx != ch.prev) ld_cell(geo.oct + 2 * cell_off(idx), ch.pa, ch.pb);
+    } else if (OCT == GL_PLAIN) {
+      // the same 8 values from mu, coefficients in-kernel (identical bits)
+      idx = 0u;
+      if (valid) {
+        float4 a, b;
+        geo.fetch_plain(c, a, b);
+        trilinear_coeffs(a, b, ch.pa, ch.pb);
+      }
+      return trilinear_eval(ch.pa, ch.pb, c.w0, c.w1, c.w2);
+    } else {
+      idx = geo.template quad_cell<WRAP>(c, 0u);
+      if (valid && idx != ch.prev) {
+        const float4 a = ld_vquad(geo.qraw + idx);
+        const float4 b = ld_vquad(geo.qraw + geo.template quad_cell<WRAP>(c, 1u));
+        ch.pa = a;
+        float x0, x1, y0, y1;
+        upk(sub2(pk(b.x, b.y), pk(a.x, a.y)), x0, x1);
+        upk(sub2(pk(b.z, b.w), pk(a.z, a.w)), y0, y1);
+        ch.pb = make_float4(x0, x1, y0, y1);
+      }
+    }
+    ch.prev = valid ? idx : ch.prev;
+    return trilinear_eval(ch.pa, ch.pb, c.w0, c.w1, c.w2);
+  };
+#if CT_FP_ALIGN == 2
+  // one chain: two consecutive samples per f32x2 locate
+  Chain ch;
+  const int T = G1 - G0;                        // <= 0: no interior samples in the warp
+  int k = G0 - D;
+  const unsigned e = (unsigned)n_int;
+  f32x2 KF = pk((float)k, (float)(k + 1));
+#pragma unroll FP_UNROLL
+  for (int j = 0; j < T; j += 2) {
+    Cell c0, c1;
+    geo.locate2(KF, ry, c0, c1);
+    KF = add2(KF, dup2(2.0f));
+    const bool v0 = (unsigned)k < e, v1 = (unsigned)(k + 1) < e;
+    k += 2;
+    const float a0 = value(ch, c0, v0);
+    const float a1 = value(ch, c1, v1);
+    ch.sum += (v0 ? a0 : 0.0f) + (v1 ? a1 : 0.0f);
+  }
+  float sum = ch.sum;
+  if (with_last) sum += value(ch, geo.locate1(k_last, ry), true);
+  return sum;
+#else
+  Chain ch0, ch1;
+  // G0 > G1: no lane of the warp has interior samples
+  const int Gm = G1 >= G0 ? G0 + (G1 - G0 + 1) / 2 : G0;
+  const int T = Gm - G0;                        // >= G1 - Gm
+  int k0 = G0 - D;                              // chain 0's sample; chain 1's is k0 + T
+  const unsigned e0 = (unsigned)max(0, min(n_int, Gm - D)), e1 = (unsigned)n_int;
+  f32x2 KF = pk((float)k0, (float)(k0 + T));
+#pragma unroll FP_UNROLL
+  for (int j = 0; j < T; j += 2) {
+    Cell c0, c1, c2, c3;
+    geo.locate2(KF, ry, c0, c1);
+    geo.locate2(add2(KF, dup2(1.0f)), ry, c2, c3);
+    KF = add2(KF, dup2(2.0f));
+    // (unsigned)k < end: 0 <= k < end in one compare
+    const int k1 = k0 + T;
+    const bool v0 = (unsigned)k0 < e0, v1 = (unsigned)k1 < e1;
+    const bool v2 = (unsigned)(k0 + 1) < e0, v3 = (unsigned)(k1 + 1) < e1;
+    k0 += 2;
+    const float a0 = value(ch0, c0, v0);
+    const float b0 = value(ch1, c1, v1);
+    const float a1 = value(ch0, c2, v2);
+    const float b1 = value(ch1, c3, v3);
+    ch0.sum += (v0 ? a0 : 0.0f) + (v2 ? a1 : 0.0f);
+    ch1.sum += (v1 ? b0 : 0.0f) + (v3 ? b1 : 0.0f);
+  }
+  float sum = ch0.sum + ch1.sum;
+  if (with_last) sum += value(ch1, geo.locate1(k_last, ry), true);
+  return sum;
+#endif
+}
+
 // One sub-ray, chunk `chunk` of `K`: returns this chunk's in-support sample
 // count and adds the fp32 sum of its interpolated values into acc (COUNT_ONLY:
 // chunk 0 returns the whole ray's count, without marching).
 template <class Geo, bool NEAREST, int OCT, bool COUNT_ONLY>
 __device__ __forceinline__ int march(const Geo& geo, const ct_ray_view& v, double cu, double cv,
-                                     double step, float& acc, int chunk, int K) {
+                                     double step, float& acc, int chunk, int K, bool present) {
+  // ALIGNED: every lane of the warp arrives here (present or not) -- the
+  // warp's depth range is a full-warp reduction
+  constexpr bool ALIGNED = CT_FP_ALIGN && !NEAREST && !COUNT_ONLY;
+  const bool aligned = ALIGNED && K == 1;
   double d[3];
-  subray_dir(v, cu, cv, d);
-  double t0, t1;
-  if (!geo.interval(v.src, d, t0, t1)) return 0;
-  if (t1 <= t0) return 0;
-  const int n = (int)ceil(ddiv(dsub(t1, t0), step));
+  double t0 = 0.0, t1 = 0.0;
+  bool hit = false;
+  if (present) {
+    subray_dir(v, cu, cv, d);
+    hit = geo.interval(v.src, d, t0, t1) && t1 > t0;
+  }
+  int n = 0;
+  if (hit) n = (int)ceil(ddiv(dsub(t1, t0), step));
+  int G0 = 0, G1 = 0, D = 0;
+  if (aligned) {
+    D = hit ? (int)floor(ddiv(t0, step)) : 0;     // depth index of the ray's first sample
+    const bool interior = hit && n > 1;
+    G0 = __reduce_min_sync(0xffffffffu, interior ? D : INT_MAX);
+    G1 = __reduce_max_sync(0xffffffffu, interior ? D + n - 1 : INT_MIN);
+  }
+  if (!hit) return 0;
   const double t_last = dadd(t0, dmul((double)(n - 1) + 0.5, step));
   const bool last_in = geo.inside(v.src, d, t_last);
   if (COUNT_ONLY) return chunk == 0 ? n - 1 + (last_in ? 1 : 0) : 0;
@@ -297,10 +440,17 @@ __device__ __forceinline__ int march(const Geo& geo, const ct_ray_view& v, doubl
   const bool with_last = own_last && last_in && geo.interp_nonzero(v.src, d, t_last);
   // rays crossing theta = 2 pi need the wrapped cell index; the choice is
   // warp-uniform so the two loop versions never diverge within a warp
-  if (__any_sync(__activemask(), ry.wrap))
+  const bool wrap = __any_sync(__activemask(), ry.wrap);
+  if (ALIGNED && aligned) {
+    if (wrap)
+      sum = march_aligned<Geo, OCT, true>(geo, ry, D, n_int, G0, G1, with_last, (float)n_int);
+    else
+      sum = march_aligned<Geo, OCT, false>(geo, ry, D, n_int, G0, G1, with_last, (float)n_int);
+  } else if (wrap) {
     sum = march_linear<Geo, OCT, true>(geo, ry, k, k_end, with_last, (float)n_int);
-  else
+  } else {
     sum = march_linear<Geo, OCT, false>(geo, ry, k, k_end, with_last, (float)n_int);
+  }
   acc += sum;
   return (k_end - (chunk * n_int) / K) + ((own_last && last_in) ? 1 : 0);
 }
@@ -340,21 +490,26 @@ __device__ __forceinline__ void fp_body(const FpArgs<Geo>& a) {
 
   float acc = 0.0f;
   int count = 0;
-  if (active && a.ss == 1) {
+  // every lane calls march (the depth-aligned march reduces over the whole
+  // warp); lanes off the detector or outside the row range march nothing.
+  // Row ranges are FP tile aligned (ct_fp_row_tile), i.e. whole warps.
+  if (a.ss == 1) {
     // one sub-ray at the pixel centre ((0 + .5)/1 - .5 = 0 exactly): the view
     // basis is dead after the per-ray setup, keeping the march loop's
     // register footprint small
-    count = march<Geo, NEAREST, OCT, EPI == EPI_ROWMAX || EPI == EPI_ROWCOUNT>(a.geo, a.views[vid], (double)col,
-                                                       (double)row, a.step, acc, chunk, K);
-  } else if (active) {
-    const ct_ray_view& v = a.views[vid];
+    count = march<Geo, NEAREST, OCT, EPI == EPI_ROWMAX || EPI == EPI_ROWCOUNT>(
+        a.geo, a.views[active ? vid : 0], (double)col, (double)row, a.step, acc, chunk, K,
+        active);
+  } else {
+    const ct_ray_view& v = a.views[active ? vid : 0];
     const int ss = a.ss;
     for (int sv = 0; sv < ss; ++sv) {
       const double off_v = dsub(ddiv((double)sv + 0.5, (double)ss), 0.5);
       for (int su = 0; su < ss; ++su) {
         const double off_u = dsub(ddiv((double)su + 0.5, (double)ss), 0.5);
         count += march<Geo, NEAREST, OCT, EPI == EPI_ROWMAX || EPI == EPI_ROWCOUNT>(
-            a.geo, v, dadd((double)col, off_u), dadd((double)row, off_v), a.step, acc, chunk, K);
+            a.geo, v, dadd((double)col, off_u), dadd((double)row, off_v), a.step, acc, chunk, K,
+            active);
       }
     }
   }
@@ -464,7 +619,7 @@ int check_batch(const ct_batch* b, const void* views, const ct_sampling* s) {
   return CT_OK;
 }
 
-#if CT_DEBUG_BOUNDS
+#if CT_DEBUG_BOUNDS || CT_QUAD_TEX
 int64_t gather_floats_cyl(const ct_cyl_grid& g);
 int64_t gather_floats_cart(const ct_cart_grid& g);
 inline int64_t gather_floats_of(const CylGeo& g) {
@@ -498,6 +653,34 @@ int launch_fp(const Geo& geo, const ct_ray_view* views, const ct_batch& b, const
   a.frow_hi = frow_hi;
 #if !CT_DEBUG_BOUNDS
   a.geo = geo;
+#endif
+#if CT_QUAD_TEX
+  if (geo.quad && geo.qraw) {
+    // one texture object per gather buffer, kept for the process lifetime
+    static const void* tex_ptr[8] = {};
+    static unsigned long long tex_obj[8] = {};
+    static int tex_n = 0;
+    int slot = -1;
+    for (int i = 0; i < tex_n; ++i)
+      if (tex_ptr[i] == geo.qraw) slot = i;
+    if (slot < 0) {
+      cudaResourceDesc rd = {};
+      rd.resType = cudaResourceTypeLinear;
+      rd.res.linear.devPtr = const_cast<float4*>(geo.qraw);
+      rd.res.linear.desc = cudaCreateChannelDesc<float4>();
+      rd.res.linear.sizeInBytes = (size_t)gather_floats_of(geo) * 4;
+      cudaTextureDesc td = {};
+      td.readMode = cudaReadModeElementType;
+      td.filterMode = cudaFilterModePoint;
+      cudaTextureObject_t t = 0;
+      if (cudaCreateTextureObject(&t, &rd, &td, nullptr) != cudaSuccess)
+        return check_launch("cudaCreateTextureObject");
+      slot = tex_n < 8 ? tex_n++ : 7;
+      tex_ptr[slot] = geo.qraw;
+      tex_obj[slot] = t;
+    }
+    a.geo.qtex = tex_obj[slot];
+  }
 #endif
   a.views = views;
   a.view_ids = b.view_ids;
