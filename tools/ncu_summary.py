@@ -4,6 +4,8 @@ import subprocess
 import sys
 
 KEYS = ['gpu__time_duration.sum', 'l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed',
+        'l1tex__data_pipe_lsu_wavefronts.avg', 'sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed',
+        'lts__t_sectors.avg.pct_of_peak_sustained_elapsed',
         'smsp__issue_active.avg.pct_of_peak_sustained_active',
         'l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum', 'l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum',
         'smsp__inst_executed.sum', 'sm__warps_active.avg.pct_of_peak_sustained_active',
@@ -18,16 +20,21 @@ KEYS = ['gpu__time_duration.sum', 'l1tex__data_pipe_lsu_wavefronts.avg.pct_of_pe
 
 
 def main(rep):
-    out = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True,
-                         text=True, check=True).stdout
+    if rep.endswith('.csv'):                 # raw page exported on the GPU box
+        out = open(rep).read()
+    else:
+        out = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True,
+                             text=True, check=True).stdout
     r = list(csv.reader(out.splitlines()))
-    h, units, rows = r[0], r[1], r[2:]
+    i0 = next(i for i, row in enumerate(r) if row and row[0] == 'ID')
+    h, units, rows = r[i0], r[i0 + 1], r[i0 + 2:]
     ki = h.index('Kernel Name')
     for row in rows:
         print('==', row[ki][:90])
         for k in KEYS:
-            if k in h:
-                i = h.index(k)
+            idx = [j for j, n in enumerate(h) if n == k or n.endswith('.' + k)]
+            if idx:
+                i = idx[0]
                 print(f"   {k:72s} {row[i]:>20s} {units[i]}")
         stalls = [(float(row[i] or 0), n) for i, n in enumerate(h)
                   if n.startswith('smsp__pcsamp_warps_issue_stalled') and not n.endswith('not_issued')]
