@@ -2,7 +2,54 @@
 // SART / OS-SART update (recon.py:105-119), and its footprint packing.
 #include "ct_common.cuh"
 
+#include <cuda.h>   // CUtensorMap (the TMA-staged BP variant, CT_BP_TMA)
+
 namespace {
+
+// TMA staging of the BP's footprint quads (A/B, run time CT_BP_TMA=1): per
+// view pair, each CTA's detector window (the bounding box of its 64 x 4 voxel
+// tile's footprints, from the tile's corner voxels) is brought into shared
+// memory with cp.async.bulk.tensor (one box of TMA_BU x bv quads per view,
+// mbarrier completion), and interior footprints inside the window read their
+// quad from shared memory instead of global/L1.  Windows that do not fit the
+// box, and footprints outside it, use the global path (same arithmetic).
+#ifndef CT_BP_TMA_BU
+#define CT_BP_TMA_BU 64
+#endif
+constexpr int TMA_BU = CT_BP_TMA_BU;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 4-D tile load (quads as FLOAT32 {4, cols, rows, n_batch}) into shared memory
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+      "r"(smem_u32(bar))
+      : "memory");
+}
 
 // ---------------------------------------------------------------------------
 // back-projection
@@ -110,6 +157,8 @@ struct BpArgs {
   ct_update upd;
   int vox_off, vox_end;   // voxels [vox_off, vox_end) (a rank's shard, distributed.py)
   int row0, nseg;         // first row of the range; CTAs per row group
+  int tma_bv;             // TMA: window rows (box dim 2); the box is TMA_BU x tma_bv quads
+  CUtensorMap tmap;       // TMA: the quads of the batch (CT_BP_TMA)
 };
 
 // fp64 re-evaluation of one voxel-view with the reference's arithmetic
@@ -195,9 +244,18 @@ __device__ __forceinline__ float2 bp_view_slow(const BpArgs<Vox>& a, int m, int 
 // the floor bit patterns, lerp-form bilinear in f32x2, den += 1 (the four
 // weights sum to 1); everything else goes through bp_view_slow.  num / den
 // accumulate per pair lane (even / odd batch slots) and are summed at the end.
-template <class Vox, int MODE, bool QUADS>
-__global__ void __launch_bounds__(BP_THREADS, BP_MIN_BLOCKS) bp_kernel(const __grid_constant__ BpArgs<Vox> a) {
+template <class Vox, int MODE, bool QUADS, bool TMA = false>
+__global__ void __launch_bounds__(BP_THREADS, TMA ? 4 : BP_MIN_BLOCKS) bp_kernel(const __grid_constant__ BpArgs<Vox> a) {
   __shared__ BpPairF sv[BP_CHUNK / 2];
+  // TMA: two windows (the views of a pair) in dynamic shared memory
+  extern __shared__ __align__(128) float4 win[];
+  __shared__ int2 worg[2];                 // window origin (u, v) per pair view; x = INT_MIN: none
+  __shared__ __align__(8) uint64_t tbar;
+  unsigned tphase = 0;
+  if (TMA && threadIdx.x == 0) {
+    mbar_init(&tbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   const int nr = a.vox.row_len();
   const int bs = (int)(blockIdx.x % (unsigned)a.nseg), bg = (int)(blockIdx.x / (unsigned)a.nseg);
   const int i = bs * BP_SEG + (threadIdx.x >> 5) * BP_PR + (threadIdx.x & (BP_PR - 1));
@@ -241,13 +299,68 @@ __global__ void __launch_bounds__(BP_THREADS, BP_MIN_BLOCKS) bp_kernel(const __g
           (unsigned)a.cols - 1u;
     }
     __syncthreads();
-    if (!active) continue;
+    if (!TMA && !active) continue;
     const float* __restrict__ img0 = a.corr + (size_t)c0 * npix;
     const int np = nc >> 1;
     unsigned slow = 0;   // pairs of this chunk for the slow path (BP_CHUNK / 2 <= 32)
 #pragma unroll BP_UNROLL
     for (int i = 0; i < np; ++i) {
       const BpPairF f = sv[i];
+      if (TMA) {
+        // corner voxels of the CTA tile (2 row ends x 4 rows) projected into
+        // both views of the pair: lanes 0-7 view 0, 8-15 view 1 of warp 0
+        __syncthreads();                     // the previous pair's windows are consumed
+        if (threadIdx.x < 32) {
+          const int l = (threadIdx.x >> 3) & 1, cidx = threadIdx.x & 7;
+          const int bs0 = (int)(blockIdx.x % (unsigned)a.nseg);
+          const int bg0 = (int)(blockIdx.x / (unsigned)a.nseg);
+          const int ci = min(bs0 * BP_SEG + (cidx & 1) * (BP_SEG - 1), nr - 1);
+          const int cq = a.row0 + bg0 * BP_PT + (cidx >> 1);
+          const long long cm = (long long)cq * nr + ci;
+          float umin = 3.0e38f, umax = -3.0e38f, vmin = 3.0e38f, vmax = -3.0e38f;
+          if (threadIdx.x < 16 && cm < a.vox.count()) {
+            double w64[3];
+            a.vox.world((int)cm, w64);
+            const float* fp = reinterpret_cast<const float*>(&sv[i]);
+            const float cphi = fp[0 + l], sphi = fp[2 + l], sod = fp[4 + l], sdd_p = fp[6 + l];
+            const float u0 = fp[8 + l], v0 = fp[10 + l];
+            const float xw0 = (float)w64[0], yw0 = (float)w64[1], zw0 = (float)w64[2];
+            const float xi = fmaf(cphi, xw0, sphi * -yw0);
+            const float depth = sod + fmaf(sphi, xw0, cphi * yw0);
+            const float sc = sdd_p / depth;
+            umin = umax = fmaf(xi, sc, u0) - 1.0f;   // u, v (the table holds u0 + 1, v0 + 1)
+            vmin = vmax = fmaf(zw0, sc, v0) - 1.0f;
+          }
+          for (int o = 1; o < 8; o <<= 1) {
+            umin = fminf(umin, __shfl_xor_sync(0xffffffffu, umin, o));
+            umax = fmaxf(umax, __shfl_xor_sync(0xffffffffu, umax, o));
+            vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
+            vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+          }
+          if (threadIdx.x == 0 || threadIdx.x == 8) {
+            // 1 px slack each side (fp32 corners vs the voxels' own projections)
+            const float ul = floorf(umin) - 1.0f, vl = floorf(vmin) - 1.0f;
+            const bool fits = umin < 1.0e30f && floorf(umax) + 2.0f - ul < (float)TMA_BU &&
+                              floorf(vmax) + 2.0f - vl < (float)a.tma_bv &&
+                              fabsf(ul) < 1.0e6f && fabsf(vl) < 1.0e6f;
+            worg[l] = fits ? make_int2((int)ul, (int)vl) : make_int2(INT_MIN, 0);
+          }
+        }
+        __syncthreads();
+        const int2 o0 = worg[0], o1 = worg[1];
+        const bool s0 = o0.x != INT_MIN, s1 = o1.x != INT_MIN && 2 * i + 1 < nc;
+        if (threadIdx.x == 0 && (s0 || s1)) {
+          const unsigned box = (unsigned)(TMA_BU * a.tma_bv * 16);
+          mbar_arrive_expect_tx(&tbar, box * ((s0 ? 1u : 0u) + (s1 ? 1u : 0u)));
+          if (s0) tma_load_4d(win, &a.tmap, &tbar, 0, o0.x, o0.y, c0 + 2 * i);
+          if (s1) tma_load_4d(win + TMA_BU * a.tma_bv, &a.tmap, &tbar, 0, o1.x, o1.y, c0 + 2 * i + 1);
+        }
+        if (s0 || s1) {
+          mbar_wait(&tbar, tphase);
+          tphase ^= 1u;
+        }
+        if (!active) continue;
+      }
       const f32x2 XI = fma2(f.cphi, XW, mul2(f.sphi, NYW));
       const f32x2 YI = fma2(f.sphi, XW, mul2(f.cphi, YW));
       const f32x2 DEPTH = add2(f.sod, YI);
@@ -280,7 +393,22 @@ __global__ void __launch_bounds__(BP_THREADS, BP_MIN_BLOCKS) bp_kernel(const __g
                  (long long)ob < (long long)a.n_batch * npix);
 #endif
           // one 16-byte footprint per view; lerp-form bilinear per lane
-          const float4 qa = ld_quad(a.quads + oa), qb = ld_quad(a.quads + ob);
+          float4 qa, qb;
+          if (TMA) {
+            // quad (iv, iu) = floor bits - magic - 1 (U1 = u + 1), window-relative
+            const int2 o0 = worg[0], o1 = worg[1];
+            const int lua = (int)(tu.x - kMagicBits) - 1 - o0.x, lva = (int)(tv.x - kMagicBits) - 1 - o0.y;
+            const int lub = (int)(tu.y - kMagicBits) - 1 - o1.x, lvb = (int)(tv.y - kMagicBits) - 1 - o1.y;
+            const bool ina = o0.x != INT_MIN && (unsigned)lua < (unsigned)TMA_BU &&
+                             (unsigned)lva < (unsigned)a.tma_bv;
+            const bool inb = o1.x != INT_MIN && (unsigned)lub < (unsigned)TMA_BU &&
+                             (unsigned)lvb < (unsigned)a.tma_bv;
+            qa = ina ? win[lva * TMA_BU + lua] : ld_quad(a.quads + oa);
+            qb = inb ? win[TMA_BU * a.tma_bv + lvb * TMA_BU + lub] : ld_quad(a.quads + ob);
+          } else {
+            qa = ld_quad(a.quads + oa);
+            qb = ld_quad(a.quads + ob);
+          }
           float fua, fub, fva, fvb;
           upk(FU, fua, fub);
           upk(FV, fva, fvb);
@@ -313,6 +441,7 @@ __global__ void __launch_bounds__(BP_THREADS, BP_MIN_BLOCKS) bp_kernel(const __g
     }
     // interior pairs: den += 1 per view, counted from the slow mask (no
     // per-pair counter in the hot loop)
+    if (TMA && !active) continue;          // (after the pair loop's barriers)
     nfast += 2 * (np - __popc(slow));
     // the chunk's pairs with a frame-edge / refine-band / near-source view:
     // recompute the projection per view (the same fp32 ops as the pair path)
@@ -390,6 +519,45 @@ __global__ void __launch_bounds__(BP_THREADS, BP_MIN_BLOCKS) bp_kernel(const __g
   }
 }
 
+bool bp_tma_enabled() {
+  const char* e = getenv("CT_BP_TMA");
+  return e && e[0] == '1';
+}
+int bp_tma_rows() {
+  const char* e = getenv("CT_BP_TMA_BV");
+  const int v = e ? atoi(e) : 12;
+  return v < 2 ? 2 : (v > 64 ? 64 : v);
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// The batch's footprint quads [n_batch][rows][cols] float4 as a 4-D FLOAT32
+// tensor {4, cols, rows, n_batch}; box {4, TMA_BU, bv, 1}; out-of-bounds
+// elements (windows past the frame) read as zero.
+int encode_quads_map(CUtensorMap* map, const float* quads, const ct_batch& b, int bv) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&fn),
+                                cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return set_err(CT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  }
+  const cuuint64_t dims[4] = {4, (cuuint64_t)b.det_cols, (cuuint64_t)b.det_rows,
+                              (cuuint64_t)b.n_batch};
+  const cuuint64_t strides[3] = {16, 16ull * b.det_cols, 16ull * b.det_cols * b.det_rows};
+  const cuuint32_t box[4] = {4, (cuuint32_t)TMA_BU, (cuuint32_t)bv, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(quads), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? CT_OK : set_err(CT_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+}
+
 template <class Vox, int MODE>
 int launch_bp(const Vox& vox, const float* corr, const float* quads, const ct_det_view* dets,
               const ct_batch& b, float* num, float* den, const ct_update* upd, cudaStream_t st,
@@ -416,6 +584,20 @@ int launch_bp(const Vox& vox, const float* corr, const float* quads, const ct_de
   a.nseg = (nr + BP_SEG - 1) / BP_SEG;
   const int64_t groups = (row_end - row0 + BP_PT - 1) / BP_PT;
   const unsigned blocks = (unsigned)(groups * a.nseg);
+  if (MODE == BP_UPDATE && quads && bp_tma_enabled()) {
+    a.tma_bv = bp_tma_rows();
+    int rc = encode_quads_map(&a.tmap, quads, b, a.tma_bv);
+    if (rc) return rc;
+    const int smem = 2 * TMA_BU * a.tma_bv * 16;
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(bp_kernel<Vox, MODE, true, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      attr_set = true;
+    }
+    bp_kernel<Vox, MODE, true, true><<<blocks, BP_THREADS, smem, st>>>(a);
+    return check_launch("bp_kernel (TMA)");
+  }
   if (quads)
     bp_kernel<Vox, MODE, true><<<blocks, BP_THREADS, 0, st>>>(a);
   else
