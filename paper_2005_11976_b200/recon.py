@@ -222,6 +222,18 @@ class SartEngine:
                C.byref(b), C.byref(self.samp), D.ptr(p_meas), D.ptr(self.row_thr), D.ptr(corr),
                D.stream_handle())
 
+    def correction_single(self, mu, p_view, i: int, slot, corr, gather=None) -> None:
+        """correction() of ONE table slot i (slot: device int32 [i]) whose
+        measured image p_view (1, H, W) is stored alone: the kernels address
+        p_meas by table slot, so the pointer handed over is p_view's address
+        minus i images (only image i is ever read)."""
+        b = D.batch_c(1, self.rows, self.cols, slot)
+        base = p_view.data_ptr() - i * self.rows * self.cols * 4
+        fn = "ct_fp_cyl_correction" if self.cyl else "ct_fp_cart_correction"
+        N.call(fn, D.ptr(mu), D.ptr(gather), C.byref(self.gc), D.ptr(self.fp_views),
+               C.byref(b), C.byref(self.samp), C.c_void_p(base), D.ptr(self.row_thr),
+               D.ptr(corr), D.stream_handle())
+
     def alloc_quads(self, n: int):
         """Buffer for the bilinear footprints of an n-view correction stack
         (None with CT_BP_QUADS=0: the BP reads the four taps from corr)."""
@@ -350,24 +362,98 @@ def _volume_cls(grid):
     return CylVolume if isinstance(grid, CylGrid) else CartVolume
 
 
+def _grid_key(grid) -> tuple:
+    if isinstance(grid, CylGrid):
+        p = grid.pose
+        return ("cyl", grid.shape, float(grid.radius), float(grid.height), float(p.alpha),
+                float(p.beta), float(p.gamma), tuple(float(x) for x in p.t))
+    return ("cart", grid.shape, float(grid.voxel_size), tuple(float(x) for x in grid.origin))
+
+
+def _geom_key(geom: ScanGeometry) -> tuple:
+    angles = np.ascontiguousarray(geom.stage_angles, dtype=np.float64)
+    return (float(geom.sdd), float(geom.sod), int(geom.det_cols), int(geom.det_rows),
+            float(geom.pixel_pitch), tuple(float(x) for x in geom.principal_point),
+            angles.size, hash(angles.tobytes()))
+
+
+class _ViewUpdater:
+    """Device state of the per-view SART entry point for one (grid, geometry,
+    sampling): the tables of ALL views, their row maxima (one launch, one
+    host copy -- EmptyView is decided per view from it), slot lists and a
+    correction buffer.  sart_update_view keeps a few of these keyed by the
+    CONTENT of grid / geometry / sampling, so a reference-style loop over
+    views pays the setup once instead of per call."""
+
+    def __init__(self, grid, geom: ScanGeometry, sampling: RaySamplingConfig):
+        torch = D.torch_mod()
+        self.eng = SartEngine(grid, geom, sampling)
+        # row maxima of every view (pure geometry): host copy for the per-view
+        # EmptyView decision, device skip thresholds for the correction FP
+        self.max_row = self.eng.row_max()
+        self.eng.row_thr = D.upload_f64(ROW_SUM_SKIP_FRACTION * self.max_row)
+        self.corr = torch.empty((1, self.eng.rows, self.eng.cols), dtype=torch.float32,
+                                device=self.eng.device)
+        self.slots = {}
+
+    def slot(self, i: int):
+        t = self.slots.get(i)
+        if t is None:
+            t = self.slots[i] = D.upload_i32([i])
+        return t
+
+    def device_weights(self, w, shape):
+        """The weight map on the device: a CUDA tensor as is, a host array
+        uploaded per call (the caller may change it between calls)."""
+        if w is None:
+            return None
+        if tuple(np.shape(w)) != tuple(shape):
+            raise ConfigError("weight map shape does not match the volume")
+        return D.to_device(w, device=self.eng.device)
+
+
+_VIEW_UPDATERS: dict = {}
+_VIEW_UPDATERS_MAX = 4
+
+
+def _view_updater(grid, geom: ScanGeometry, sampling: RaySamplingConfig) -> _ViewUpdater:
+    key = (_grid_key(grid), _geom_key(geom), sampling.step_for(grid), int(sampling.supersample),
+           sampling.interpolation)
+    u = _VIEW_UPDATERS.pop(key, None)
+    if u is None:
+        u = _ViewUpdater(grid, geom, sampling)
+        while len(_VIEW_UPDATERS) >= _VIEW_UPDATERS_MAX:
+            _VIEW_UPDATERS.pop(next(iter(_VIEW_UPDATERS)))
+    _VIEW_UPDATERS[key] = u                                # most recently used last
+    return u
+
+
 def sart_update_view(vol, ps: ProjectionSet, i: int, cfg: SartConfig):
     """Apply the SART correction of view i to the volume, in place
     (``cyltomo/recon.py:88-120``).  Raises EmptyView when no ray of the view
-    intersects the volume."""
+    intersects the volume.
+
+    Two launches per call (correction FP, fused BP update) on device state
+    cached per (grid, geometry, sampling) content; a CUDA-tensor volume is
+    updated in HBM without copies, a host array is uploaded and written back
+    (the reference mutates its float64 array in place)."""
     if ps.kind != LINE_INTEGRAL:
         raise ConfigError("SART needs line-integral projections")
-    torch = D.torch_mod()
+    if not isinstance(vol.grid, (CylGrid, CartGrid)):
+        raise TypeError(f"cannot reconstruct on {type(vol.grid).__name__}")
     i = int(i)
-    eng = SartEngine(vol.grid, ps.geom, cfg.sampling, views=[i])
-    eng.prepare_thresholds()
+    u = _view_updater(vol.grid, ps.geom, cfg.sampling)
+    if u.max_row[i] <= 0.0:
+        raise EmptyView(f"view {i} misses the volume entirely")
+    eng = u.eng
     dev = eng.device
     mu = D.to_device(vol.mu, device=dev)
-    weights = _device_weights(cfg, mu.shape, dev)
+    weights = u.device_weights(cfg.weights, mu.shape)
     p_meas = D.to_device(ps.images[i:i + 1], device=dev)
-    corr = torch.empty((1, eng.rows, eng.cols), dtype=torch.float32, device=dev)
-    slots = D.upload_i32([0])
-    eng.correction(mu, p_meas, slots, 1, corr)
-    eng.bp_update(corr, slots, 1, make_update(mu, weights, cfg))
+    # the tables hold all views: view i is slot i; p_meas holds only view i,
+    # so it is addressed as a one-view batch whose table slot is i
+    eng.correction_single(mu, p_meas, i, u.slot(i), u.corr)
+    eng.bp_update(u.corr, u.slot(i), 1, make_update(mu, weights, cfg))
     if is_device_array(vol.mu):
         if vol.mu.data_ptr() != mu.data_ptr():
             vol.mu.copy_(mu)

@@ -483,3 +483,35 @@ def test_quad_layout_sart_bit_identical(small_cyl_setup, monkeypatch):
     for o in out[1:]:
         assert np.array_equal(out[0][0], o[0])
         assert out[0][1] == o[1]
+
+
+def test_sart_update_view_reuses_device_state(small_cyl_setup, monkeypatch):
+    """A reference-style loop of sart_update_view calls builds the tables,
+    row maxima and buffers once per (grid, geometry, sampling) content, and
+    gives the same volume as the one-view-per-launch SartRun path."""
+    from paper_2005_11976_b200 import recon
+    grid, vol, ps = small_cyl_setup
+    built = []
+    orig = recon.SartEngine.__init__
+
+    def counting(self, *a, **k):
+        built.append(1)
+        orig(self, *a, **k)
+    monkeypatch.setattr(recon.SartEngine, "__init__", counting)
+    recon._VIEW_UPDATERS.clear()
+    init = (np.asarray(vol.mu) * 0.5).astype(np.float32)
+    work = CylVolume(grid, init.copy())
+    cfg = SartConfig(relaxation=0.7)
+    for i in range(ps.geom.n_proj):
+        sart_update_view(work, ps, i, cfg)
+    assert len(built) == 1
+    ref, _ = sart_run(ps, grid, SartConfig(relaxation=0.7, initial=CylVolume(grid, init.copy()),
+                                           compute_residuals=False))
+    assert np.array_equal(work.mu, ref.mu)
+    # a different geometry (content) gets its own state; the same content reuses it
+    built.clear()
+    geom2 = ps.geom.subset(list(range(ps.geom.n_proj))[::-1])
+    sart_update_view(work, ProjectionSet(geom2, np.asarray(ps.images)[::-1]), 0, cfg)
+    assert len(built) == 1
+    sart_update_view(work, ps, 1, cfg)
+    assert len(built) == 1
