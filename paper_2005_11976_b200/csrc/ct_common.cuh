@@ -392,6 +392,15 @@ __host__ __device__ __forceinline__ unsigned quad_brick_index(unsigned kc, unsig
          ((kc & ((1u << QB_LK) - 1u)) << (QB_LJ + QB_LI)) |
          ((jc & ((1u << QB_LJ) - 1u)) << QB_LI) | (ic & ((1u << QB_LI) - 1u));
 }
+// The bricked GL_QUAD cell of layer kc + 1 from that of layer kc: the next
+// slot of the brick, or (last layer of a brick) the first layer slot of the
+// next brick layer, brick_layer = cells per brick layer (jbr * ibr * 8).
+// Same value as quad_brick_index(kc + 1, jc, ic, ...), fewer integer ops.
+__host__ __device__ __forceinline__ unsigned quad_next_layer(unsigned idx, unsigned kc,
+                                                             unsigned brick_layer) {
+  constexpr unsigned kmask = (1u << QB_LK) - 1u, kstep = 1u << (QB_LJ + QB_LI);
+  return (kc & kmask) == kmask ? idx - kmask * kstep + brick_layer : idx + kstep;
+}
 // GL_OCTB: GL_OCT cells in 2x2 (row, column) bricks per layer, one 128-byte
 // line each (gather_obrick)
 __host__ __device__ __forceinline__ unsigned oct_brick_index(unsigned kc, unsigned jc,
@@ -449,6 +458,7 @@ struct CylGeo {
   unsigned long long qtex = 0;       // CT_QUAD_TEX: texture object over qraw (A/B)
   unsigned brick_j, brick_i;         // GL_OCTB bricks per layer: rows / 2, columns / 2
   unsigned qbrick_j, qbrick_i;       // GL_QUAD bricks per layer pair
+  unsigned qbrick_layer;             // GL_QUAD cells per brick layer (qbrick_j * qbrick_i * 8)
 
   __host__ void init(const float* m, const float* gather, const ct_cyl_grid& g) {
     mu = m;
@@ -477,6 +487,7 @@ struct CylGeo {
     brick_i = ((unsigned)g.n_r + 2u) / 2u;
     qbrick_j = qbricks((unsigned)gather_rows(g.n_theta), QB_LJ);
     qbrick_i = qbricks((unsigned)g.n_r + 1u, QB_LI);
+    qbrick_layer = qbrick_j * qbrick_i * 8u;
     jb_wrap = B + (unsigned)g.n_theta;
   }
   // theta rows of the gather layout: indices -1 .. n_theta - 1 (see RayF)
@@ -638,6 +649,10 @@ struct CylGeo {
     return quad_brick_index(c.kb - kMagicBits + dk, jb - kMagicBits, c.ib - kMagicBits + 1u,
                             qbrick_j, qbrick_i);
   }
+  // the cell of layer kc + 1 (same row / column) from quad_cell(c, 0)
+  __device__ __forceinline__ unsigned quad_cell_up(const Cell& c, unsigned idx0) const {
+    return quad_next_layer(idx0, c.kb - kMagicBits, qbrick_layer);
+  }
   template <bool WRAP>
   __device__ __forceinline__ unsigned oct_cell(const Cell& c) const {
     const unsigned jb = (WRAP && c.jb > jb_wrap) ? c.jb - (unsigned)nt : c.jb;
@@ -686,7 +701,7 @@ struct CartGeo {
   double cells_layer;
   const float4* __restrict__ qraw;
   unsigned long long qtex = 0;
-  unsigned brick_j, brick_i, qbrick_j, qbrick_i;
+  unsigned brick_j, brick_i, qbrick_j, qbrick_i, qbrick_layer;
 
   __host__ void init(const float* m, const float* gather, const ct_cart_grid& g) {
     mu = m;
@@ -713,6 +728,7 @@ struct CartGeo {
     brick_i = ((unsigned)nx + 2u) / 2u;
     qbrick_j = qbricks((unsigned)ny + 1u, QB_LJ);
     qbrick_i = qbricks((unsigned)nx + 1u, QB_LI);
+    qbrick_layer = qbrick_j * qbrick_i * 8u;
   }
 
   // _kernels.py:207-231
@@ -813,6 +829,9 @@ struct CartGeo {
   __device__ __forceinline__ unsigned quad_cell(const Cell& c, unsigned dk) const {
     return quad_brick_index(c.kb - kMagicBits + dk, c.jb - kMagicBits, c.ib - kMagicBits,
                             qbrick_j, qbrick_i);
+  }
+  __device__ __forceinline__ unsigned quad_cell_up(const Cell& c, unsigned idx0) const {
+    return quad_next_layer(idx0, c.kb - kMagicBits, qbrick_layer);
   }
   template <bool WRAP>
   __device__ __forceinline__ unsigned oct_cell(const Cell& c) const {

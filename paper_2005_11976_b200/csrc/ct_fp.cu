@@ -178,6 +178,7 @@ __device__ __forceinline__ float march_linear(const Geo& geo, const RayF& ry, in
 #if CT_QUAD_BRICK
       const unsigned idx = geo.template quad_cell<WRAP>(c, 0u);
 #if CT_DEBUG_BOUNDS
+      assert(geo.quad_cell_up(c, idx) == geo.template quad_cell<WRAP>(c, 1u));
       assert(4LL * ((long long)geo.template quad_cell<WRAP>(c, 1u) + 1) <= geo.dbg_floats &&
              4LL * ((long long)idx + 1) <= geo.dbg_floats);
 #endif
@@ -188,9 +189,9 @@ __device__ __forceinline__ float march_linear(const Geo& geo, const RayF& ry, in
         const float4 a = ld_vquad(geo.qraw + idx);
 #endif
 #if CT_QUAD_TEX >= 1
-        const float4 b = tex1Dfetch<float4>(geo.qtex, (int)geo.template quad_cell<WRAP>(c, 1u));
+        const float4 b = tex1Dfetch<float4>(geo.qtex, (int)geo.quad_cell_up(c, idx));
 #else
-        const float4 b = ld_vquad(geo.qraw + geo.template quad_cell<WRAP>(c, 1u));
+        const float4 b = ld_vquad(geo.qraw + geo.quad_cell_up(c, idx));
 #endif
 #else
       const unsigned idx = geo.template gather_index<WRAP>(c);
@@ -301,7 +302,7 @@ __device__ __forceinline__ float march_aligned(const Geo& geo, const RayF& ry, i
       idx = geo.template quad_cell<WRAP>(c, 0u);
       if (valid && idx != ch.prev) {
         const float4 a = ld_vquad(geo.qraw + idx);
-        const float4 b = ld_vquad(geo.qraw + geo.template quad_cell<WRAP>(c, 1u));
+        const float4 b = ld_vquad(geo.qraw + geo.quad_cell_up(c, idx));
         ch.pa = a;
         float x0, x1, y0, y1;
         upk(sub2(pk(b.x, b.y), pk(a.x, a.y)), x0, x1);
