@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define CT_ABI_VERSION 7
+#define CT_ABI_VERSION 8
 
 #define CT_OK 0
 #define CT_ERR_ARG (-1)   /* invalid argument (null pointer, bad size) */
@@ -211,6 +211,48 @@ int ct_fp_cart_residual_rows(const float *mu, const float *gather, const ct_cart
                              int64_t row_hi, int n_slots, double *scratch, ct_stream_t stream);
 int ct_residual_sum(const double *scratch, int64_t n, double *accum, ct_stream_t stream);
 
+/* Row bands (ABI v8; the slab decomposition of distributed.SlabSartRun): per
+ * view slot b, only detector rows [bands[2b], bands[2b+1]) are marched.
+ * bands is a DEVICE int32 array [n_batch][2]; every bands[2b] must be a
+ * multiple of ct_fp_row_tile() and band_rows >= max(bands[2b+1] - bands[2b]).
+ * Outputs land at their full-stack positions: the correction of (b, row,
+ * col) at corr[(b * det_rows + row) * det_cols + col] (rows outside the band
+ * untouched); residual partials at the n_slots-view slots of the full launch
+ * (see above), so disjoint bands of one view on different ranks fill
+ * disjoint slots.  _correction_bands with a scratch: both epilogues. */
+int ct_fp_cyl_correction_bands(const float *mu, const float *gather, const ct_cyl_grid *grid,
+                               const ct_ray_view *views, const ct_batch *batch,
+                               const ct_sampling *sampling, const float *p_meas,
+                               const double *row_thr, float *corr, const int32_t *bands,
+                               int band_rows, int n_slots, double *scratch,
+                               ct_stream_t stream);
+int ct_fp_cart_correction_bands(const float *mu, const float *gather, const ct_cart_grid *grid,
+                                const ct_ray_view *views, const ct_batch *batch,
+                                const ct_sampling *sampling, const float *p_meas,
+                                const double *row_thr, float *corr, const int32_t *bands,
+                                int band_rows, int n_slots, double *scratch,
+                                ct_stream_t stream);
+int ct_fp_cyl_residual_bands(const float *mu, const float *gather, const ct_cyl_grid *grid,
+                             const ct_ray_view *views, const ct_batch *batch,
+                             const ct_sampling *sampling, const float *p_meas,
+                             const int32_t *bands, int band_rows, int n_slots, double *scratch,
+                             ct_stream_t stream);
+int ct_fp_cart_residual_bands(const float *mu, const float *gather, const ct_cart_grid *grid,
+                              const ct_ray_view *views, const ct_batch *batch,
+                              const ct_sampling *sampling, const float *p_meas,
+                              const int32_t *bands, int band_rows, int n_slots,
+                              double *scratch, ct_stream_t stream);
+/* Geometry only (ABI v8): per (view slot b, detector row) the smallest and
+ * largest FP cell layer kc any sample of the row's rays reads, cells[2 *
+ * (b * det_rows + row) + {0, 1}] (device int32, overwritten; rows without
+ * samples: INT32_MAX, INT32_MIN).  kc is the march's own fp32 h (z) cell
+ * index: the FP reads mu layers kc - 1 and kc (clamped to the grid) there,
+ * i.e. gather cells packed by ct_pack_gather_*_layers(kc_lo, kc_hi). */
+int ct_row_cells_cyl(const ct_cyl_grid *grid, const ct_ray_view *views, const ct_batch *batch,
+                     const ct_sampling *sampling, int32_t *cells, ct_stream_t stream);
+int ct_row_cells_cart(const ct_cart_grid *grid, const ct_ray_view *views, const ct_batch *batch,
+                      const ct_sampling *sampling, int32_t *cells, ct_stream_t stream);
+
 /* Geometry-only in-support sample count summed per detector row:
  * row_samples[b * det_rows + row] (uint64, overwritten), the per-row cost
  * model of the angle-sharded row split (distributed.py; ABI v6). */
@@ -319,6 +361,13 @@ int ct_pack_gather_cyl(const float *mu, const ct_cyl_grid *grid, float *gather,
                        ct_stream_t stream);
 int ct_pack_gather_cart(const float *mu, const ct_cart_grid *grid, float *gather,
                         ct_stream_t stream);
+/* (ABI v8) Pack only what FP cell layers kc in [kc_lo, kc_hi] read (see
+ * ct_row_cells_*; reads mu layers kc_lo - 1 .. kc_hi, clamped); the rest of
+ * the buffer is left as is.  ct_pack_gather_* = kc in [0, n_h] ([0, n_z]). */
+int ct_pack_gather_cyl_layers(const float *mu, const ct_cyl_grid *grid, float *gather,
+                              int32_t kc_lo, int32_t kc_hi, ct_stream_t stream);
+int ct_pack_gather_cart_layers(const float *mu, const ct_cart_grid *grid, float *gather,
+                               int32_t kc_lo, int32_t kc_hi, ct_stream_t stream);
 
 /* ---- input conversion (cyltomo/projector.py:169-181) ---------------------- */
 /* out[i] = -ln(intensity[i] / I0) with I0 = flat[i % npix] (flat != NULL, one

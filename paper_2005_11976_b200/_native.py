@@ -20,7 +20,7 @@ LIB_NAME = "libcyltomo_b200.so"
 LIB_PATH = Path(os.environ.get("CT_LIBRARY") or Path(__file__).resolve().parent / LIB_NAME)
 
 CT_OK = 0
-CT_ABI_VERSION = 7
+CT_ABI_VERSION = 8
 
 
 class CylGridC(C.Structure):
@@ -92,12 +92,32 @@ _SIGNATURES = {
                                            C.POINTER(SamplingC), P, C.c_int64, C.c_int64,
                                            C.c_int, P, P]),
     "ct_residual_sum": (C.c_int, [P, C.c_int64, P, P]),
+    "ct_fp_cyl_correction_bands": (C.c_int, [P, P, C.POINTER(CylGridC), P, C.POINTER(BatchC),
+                                             C.POINTER(SamplingC), P, P, P, P, C.c_int,
+                                             C.c_int, P, P]),
+    "ct_fp_cart_correction_bands": (C.c_int, [P, P, C.POINTER(CartGridC), P, C.POINTER(BatchC),
+                                              C.POINTER(SamplingC), P, P, P, P, C.c_int,
+                                              C.c_int, P, P]),
+    "ct_fp_cyl_residual_bands": (C.c_int, [P, P, C.POINTER(CylGridC), P, C.POINTER(BatchC),
+                                           C.POINTER(SamplingC), P, P, C.c_int, C.c_int, P,
+                                           P]),
+    "ct_fp_cart_residual_bands": (C.c_int, [P, P, C.POINTER(CartGridC), P, C.POINTER(BatchC),
+                                            C.POINTER(SamplingC), P, P, C.c_int, C.c_int, P,
+                                            P]),
+    "ct_row_cells_cyl": (C.c_int, [C.POINTER(CylGridC), P, C.POINTER(BatchC),
+                                   C.POINTER(SamplingC), P, P]),
+    "ct_row_cells_cart": (C.c_int, [C.POINTER(CartGridC), P, C.POINTER(BatchC),
+                                    C.POINTER(SamplingC), P, P]),
     "ct_gather_floats_cyl": (C.c_int64, [C.POINTER(CylGridC)]),
     "ct_gather_floats_cart": (C.c_int64, [C.POINTER(CartGridC)]),
     "ct_gather_layout_cyl": (C.c_int, [C.POINTER(CylGridC)]),
     "ct_gather_layout_cart": (C.c_int, [C.POINTER(CartGridC)]),
     "ct_pack_gather_cyl": (C.c_int, [P, C.POINTER(CylGridC), P, P]),
     "ct_pack_gather_cart": (C.c_int, [P, C.POINTER(CartGridC), P, P]),
+    "ct_pack_gather_cyl_layers": (C.c_int, [P, C.POINTER(CylGridC), P, C.c_int32, C.c_int32,
+                                            P]),
+    "ct_pack_gather_cart_layers": (C.c_int, [P, C.POINTER(CartGridC), P, C.c_int32, C.c_int32,
+                                             P]),
     "ct_rowsum_max_cyl": (C.c_int, [C.POINTER(CylGridC), P, C.POINTER(BatchC),
                                     C.POINTER(SamplingC), P, P]),
     "ct_rowsum_max_cart": (C.c_int, [C.POINTER(CartGridC), P, C.POINTER(BatchC),

@@ -101,6 +101,12 @@ struct FpArgs {
   float* const* __restrict__ peers;
   int n_peers;
   int64_t peer_off;
+  // per-view detector-row bands (slab decomposition, distributed.SlabSartRun):
+  // with bands set, view slot b marches rows [bands[2b], bands[2b+1]) only,
+  // grid z counting row tiles from bands[2b] (a multiple of the row tile, so
+  // residual partial slots stay those of the full launch); outputs land at
+  // their full-stack positions (frow_lo = 0)
+  const int32_t* __restrict__ bands;
 };
 
 // A correction value: local output, or (fused all-gather) every rank's copy
@@ -509,6 +515,12 @@ __device__ __forceinline__ FpPixel fp_pixel(const FpArgs<Geo>& a) {
   p.col = blk.x * (FP_WX * ww) + (p.warp % FP_WX) * ww + (rslot & (ww - 1));
   p.row = blk.z * (FP_WY * wh) + (p.warp / FP_WX) * wh + (rslot >> lw);
   p.b = blk.y;
+  if (a.bands) {
+    const int lo = __ldg(a.bands + 2 * p.b), hi = min(__ldg(a.bands + 2 * p.b + 1), a.rows);
+    p.row += lo;
+    p.active = p.row < hi && p.col < a.cols;
+    return p;
+  }
   const int64_t frow = (int64_t)p.b * a.rows + p.row;
   p.active = p.row < a.rows && p.col < a.cols && frow >= a.frow_lo && frow < a.frow_hi;
   return p;
@@ -618,10 +630,18 @@ __device__ __forceinline__ void fp_body(const FpArgs<Geo>& a) {
       for (int w = 1; w < FP_THREADS / 32; ++w)
         t = SUM ? t + sred[w] : fmax(t, sred[w]);
       if (SUM) {
+        // the block's row tile in the full launch (band launches start at bands[2b])
+        const unsigned zt = blockIdx.z + (a.bands ? (unsigned)__ldg(a.bands + 2 * b) /
+                                                        (unsigned)(FP_WY * tile_wh(K))
+                                                  : 0u);
         const size_t blk = a.red_rows > 0
-            ? ((size_t)blockIdx.z * a.red_rows + vid) * gridDim.x + blockIdx.x
+            ? ((size_t)zt * a.red_rows + vid) * gridDim.x + blockIdx.x
             : ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-        a.red[blk] = t;
+        // a band launch's tiles past this view's band (its grid spans the
+        // longest band) hold another band's slots: no write
+        const bool mine = !a.bands || (int)(zt * (unsigned)(FP_WY * tile_wh(K))) <
+                                          __ldg(a.bands + 2 * b + 1);
+        if (mine) a.red[blk] = t;
       } else {
         // non-negative doubles order like their bit patterns
         atomicMax(reinterpret_cast<unsigned long long*>(a.red + b),
@@ -645,6 +665,10 @@ __global__ void __launch_bounds__(1024) sum_partials_kernel(const double* __rest
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
     *accum += t;
   }
+}
+
+int fp_tile_rows(const ct_batch& b) {
+  return FP_WY * tile_wh(lanes_for(b.det_rows, b.det_cols));
 }
 
 dim3 fp_grid(const ct_batch& b) {
@@ -682,8 +706,11 @@ int launch_fp(const Geo& geo, const ct_ray_view* views, const ct_batch& b, const
               const float* p_meas, const double* thr, float* o0, float* o1, double* red,
               cudaStream_t st, int red_rows = 0, int64_t frow_lo = 0,
               int64_t frow_hi = INT64_MAX, float* const* peers = nullptr, int n_peers = 0,
-              int64_t peer_off = 0) {
+              int64_t peer_off = 0, const int32_t* bands = nullptr, int band_rows = 0) {
   FpArgs<Geo> a;
+  a.bands = bands;
+  dim3 grid = fp_grid(b);
+  if (bands) grid.z = (band_rows + fp_tile_rows(b) - 1) / fp_tile_rows(b);
   a.peers = peers;
   a.n_peers = n_peers;
   a.peer_off = peer_off;
@@ -738,20 +765,20 @@ int launch_fp(const Geo& geo, const ct_ray_view* views, const ct_batch& b, const
   a.out1 = o1;
   a.red = red;
   if (s.nearest)
-    fp_kernel<Geo, EPI, true, GL_PLAIN><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
+    fp_kernel<Geo, EPI, true, GL_PLAIN><<<grid, FP_THREADS, 0, st>>>(a);
   else if (EPI != EPI_ROWMAX && EPI != EPI_ROWCOUNT && geo.oct && geo.quad)
-    fp_kernel<Geo, EPI, false, GL_QUAD><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
+    fp_kernel<Geo, EPI, false, GL_QUAD><<<grid, FP_THREADS, 0, st>>>(a);
   else if (EPI != EPI_ROWMAX && EPI != EPI_ROWCOUNT && geo.oct && geo.obrick)
-    fp_kernel<Geo, EPI, false, GL_OCTB><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
+    fp_kernel<Geo, EPI, false, GL_OCTB><<<grid, FP_THREADS, 0, st>>>(a);
   else if (EPI != EPI_ROWMAX && EPI != EPI_ROWCOUNT && geo.oct)
   {
     if (32.0 * geo.cells_layer <= CT_FP_SMALL_LAYER_BYTES)
-      fp_kernel_small<Geo, EPI, false, GL_OCT><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
+      fp_kernel_small<Geo, EPI, false, GL_OCT><<<grid, FP_THREADS, 0, st>>>(a);
     else
-      fp_kernel<Geo, EPI, false, GL_OCT><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
+      fp_kernel<Geo, EPI, false, GL_OCT><<<grid, FP_THREADS, 0, st>>>(a);
   }
   else
-    fp_kernel<Geo, EPI, false, GL_PLAIN><<<fp_grid(b), FP_THREADS, 0, st>>>(a);
+    fp_kernel<Geo, EPI, false, GL_PLAIN><<<grid, FP_THREADS, 0, st>>>(a);
   return check_launch("fp_kernel");
 }
 
@@ -765,14 +792,14 @@ int launch_fp(const Geo& geo, const ct_ray_view* views, const ct_batch& b, const
 // the stride padding (zeroed, never read)
 template <bool BRICK>
 __global__ void pack_gather_cyl_kernel(const float* __restrict__ mu, int nh, int nt, int nr,
-                                       unsigned ks, unsigned js, float4* __restrict__ oct) {
+                                       unsigned ks, unsigned js, float4* __restrict__ oct, int kc0) {
   // cells (kc, jc, ic), kc in [0, nh], jc in [0, nt], ic in [0, nr]: corner
   // (kc-1, jc-1, ic-1); index -1 is a halo (r/h: copy of 0; theta: row nt-1).
   // Only real cells are written (the stride padding is never read).
   const unsigned rem = blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned nc = (unsigned)nr + 1u;
   if (rem >= (unsigned)(nt + 1) * nc) return;
-  const int kc = blockIdx.y;
+  const int kc = kc0 + (int)blockIdx.y;
   const int jc = (int)(rem / nc), ic = (int)(rem % nc);
   const size_t m = BRICK ? (size_t)oct_brick_index((unsigned)kc, (unsigned)jc, (unsigned)ic,
                                                    ((unsigned)nt + 2u) / 2u, (nc + 1u) / 2u)
@@ -790,12 +817,12 @@ __global__ void pack_gather_cyl_kernel(const float* __restrict__ mu, int nh, int
 
 template <bool BRICK>
 __global__ void pack_gather_cart_kernel(const float* __restrict__ mu, int nz, int ny, int nx,
-                                        unsigned ks, unsigned js, float4* __restrict__ oct) {
+                                        unsigned ks, unsigned js, float4* __restrict__ oct, int kc0) {
   // cells (kc, jc, ic) in [0, n] per axis: corner (kc-1, jc-1, ic-1)
   const unsigned rem = blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned nc = (unsigned)nx + 1u;
   if (rem >= (unsigned)(ny + 1) * nc) return;
-  const int kc = blockIdx.y;
+  const int kc = kc0 + (int)blockIdx.y;
   const int jc = (int)(rem / nc), ic = (int)(rem % nc);
   const size_t m = BRICK ? (size_t)oct_brick_index((unsigned)kc, (unsigned)jc, (unsigned)ic,
                                                    ((unsigned)ny + 2u) / 2u, (nc + 1u) / 2u)
@@ -818,11 +845,11 @@ __global__ void pack_gather_cart_kernel(const float* __restrict__ mu, int nz, in
 // trilinear_coeffs, so GL_QUAD, GL_OCT and the plain path agree bit for bit.
 template <bool CYL>
 __global__ void pack_vquad_kernel(const float* __restrict__ mu, int nk, int nj, int ni,
-                                  unsigned ks, unsigned js, float4* __restrict__ q) {
+                                  unsigned ks, unsigned js, float4* __restrict__ q, int kc0) {
   const unsigned rem = blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned nc = (unsigned)ni + 1u;
   if (rem >= (unsigned)(nj + 1) * nc) return;
-  const int kc = blockIdx.y;
+  const int kc = kc0 + (int)blockIdx.y;
   const int jc = (int)(rem / nc), ic = (int)(rem % nc);
 #if CT_QUAD_BRICK
   const size_t m = quad_brick_index((unsigned)kc, (unsigned)jc, (unsigned)ic,
@@ -931,6 +958,106 @@ int launch_row_samples(const Geo& geo, const ct_ray_view* views, const ct_batch*
     return check_launch("memset");
   return launch_fp<Geo, EPI_ROWCOUNT>(geo, views, *batch, *s, nullptr, nullptr, nullptr, nullptr,
                                       reinterpret_cast<double*>(out), CT_STREAM(stream));
+}
+
+// Band launches (slab decomposition): corrections of view slot b's rows
+// [bands[2b], bands[2b+1]) into the full [n][rows][cols] stack, with residual
+// partials at the full launch's slots when a scratch is given.
+template <class Geo>
+int fp_bands(const Geo& geo, const ct_ray_view* views, const ct_batch* batch,
+             const ct_sampling* s, const float* p_meas, const double* row_thr, float* corr,
+             const int32_t* bands, int band_rows, int n_slots, double* scratch,
+             ct_stream_t stream) {
+  if (!bands) return set_err(CT_ERR_ARG, "null bands");
+  if (band_rows < 1 || band_rows > batch->det_rows) return set_err(CT_ERR_ARG, "bad band_rows");
+  const cudaStream_t st = CT_STREAM(stream);
+  if (corr && !scratch)
+    return launch_fp<Geo, EPI_CORR>(geo, views, *batch, *s, p_meas, row_thr, corr, nullptr,
+                                    nullptr, st, 0, 0, INT64_MAX, nullptr, 0, 0, bands,
+                                    band_rows);
+  int rc = check_slots(batch, n_slots, scratch);
+  if (rc) return rc;
+  if (corr)
+    return launch_fp<Geo, EPI_CORR_RESID>(geo, views, *batch, *s, p_meas, row_thr, corr,
+                                          nullptr, scratch, st, n_slots, 0, INT64_MAX, nullptr,
+                                          0, 0, bands, band_rows);
+  return launch_fp<Geo, EPI_RESID>(geo, views, *batch, *s, p_meas, nullptr, nullptr, nullptr,
+                                   scratch, st, n_slots, 0, INT64_MAX, nullptr, 0, 0, bands,
+                                   band_rows);
+}
+
+// FP cell layers of a ray: the layer index kc = floor(fh1) of the gather
+// cell every sample reads (the march's own fp32 h index, CylGeo::locate /
+// CartGeo::locate); monotone in the sample index, so the ray's extremes are
+// its first and last samples.
+__device__ __forceinline__ int cell_layer_of(const CylGeo&, const RayF& ry, float k) {
+  return (int)(__float_as_uint(__fadd_rd(fmaf(k, ry.ih, ry.eh), 8388608.0f)) - kMagicBits);
+}
+__device__ __forceinline__ int cell_layer_of(const CartGeo& g, const RayF& ry, float k) {
+  const float fz1 = fmaf(fmaf(k, ry.iz, ry.ez), g.inv_vs, g.off1[2]);
+  return (int)(__float_as_uint(__fadd_rd(fz1, 8388608.0f)) - kMagicBits);
+}
+
+// per (view slot, detector row): [min, max] FP cell layer over the row's rays
+// and sub-rays (rows without samples keep INT_MAX / INT_MIN)
+template <class Geo>
+__global__ void row_cells_kernel(const Geo geo, const ct_ray_view* __restrict__ views,
+                                 const int32_t* __restrict__ view_ids, int rows, int cols,
+                                 int ss, double step, int* __restrict__ out) {
+  const int64_t pix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  int lo = INT_MAX, hi = INT_MIN;
+  int row = 0;
+  if (pix < (int64_t)rows * cols) {
+    row = (int)(pix / cols);
+    const int col = (int)(pix % cols);
+    const ct_ray_view& v = views[view_ids ? view_ids[b] : b];
+    for (int sv = 0; sv < ss; ++sv) {
+      const double off_v = ss == 1 ? 0.0 : dsub(ddiv((double)sv + 0.5, (double)ss), 0.5);
+      for (int su = 0; su < ss; ++su) {
+        const double off_u = ss == 1 ? 0.0 : dsub(ddiv((double)su + 0.5, (double)ss), 0.5);
+        double d[3], t0, t1;
+        subray_dir(v, dadd((double)col, off_u), dadd((double)row, off_v), d);
+        if (!geo.interval(v.src, d, t0, t1) || !(t1 > t0)) continue;
+        const int n = (int)ceil(ddiv(dsub(t1, t0), step));
+        const double ts = dadd(t0, dmul(0.5, step));
+        double e[3], inc[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          e[a] = v.src[a] + ts * d[a];
+          inc[a] = step * d[a];
+        }
+        RayF ry;
+        geo.setup_ray(e, inc, n, ry);
+        const int k0 = cell_layer_of(geo, ry, 0.0f), k1 = cell_layer_of(geo, ry, (float)(n - 1));
+        lo = min(lo, min(k0, k1));
+        hi = max(hi, max(k0, k1));
+      }
+    }
+  }
+  if (lo <= hi) {
+    atomicMin(out + 2 * ((int64_t)b * rows + row), lo);
+    atomicMax(out + 2 * ((int64_t)b * rows + row) + 1, hi);
+  }
+}
+
+__global__ void fill_cells_kernel(int* out, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (i & 1) ? INT_MIN : INT_MAX;
+}
+
+template <class Geo>
+int launch_row_cells(const Geo& geo, const ct_ray_view* views, const ct_batch* batch,
+                     const ct_sampling* s, int32_t* out, ct_stream_t stream) {
+  if (!out) return set_err(CT_ERR_ARG, "null row cells");
+  const cudaStream_t st = CT_STREAM(stream);
+  const int64_t n = 2LL * batch->n_batch * batch->det_rows;
+  fill_cells_kernel<<<blocks_for(n, 256), 256, 0, st>>>(out, n);
+  const int64_t npix = (int64_t)batch->det_rows * batch->det_cols;
+  row_cells_kernel<Geo><<<dim3(blocks_for(npix, 256), batch->n_batch), 256, 0, st>>>(
+      geo, views, batch->view_ids, batch->det_rows, batch->det_cols, s->supersample, s->step,
+      out);
+  return check_launch("row_cells_kernel");
 }
 
 }  // namespace
@@ -1103,6 +1230,78 @@ int ct_rowsum_max_cyl(const ct_cyl_grid* grid, const ct_ray_view* views, const c
                                        nullptr, max_row, CT_STREAM(stream));
 }
 
+int ct_fp_cyl_correction_bands(const float* mu, const float* gather, const ct_cyl_grid* grid,
+                               const ct_ray_view* views, const ct_batch* batch,
+                               const ct_sampling* s, const float* p_meas, const double* row_thr,
+                               float* corr, const int32_t* bands, int band_rows, int n_slots,
+                               double* scratch, ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cyl(grid))) return rc;
+  if (!mu || !p_meas || !row_thr || !corr) return set_err(CT_ERR_ARG, "null pointer");
+  CylGeo geo;
+  geo.init(mu, gather, *grid);
+  return fp_bands(geo, views, batch, s, p_meas, row_thr, corr, bands, band_rows, n_slots,
+                  scratch, stream);
+}
+
+int ct_fp_cart_correction_bands(const float* mu, const float* gather, const ct_cart_grid* grid,
+                                const ct_ray_view* views, const ct_batch* batch,
+                                const ct_sampling* s, const float* p_meas, const double* row_thr,
+                                float* corr, const int32_t* bands, int band_rows, int n_slots,
+                                double* scratch, ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cart(grid))) return rc;
+  if (!mu || !p_meas || !row_thr || !corr) return set_err(CT_ERR_ARG, "null pointer");
+  CartGeo geo;
+  geo.init(mu, gather, *grid);
+  return fp_bands(geo, views, batch, s, p_meas, row_thr, corr, bands, band_rows, n_slots,
+                  scratch, stream);
+}
+
+int ct_fp_cyl_residual_bands(const float* mu, const float* gather, const ct_cyl_grid* grid,
+                             const ct_ray_view* views, const ct_batch* batch,
+                             const ct_sampling* s, const float* p_meas, const int32_t* bands,
+                             int band_rows, int n_slots, double* scratch, ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cyl(grid))) return rc;
+  if (!mu || !p_meas || !scratch) return set_err(CT_ERR_ARG, "null pointer");
+  CylGeo geo;
+  geo.init(mu, gather, *grid);
+  return fp_bands(geo, views, batch, s, p_meas, nullptr, nullptr, bands, band_rows, n_slots,
+                  scratch, stream);
+}
+
+int ct_fp_cart_residual_bands(const float* mu, const float* gather, const ct_cart_grid* grid,
+                              const ct_ray_view* views, const ct_batch* batch,
+                              const ct_sampling* s, const float* p_meas, const int32_t* bands,
+                              int band_rows, int n_slots, double* scratch, ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cart(grid))) return rc;
+  if (!mu || !p_meas || !scratch) return set_err(CT_ERR_ARG, "null pointer");
+  CartGeo geo;
+  geo.init(mu, gather, *grid);
+  return fp_bands(geo, views, batch, s, p_meas, nullptr, nullptr, bands, band_rows, n_slots,
+                  scratch, stream);
+}
+
+int ct_row_cells_cyl(const ct_cyl_grid* grid, const ct_ray_view* views, const ct_batch* batch,
+                     const ct_sampling* s, int32_t* cells, ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cyl(grid))) return rc;
+  CylGeo geo;
+  geo.init(nullptr, nullptr, *grid);
+  return launch_row_cells(geo, views, batch, s, cells, stream);
+}
+
+int ct_row_cells_cart(const ct_cart_grid* grid, const ct_ray_view* views, const ct_batch* batch,
+                      const ct_sampling* s, int32_t* cells, ct_stream_t stream) {
+  int rc = check_batch(batch, views, s);
+  if (rc || (rc = check_cart(grid))) return rc;
+  CartGeo geo;
+  geo.init(nullptr, nullptr, *grid);
+  return launch_row_cells(geo, views, batch, s, cells, stream);
+}
+
 int ct_row_samples_cyl(const ct_cyl_grid* grid, const ct_ray_view* views, const ct_batch* batch,
                        const ct_sampling* s, uint64_t* row_samples, ct_stream_t stream) {
   int rc = check_batch(batch, views, s);
@@ -1158,7 +1357,8 @@ int ct_gather_layout_cart(const ct_cart_grid* grid) {
   return check_cart(grid) ? CT_ERR_ARG : layout_of(cells_layer_cart(*grid));
 }
 
-int ct_pack_gather_cyl(const float* mu, const ct_cyl_grid* grid, float* gather,
+static int pack_cyl_layers(const float* mu, const ct_cyl_grid* grid, float* gather,
+                             int kc_lo, int kc_hi,
                        ct_stream_t stream) {
   int rc = check_cyl(grid);
   if (rc) return rc;
@@ -1171,21 +1371,39 @@ int ct_pack_gather_cyl(const float* mu, const ct_cyl_grid* grid, float* gather,
       quad_brick_floats(grid->n_h + 2, grid->n_theta + 1, grid->n_r + 1) / 4 >= 2147483648LL)
     return set_err(CT_ERR_ARG, "gather layout too large for 32-bit brick indices");
   const unsigned nb = blocks_for((int64_t)cells, 256);
-  if (gather_quad(cells)) {
-    pack_vquad_kernel<true><<<dim3(nb, grid->n_h + 2), 256, 0, CT_STREAM(stream)>>>(
-        mu, grid->n_h, grid->n_theta, grid->n_r, cs.ks, cs.js, reinterpret_cast<float4*>(gather));
+  // FP cell layers [kc_lo, kc_hi]: GL_QUAD cells read quad layers kc, kc + 1
+  const bool q = gather_quad(cells);
+  const int k0 = max(kc_lo, 0), k1 = min(q ? kc_hi + 1 : kc_hi, grid->n_h + (q ? 1 : 0));
+  if (k1 < k0) return CT_OK;
+  const unsigned nl = (unsigned)(k1 - k0 + 1);
+  if (q) {
+    pack_vquad_kernel<true><<<dim3(nb, nl), 256, 0, CT_STREAM(stream)>>>(
+        mu, grid->n_h, grid->n_theta, grid->n_r, cs.ks, cs.js, reinterpret_cast<float4*>(gather), k0);
     return check_launch("pack_vquad_kernel");
   }
   if (gather_obrick(cells))
-    pack_gather_cyl_kernel<true><<<dim3(nb, grid->n_h + 1), 256, 0, CT_STREAM(stream)>>>(
-        mu, grid->n_h, grid->n_theta, grid->n_r, cs.ks, cs.js, reinterpret_cast<float4*>(gather));
+    pack_gather_cyl_kernel<true><<<dim3(nb, nl), 256, 0, CT_STREAM(stream)>>>(
+        mu, grid->n_h, grid->n_theta, grid->n_r, cs.ks, cs.js, reinterpret_cast<float4*>(gather), k0);
   else
-    pack_gather_cyl_kernel<false><<<dim3(nb, grid->n_h + 1), 256, 0, CT_STREAM(stream)>>>(
-        mu, grid->n_h, grid->n_theta, grid->n_r, cs.ks, cs.js, reinterpret_cast<float4*>(gather));
+    pack_gather_cyl_kernel<false><<<dim3(nb, nl), 256, 0, CT_STREAM(stream)>>>(
+        mu, grid->n_h, grid->n_theta, grid->n_r, cs.ks, cs.js, reinterpret_cast<float4*>(gather), k0);
   return check_launch("pack_gather_cyl_kernel");
 }
 
-int ct_pack_gather_cart(const float* mu, const ct_cart_grid* grid, float* gather,
+int ct_pack_gather_cyl(const float* mu, const ct_cyl_grid* grid, float* gather,
+                        ct_stream_t stream) {
+  if (!grid) return set_err(CT_ERR_ARG, "null grid");
+  return pack_cyl_layers(mu, grid, gather, 0, grid->n_h, stream);
+}
+
+int ct_pack_gather_cyl_layers(const float* mu, const ct_cyl_grid* grid, float* gather,
+                               int32_t kc_lo, int32_t kc_hi, ct_stream_t stream) {
+  if (!grid) return set_err(CT_ERR_ARG, "null grid");
+  return pack_cyl_layers(mu, grid, gather, kc_lo, kc_hi, stream);
+}
+
+static int pack_cart_layers(const float* mu, const ct_cart_grid* grid, float* gather,
+                             int kc_lo, int kc_hi,
                         ct_stream_t stream) {
   int rc = check_cart(grid);
   if (rc) return rc;
@@ -1198,18 +1416,35 @@ int ct_pack_gather_cart(const float* mu, const ct_cart_grid* grid, float* gather
       quad_brick_floats(grid->n_z + 2, grid->n_y + 1, grid->n_x + 1) / 4 >= 2147483648LL)
     return set_err(CT_ERR_ARG, "gather layout too large for 32-bit brick indices");
   const unsigned nb = blocks_for((int64_t)cells, 256);
-  if (gather_quad(cells)) {
-    pack_vquad_kernel<false><<<dim3(nb, grid->n_z + 2), 256, 0, CT_STREAM(stream)>>>(
-        mu, grid->n_z, grid->n_y, grid->n_x, cs.ks, cs.js, reinterpret_cast<float4*>(gather));
+  // FP cell layers [kc_lo, kc_hi]: GL_QUAD cells read quad layers kc, kc + 1
+  const bool q = gather_quad(cells);
+  const int k0 = max(kc_lo, 0), k1 = min(q ? kc_hi + 1 : kc_hi, grid->n_z + (q ? 1 : 0));
+  if (k1 < k0) return CT_OK;
+  const unsigned nl = (unsigned)(k1 - k0 + 1);
+  if (q) {
+    pack_vquad_kernel<false><<<dim3(nb, nl), 256, 0, CT_STREAM(stream)>>>(
+        mu, grid->n_z, grid->n_y, grid->n_x, cs.ks, cs.js, reinterpret_cast<float4*>(gather), k0);
     return check_launch("pack_vquad_kernel");
   }
   if (gather_obrick(cells))
-    pack_gather_cart_kernel<true><<<dim3(nb, grid->n_z + 1), 256, 0, CT_STREAM(stream)>>>(
-        mu, grid->n_z, grid->n_y, grid->n_x, cs.ks, cs.js, reinterpret_cast<float4*>(gather));
+    pack_gather_cart_kernel<true><<<dim3(nb, nl), 256, 0, CT_STREAM(stream)>>>(
+        mu, grid->n_z, grid->n_y, grid->n_x, cs.ks, cs.js, reinterpret_cast<float4*>(gather), k0);
   else
-    pack_gather_cart_kernel<false><<<dim3(nb, grid->n_z + 1), 256, 0, CT_STREAM(stream)>>>(
-        mu, grid->n_z, grid->n_y, grid->n_x, cs.ks, cs.js, reinterpret_cast<float4*>(gather));
+    pack_gather_cart_kernel<false><<<dim3(nb, nl), 256, 0, CT_STREAM(stream)>>>(
+        mu, grid->n_z, grid->n_y, grid->n_x, cs.ks, cs.js, reinterpret_cast<float4*>(gather), k0);
   return check_launch("pack_gather_cart_kernel");
+}
+
+int ct_pack_gather_cart(const float* mu, const ct_cart_grid* grid, float* gather,
+                        ct_stream_t stream) {
+  if (!grid) return set_err(CT_ERR_ARG, "null grid");
+  return pack_cart_layers(mu, grid, gather, 0, grid->n_z, stream);
+}
+
+int ct_pack_gather_cart_layers(const float* mu, const ct_cart_grid* grid, float* gather,
+                               int32_t kc_lo, int32_t kc_hi, ct_stream_t stream) {
+  if (!grid) return set_err(CT_ERR_ARG, "null grid");
+  return pack_cart_layers(mu, grid, gather, kc_lo, kc_hi, stream);
 }
 
 }  // extern "C"

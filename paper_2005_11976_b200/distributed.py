@@ -204,6 +204,28 @@ class GpuEngine:
     def synchronize(self):
         self.D.torch_mod().cuda.synchronize(self.device)
 
+    # -- slab decomposition (slab.SlabSartRun) -----------------------------------
+    def row_cells(self, views):
+        return self.eng.row_cells(views)
+
+    def pack_layers(self, mu, kc_lo, kc_hi) -> None:
+        self.eng.pack_layers(mu, self.gather, kc_lo, kc_hi)
+
+    def upload_bands(self, bands):
+        return self.D.upload_i32(np.ascontiguousarray(bands).reshape(-1))
+
+    def correction_bands(self, mu, slots, n, corr, bands, band_rows, n_slots, scratch):
+        self.eng.correction_bands(mu, self.p_meas, slots, n, corr, bands, band_rows, n_slots,
+                                  scratch, self.gather)
+
+    def residual_bands(self, mu, slots, n, bands, band_rows, n_slots, scratch):
+        self.eng.residual_bands(mu, self.p_meas, slots, n, bands, band_rows, n_slots, scratch,
+                                self.gather)
+
+    def poison_gather(self):
+        if self.gather is not None:
+            self.gather.fill_(float("nan"))
+
 
 class _RowShard:
     """This rank's flattened-row range of a view batch and the launch it needs."""
@@ -320,6 +342,25 @@ class ShardedSartRun:
                 if b > a:
                     out.append((int(sh.views[f0 // self.rows]), a - f0, b - f0))
         return out
+
+    def fp_rows(self, s: int) -> list:
+        """(view, fraction of its rows) this rank marches in FP launch s
+        (subset s >= 0; -1: the residual's other views; -2: subset 0)."""
+        sh = self.shards[s] if s >= 0 else (self.rest if s == -1 else self.shards[0])
+        out = []
+        for b, v in enumerate(sh.views):
+            ov = min(sh.hi, (b + 1) * self.rows) - max(sh.lo, b * self.rows)
+            if ov > 0:
+                out.append((int(v), ov / self.rows))
+        return out
+
+    def exchange_bytes(self, kind: str, s: int) -> float:
+        """Bytes this rank receives in collective `kind` of subset s."""
+        if kind == "all_gather":
+            return 4.0 * self.nvox * (self.world - 1) / self.world
+        if kind == "all_gather_corr":
+            return 4.0 * self.rows * self.cols * len(self.subsets[s]) * (self.world - 1) / self.world
+        return 0.0
 
     # views of subset s this rank marches (tests / accounting)
     @property
@@ -447,9 +488,22 @@ class ShardedSartRun:
                 ReconReport(residuals=res, wall_time=wall, config=_config_echo(self.cfg)))
 
 
-def sart_run_sharded(ps: ProjectionSet, grid, cfg: SartConfig | None = None, group=None):
-    """Angle-sharded (OS-)SART over the ranks of `group` (default: world)."""
-    return ShardedSartRun(ps, grid, cfg or SartConfig(), group).run()
+def sart_run_sharded(ps: ProjectionSet, grid, cfg: SartConfig | None = None, group=None,
+                     decomposition: str = "slab"):
+    """Angle-sharded (OS-)SART over the ranks of `group` (default: world).
+
+    decomposition "slab" (default): volume layers and per-view detector-row
+    bands per rank, halo exchanges (slab.SlabSartRun); "rows": flattened-row
+    split with all-gathers of the corrections and of mu (ShardedSartRun, the
+    one with the opt-in fused NVLink peer stores).  Both are bit-identical to
+    one GPU."""
+    cfg = cfg or SartConfig()
+    if decomposition == "slab":
+        from .slab import SlabSartRun
+        return SlabSartRun(ps, grid, cfg, group).run()
+    if decomposition == "rows":
+        return ShardedSartRun(ps, grid, cfg, group).run()
+    raise ConfigError(f"unknown decomposition {decomposition!r}")
 
 
 def assign_objects(n_objects: int, rank: int, world: int):
@@ -498,7 +552,8 @@ def _default_runner(ps, grid, cfg, group):
     if group is None:
         from .recon import SartRun
         return SartRun(ps, grid, cfg).run()
-    return ShardedSartRun(ps, grid, cfg, group).run()
+    from .slab import SlabSartRun
+    return SlabSartRun(ps, grid, cfg, group).run()
 
 
 def reconstruct_batch(items, cfg: SartConfig, rank: int | None = None,
@@ -529,3 +584,7 @@ def reconstruct_batch(items, cfg: SartConfig, rank: int | None = None,
         c = it[2] if len(it) > 2 else cfg
         out[idx] = run(it[0], it[1], c, group)
     return out
+
+
+# slab decomposition of the angle-sharded run (defined in slab.py)
+from .slab import SlabPlan, SlabSartRun, sart_run_slab  # noqa: E402,F401

@@ -326,6 +326,47 @@ class SartEngine:
                    C.byref(b), C.byref(self.gc), C.byref(upd), int(offset), int(count),
                    D.stream_handle())
 
+    # -- slab decomposition (distributed.SlabSartRun; ABI v8) ------------------
+    def row_cells(self, views) -> np.ndarray:
+        """FP cell layers [min, max] read by each detector row's rays, shape
+        (len(views), rows, 2) int32 (empty rows: INT32_MAX, INT32_MIN)."""
+        torch = D.torch_mod()
+        n = len(views)
+        out = torch.empty(2 * n * self.rows, dtype=torch.int32, device=self.device)
+        slots = D.upload_i32(views)
+        b = D.batch_c(n, self.rows, self.cols, slots)
+        fn = "ct_row_cells_cyl" if self.cyl else "ct_row_cells_cart"
+        N.call(fn, C.byref(self.gc), D.ptr(self.fp_views), C.byref(b), C.byref(self.samp),
+               D.ptr(out), D.stream_handle())
+        return D.to_host(out).reshape(n, self.rows, 2)
+
+    def pack_layers(self, mu, gather, kc_lo: int, kc_hi: int) -> None:
+        """Pack the gather cells FP cell layers kc_lo..kc_hi read."""
+        if gather is None:
+            return
+        fn = "ct_pack_gather_cyl_layers" if self.cyl else "ct_pack_gather_cart_layers"
+        N.call(fn, D.ptr(mu), C.byref(self.gc), D.ptr(gather), int(kc_lo), int(kc_hi),
+               D.stream_handle())
+
+    def correction_bands(self, mu, p_meas, slots, n: int, corr, bands, band_rows: int,
+                         n_slots: int = 0, scratch=None, gather=None) -> None:
+        """Corrections of each view slot's row band (bands: device int32
+        [n][2]) into the full [n][H][W] stack; with a scratch also the
+        residual partials at the n_slots-view slots."""
+        b = D.batch_c(n, self.rows, self.cols, slots)
+        fn = "ct_fp_cyl_correction_bands" if self.cyl else "ct_fp_cart_correction_bands"
+        N.call(fn, D.ptr(mu), D.ptr(gather), C.byref(self.gc), D.ptr(self.fp_views),
+               C.byref(b), C.byref(self.samp), D.ptr(p_meas), D.ptr(self.row_thr), D.ptr(corr),
+               D.ptr(bands), int(band_rows), int(n_slots), D.ptr(scratch), D.stream_handle())
+
+    def residual_bands(self, mu, p_meas, slots, n: int, bands, band_rows: int, n_slots: int,
+                       scratch, gather=None) -> None:
+        b = D.batch_c(n, self.rows, self.cols, slots)
+        fn = "ct_fp_cyl_residual_bands" if self.cyl else "ct_fp_cart_residual_bands"
+        N.call(fn, D.ptr(mu), D.ptr(gather), C.byref(self.gc), D.ptr(self.fp_views),
+               C.byref(b), C.byref(self.samp), D.ptr(p_meas), D.ptr(bands), int(band_rows),
+               int(n_slots), D.ptr(scratch), D.stream_handle())
+
     def residual_sum(self, scratch, accum) -> None:
         """accum += fixed-order sum of a residual scratch."""
         N.call("ct_residual_sum", D.ptr(scratch), int(scratch.numel()), D.ptr(accum),

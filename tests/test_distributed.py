@@ -101,6 +101,75 @@ class OracleEngine:
     def residual_sum(self, scratch, acc):
         acc += float(np.sum(scratch.numpy()))
 
+    # -- slab decomposition (slab.SlabSartRun) --------------------------------
+    def row_cells(self, views):
+        """numpy fp64 restatement of ct_row_cells_cyl (geometry only): per row
+        the [min, max] cell layer floor(h index + 1) of the first and last
+        samples of its rays."""
+        g = self.grid
+        step = self.o.default_step(g)
+        out = np.empty((len(views), self.H, 2), dtype=np.int64)
+        out[..., 0], out[..., 1] = 2 ** 31 - 1, -2 ** 31
+        rr, cc = np.meshgrid(np.arange(self.H), np.arange(self.W), indexing="ij")
+        for b, v in enumerate(views):
+            src, origin, du, dv = self.o.aligned_basis(g, self.ps.geom, int(v))
+            d = origin[None, None] + cc[..., None] * du + rr[..., None] * dv - src
+            d = d / np.sqrt((d * d).sum(-1))[..., None]
+            a = d[..., 0] ** 2 + d[..., 1] ** 2
+            bb = src[0] * d[..., 0] + src[1] * d[..., 1]
+            c = src[0] ** 2 + src[1] ** 2 - g.radius ** 2
+            disc = bb * bb - a * c
+            sq = np.sqrt(np.maximum(disc, 0.0))
+            tr0, tr1 = (-bb - sq) / a, (-bb + sq) / a
+            hh = 0.5 * g.height
+            tz0, tz1 = (-hh - src[2]) / d[..., 2], (hh - src[2]) / d[..., 2]
+            t0 = np.maximum(np.maximum(tr0, np.minimum(tz0, tz1)), 0.0)
+            t1 = np.minimum(tr1, np.maximum(tz0, tz1))
+            hit = (disc > 0) & (t1 > t0)
+            n = np.ceil((t1 - t0) / step)
+            z0 = src[2] + (t0 + 0.5 * step) * d[..., 2]
+            z1 = z0 + (n - 1) * step * d[..., 2]
+            k0 = np.floor(z0 * g.n_h / g.height + 0.5 * g.n_h + 0.5)
+            k1 = np.floor(z1 * g.n_h / g.height + 0.5 * g.n_h + 0.5)
+            lo = np.where(hit, np.minimum(k0, k1), 2 ** 31 - 1).min(axis=1)
+            hi = np.where(hit, np.maximum(k0, k1), -2 ** 31).max(axis=1)
+            out[b, :, 0], out[b, :, 1] = lo, hi
+        return out
+
+    def pack_layers(self, mu, kc_lo, kc_hi):
+        pass
+
+    def upload_bands(self, bands):
+        return np.asarray(bands).reshape(-1, 2)
+
+    def _band_rows(self, slots, bands):
+        for b, v in enumerate(slots):
+            for r in range(int(bands[b, 0]), int(bands[b, 1])):
+                yield b, int(v), r
+
+    def correction_bands(self, mu, slots, n, corr, bands, band_rows, n_slots, scratch):
+        cache = {}
+        for b, v, r in self._band_rows(slots[:n], bands):
+            if v not in cache:
+                c = self.o.correction(mu.numpy(), self.grid, self.ps.geom, v, self.images[v],
+                                      max_row=self.max_row[v])
+                sim, _ = self.o.forward(mu.numpy(), self.grid, self.ps.geom, v)
+                cache[v] = (c, sim)
+            c, sim = cache[v]
+            assert np.all(np.isfinite(c[r])), f"view {v} row {r} read poisoned mu"
+            corr[b, r] = self.torch.from_numpy(c[r])
+            if scratch is not None:
+                scratch[v * self.H + r] = float(np.sum((self.images[v][r] - sim[r]) ** 2))
+            self.marched.append((v, r))
+
+    def residual_bands(self, mu, slots, n, bands, band_rows, n_slots, scratch):
+        cache = {}
+        for b, v, r in self._band_rows(slots[:n], bands):
+            if v not in cache:
+                cache[v], _ = self.o.forward(mu.numpy(), self.grid, self.ps.geom, v)
+            assert np.all(np.isfinite(cache[v][r])), f"view {v} row {r} read poisoned mu"
+            scratch[v * self.H + r] = float(np.sum((self.images[v][r] - cache[v][r]) ** 2))
+
     def bp_update_range(self, corr, slots, n, offset, count, mu):
         shape = self.o.grid_shape(self.grid)
         num, den = np.zeros(shape), np.zeros(shape)
@@ -113,6 +182,8 @@ class OracleEngine:
                              num.ravel()[offset:offset + count],
                              den.ravel()[offset:offset + count], w,
                              self.cfg.relaxation, self.cfg.nonnegativity)
+        assert np.all(np.isfinite(mu.view(-1)[offset:offset + count].numpy())), \
+            "the BP update read a poisoned correction row"
         self.updated.append((offset, count))
 
 
@@ -303,3 +374,101 @@ def test_batch_plan():
     assert PD.BatchPlan(0, 8, 8).objects(3) == [0, 1, 2]
     with pytest.raises(ConfigError):
         PD.BatchPlan(0, 8, 3)
+
+
+# ---------------------------------------------------------------------------
+# slab decomposition (slab.SlabSartRun)
+# ---------------------------------------------------------------------------
+def _slab_problem():
+    """Taller grid than _problem so G ranks own slabs of several layers."""
+    import paper_2005_11976_b200 as P
+    rng = np.random.default_rng(7)
+    geom = P.ScanGeometry(400.0, 200.0, 40, 24, 0.4, (11.5, 19.5), P.full_turn_angles(9))
+    grid = P.CylGrid(24, 12, 6, 4.0, 12.0, P.Pose.tilt(0.3, 0.08, [0.2, 0.1, 0.3]))
+    truth = rng.random(grid.shape) * 0.05
+    return P, geom, grid, truth
+
+
+def _slab_worker(rank, world, port, outdir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    sys.path.insert(0, str(ROOT))
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import torch.distributed as dist
+    import oracle as orc
+    from paper_2005_11976_b200 import distributed as PD
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    P, geom, grid, truth = _slab_problem()
+    images = np.stack([orc.forward(truth, grid, geom, i)[0] for i in range(geom.n_proj)])
+    ps = P.ProjectionSet(geom, images)
+    cfg = P.SartConfig(relaxation=0.4, n_iterations=2, n_subsets=3)
+    eng = OracleEngine(orc, ps, grid, cfg)
+    run = PD.SlabSartRun(ps, grid, cfg, engine=eng, poison=True)
+    vol, rep = run.run()
+    st = run.plan.stats()
+    np.savez(Path(outdir) / f"slab{rank}.npz", mu=run.mu.numpy(), res=rep.residuals,
+             marched=np.array(eng.marched), updated=np.array(eng.updated),
+             n_sub=len(run.subsets), need=np.array(st["mu_need_layers"]),
+             sends=len(run.mu_sends))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_decomposed_os_sart_matches_single_process(oracle, tmp_path, world):
+    """Slab decomposition with every unowned value poisoned to NaN: each rank
+    marches its row bands from its window of mu, back-projects into its slab
+    from the correction rows it computed or received, and the gathered volume
+    and the residuals equal the single-process OS-SART oracle; every detector
+    row is corrected once per pass and every voxel updated once per subset."""
+    import torch.multiprocessing as mp
+    mp.start_processes(_slab_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
+                       start_method="spawn", join=True)
+    P, geom, grid, truth = _slab_problem()
+    images = np.stack([oracle.forward(truth, grid, geom, i)[0] for i in range(geom.n_proj)])
+    images = images.astype(np.float32)
+    mu_ref, res_ref = oracle.sart(images, grid, geom, relaxation=0.4, n_iterations=2,
+                                  n_subsets=3)
+    rs = [np.load(tmp_path / f"slab{r}.npz") for r in range(world)]
+    for r in rs:
+        assert np.array_equal(rs[0]["mu"], r["mu"])
+        assert np.abs(r["mu"] - mu_ref).max() <= 1e-12 * np.abs(mu_ref).max()
+        assert np.allclose(r["res"], res_ref, rtol=1e-12)
+        # locality: no rank needs the whole volume's layers
+        assert r["need"].max() < grid.n_h
+    rows = np.concatenate([r["marched"] for r in rs])
+    keys = rows[:, 0] * geom.det_rows + rows[:, 1]
+    counts = np.bincount(keys, minlength=geom.n_proj * geom.det_rows)
+    # rows with no in-support ray are marched too (they are in some band)
+    assert np.array_equal(counts, np.full(geom.n_proj * geom.det_rows, 2))
+    upd = np.concatenate([r["updated"] for r in rs])
+    assert upd[:, 1].sum() == int(np.prod(grid.shape)) * int(rs[0]["n_sub"]) * 2
+
+
+def test_slab_plan_helpers():
+    from paper_2005_11976_b200 import slab as S
+    assert list(S.slab_bounds(10, 3)) == [0, 3, 6, 10]
+    P, geom, grid, truth = _slab_problem()
+    rows = geom.det_rows
+    # the rows a slab's voxels project to: inside the detector, and growing
+    # with the slab
+    a = S.slab_rows_needed(grid, geom, 0, 0, 6, rows)
+    b = S.slab_rows_needed(grid, geom, 0, 0, 12, rows)
+    assert 0 <= a[0] < a[1] <= rows and b[0] <= a[0] and b[1] >= a[1]
+    assert S.slab_rows_needed(grid, geom, 0, 5, 5, rows) == (0, 0)
+    # a plan with synthetic cells: exchanges are symmetric between ranks
+    n_views, world = 4, 3
+    costs = np.ones((n_views, rows))
+    cells = np.zeros((n_views, rows, 2), dtype=np.int64)
+    cells[..., 0] = np.arange(rows)[None] * grid.n_h // rows
+    cells[..., 1] = cells[..., 0] + 2
+    plan = S.SlabPlan(world, grid.n_h, rows, 4, costs, cells,
+                      lambda v, k0, k1: S.slab_rows_needed(grid, geom, v, k0, k1, rows))
+    for me in range(world):
+        sends, _ = plan.mu_exchange(me)
+        for p, l0, l1 in sends:
+            _, recvs = plan.mu_exchange(p)
+            assert (me, l0, l1) in recvs
+        cs, _ = plan.corr_exchange(range(n_views), me)
+        for p, b, r0, r1 in cs:
+            _, cr = plan.corr_exchange(range(n_views), p)
+            assert (me, b, r0, r1) in cr

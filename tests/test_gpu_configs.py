@@ -298,7 +298,7 @@ def test_row_samples_match_row_sums():
             assert np.array_equal(got[i], counts.astype(np.int64))
 
 
-def _gloo_gpu_worker(rank, world, port, outdir):
+def _gloo_gpu_worker(rank, world, port, outdir, decomposition="rows"):
     """One rank of the angle-sharded driver with the production GPU engine;
     all ranks share cuda:0 and a gloo group (host-staged collectives, so no
     rank's kernels wait on another's)."""
@@ -313,7 +313,8 @@ def _gloo_gpu_worker(rank, world, port, outdir):
     from paper_2005_11976_b200 import distributed as PD
     dist.init_process_group("gloo", rank=rank, world_size=world)
     geom, grid, images, cfg = _gloo_gpu_problem(P)
-    vol, rep = PD.sart_run_sharded(P.ProjectionSet(geom, images), grid, cfg)
+    vol, rep = PD.sart_run_sharded(P.ProjectionSet(geom, images), grid, cfg,
+                                   decomposition=decomposition)
     np.savez(Path(outdir) / f"r{rank}.npz", mu=np.asarray(vol.mu), res=rep.residuals)
     dist.destroy_process_group()
 
@@ -328,8 +329,8 @@ def _gloo_gpu_problem(P):
     return geom, grid, images.astype(np.float32), cfg
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_gpu_engine_ranks_bit_identical(tmp_path, world):
+@pytest.mark.parametrize("world,decomposition", [(2, "rows"), (3, "rows"), (3, "slab")])
+def test_sharded_gpu_engine_ranks_bit_identical(tmp_path, world, decomposition):
     """The whole angle-sharded driver with the GPU engine at world 2 / 3 (ranks
     on one GPU over gloo): row-restricted uploads, cost-balanced row split,
     all-gathers, voxel-range updates and the deferred residual give the
@@ -341,7 +342,8 @@ def test_sharded_gpu_engine_ranks_bit_identical(tmp_path, world):
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
-    mp.start_processes(_gloo_gpu_worker, args=(world, port, str(tmp_path)), nprocs=world,
+    mp.start_processes(_gloo_gpu_worker, args=(world, port, str(tmp_path), decomposition),
+                       nprocs=world,
                        start_method="spawn", join=True)
     geom, grid, images, cfg = _gloo_gpu_problem(P)
     ref, rref = SartRun(P.ProjectionSet(geom, images), grid, cfg).run()

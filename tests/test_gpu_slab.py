@@ -1,0 +1,172 @@
+"""Slab decomposition on the GPU (slab.SlabSartRun, ABI v8 band / layer entry points).
+
+The kernels: band FP launches give the same corrections and residual slots
+as the full launch, the layer-range pack equals the full pack on its cells,
+and ct_row_cells_* bounds the cell layers the march reads.  The driver: the
+production GPU engine at world 2 / 3 (ranks sharing the one B200 over gloo,
+host-staged transfers, every unowned value poisoned to NaN) reproduces the
+single-GPU volume and residuals bit for bit.
+"""
+
+import socket
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2005_11976_b200 as P  # noqa: E402
+
+
+def _problem(cart=False):
+    rng = np.random.default_rng(11)
+    geom = P.ScanGeometry(400.0, 200.0, 72, 64, 0.2, (35.5, 31.5), P.full_turn_angles(12))
+    if cart == "quad":        # C5's layer size: the bricked GL_QUAD layout
+        grid = P.CylGrid(12, 1024, 384, 4.0, 8.0, P.Pose.tilt(0.4, 0.07, [0.2, -0.1, 0.3]))
+    elif cart:
+        grid = P.CartGrid.centered(20, 20, 24, 0.35)
+    else:
+        grid = P.CylGrid(32, 32, 16, 4.0, 8.0, P.Pose.tilt(0.4, 0.07, [0.2, -0.1, 0.3]))
+    truth = (rng.random(grid.shape) * 0.05).astype(np.float32)
+    vol = (P.CartVolume if cart is True else P.CylVolume)(grid, truth)
+    images = np.asarray(P.forward_project_all(vol, geom).images) * 1.03
+    return geom, grid, images.astype(np.float32)
+
+
+@pytest.mark.parametrize("cart", [False, True, "quad"])
+def test_band_launches_match_full_launch(cart):
+    """Corrections of per-view row bands (tile-aligned) land at their
+    full-stack positions with the full launch's bits, and the band launches'
+    residual partials fill the full launch's slots."""
+    from paper_2005_11976_b200.recon import SartEngine
+    from paper_2005_11976_b200 import _device as D
+    geom, grid, images = _problem(cart)
+    eng = SartEngine(grid, geom, P.RaySamplingConfig())
+    eng.prepare_thresholds()
+    n = geom.n_proj
+    mu = torch.as_tensor(np.random.default_rng(1).random(grid.shape).astype(np.float32) * 0.05,
+                         device="cuda")
+    gather = eng.alloc_gather()
+    eng.pack(mu, gather)
+    p = torch.as_tensor(images, device="cuda")
+    slots = D.upload_i32(np.arange(n))
+    full = torch.zeros((n, geom.det_rows, geom.det_cols), device="cuda")
+    eng.correction(mu, p, slots, n, full, gather)
+    scr_full = eng.residual_scratch(n).clone().zero_()
+    eng.residual_rows(mu, p, slots, n, n, scr_full, gather=gather)
+    tile = eng.row_tile()
+    H = geom.det_rows
+    rng = np.random.default_rng(2)
+    cuts = np.sort(rng.integers(0, H // tile + 1, size=(n, 2)), axis=1) * tile
+    cuts = np.minimum(cuts, H)
+    parts = [np.stack([np.zeros(n, int), cuts[:, 0]], 1), np.stack([cuts[:, 0], cuts[:, 1]], 1),
+             np.stack([cuts[:, 1], np.full(n, H)], 1)]
+    got = torch.full_like(full, float("nan"))
+    scr = torch.zeros_like(scr_full)
+    for bands in parts:
+        rows = int((bands[:, 1] - bands[:, 0]).max())
+        if rows == 0:
+            continue
+        dev = D.upload_i32(bands.reshape(-1).astype(np.int32))
+        eng.correction_bands(mu, p, slots, n, got, dev, rows, gather=gather)
+        eng.residual_bands(mu, p, slots, n, dev, rows, n, scr, gather=gather)
+    assert torch.equal(got, full)
+    assert torch.equal(scr, scr_full)
+
+
+@pytest.mark.parametrize("cart", [False, True, "quad"])
+def test_layer_pack_and_row_cells(cart):
+    """ct_pack_gather_*_layers writes exactly the full pack's cells of its
+    range; ct_row_cells_* bounds the march's cell layers: an FP through a
+    gather buffer packed only on a row's window (NaN elsewhere) is finite and
+    equal to the full-layout FP."""
+    from paper_2005_11976_b200.recon import SartEngine
+    from paper_2005_11976_b200 import _device as D
+    from paper_2005_11976_b200 import _native as N
+    import ctypes as C
+    geom, grid, images = _problem(cart)
+    eng = SartEngine(grid, geom, P.RaySamplingConfig())
+    eng.prepare_thresholds()
+    mu = torch.as_tensor(np.random.default_rng(3).random(grid.shape).astype(np.float32),
+                         device="cuda")
+    ref = eng.alloc_gather()
+    ref.fill_(float("nan"))
+    eng.pack(mu, ref)
+    if cart == "quad":
+        assert N.load_library().ct_gather_layout_cyl(C.byref(eng.gc)) == 2
+    part = torch.full_like(ref, float("nan"))
+    eng.pack_layers(mu, part, 0, grid.shape[0])      # the full range = ct_pack_gather_*
+    assert torch.equal(torch.nan_to_num(part, nan=-7.0), torch.nan_to_num(ref, nan=-7.0))
+    cells = eng.row_cells(np.arange(geom.n_proj))
+    ok = cells[..., 0] <= cells[..., 1]
+    assert ok.any() and (cells[ok, 0] >= 0).all() and (cells[ok, 1] <= grid.shape[0]).all()
+    p = torch.as_tensor(images, device="cuda")
+    H = geom.det_rows
+    full = torch.zeros((geom.n_proj, H, geom.det_cols), device="cuda")
+    slots = D.upload_i32(np.arange(geom.n_proj))
+    eng.correction(mu, p, slots, geom.n_proj, full, ref)
+    tile = eng.row_tile()
+    for r0 in range(0, H, 2 * tile):
+        r1 = min(r0 + 2 * tile, H)
+        c = cells[:, r0:r1]
+        okb = c[..., 0] <= c[..., 1]
+        if not okb.any():
+            continue
+        # the driver's window: the rows' cell layers with one layer of margin
+        lo, hi = int(c[okb, 0].min()) - 1, int(c[okb, 1].max()) + 1
+        buf = torch.full_like(ref, float("nan"))
+        eng.pack_layers(mu, buf, lo, hi)
+        bands = np.tile(np.array([r0, r1], np.int32), (geom.n_proj, 1))
+        got = torch.full_like(full, float("nan"))
+        eng.correction_bands(mu, p, slots, geom.n_proj, got, D.upload_i32(bands.reshape(-1)),
+                             r1 - r0, gather=buf)
+        assert torch.equal(got[:, r0:r1], full[:, r0:r1]), (r0, lo, hi)
+
+
+def _slab_gpu_worker(rank, world, port, outdir, cart):
+    import os
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    sys.path.insert(0, str(ROOT))
+    import torch.distributed as dist
+    import paper_2005_11976_b200 as PP
+    from paper_2005_11976_b200 import distributed as PD
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    geom, grid, images = _problem(cart)
+    cfg = PP.SartConfig(relaxation=0.4, n_iterations=3, n_subsets=3)
+    run = PD.SlabSartRun(PP.ProjectionSet(geom, images), grid, cfg, poison=True)
+    vol, rep = run.run()
+    np.savez(Path(outdir) / f"s{rank}.npz", mu=np.asarray(vol.mu), res=rep.residuals,
+             need=np.array(run.plan.stats()["mu_need_layers"]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,cart", [(2, False), (3, False), (2, True)])
+def test_slab_gpu_engine_ranks_bit_identical(tmp_path, world, cart):
+    """The slab-decomposed driver with the GPU engine at world 2 / 3 (ranks on
+    one GPU over gloo, unowned data poisoned): band FPs from window-packed
+    gather layouts, correction-row and mu-layer exchanges, slab updates and
+    the deferred residual give the single-GPU volume and residuals bit for
+    bit on every rank."""
+    import torch.multiprocessing as mp
+    from paper_2005_11976_b200.recon import SartRun
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mp.start_processes(_slab_gpu_worker, args=(world, port, str(tmp_path), cart), nprocs=world,
+                       start_method="spawn", join=True)
+    geom, grid, images = _problem(cart)
+    cfg = P.SartConfig(relaxation=0.4, n_iterations=3, n_subsets=3)
+    ref, rref = SartRun(P.ProjectionSet(geom, images), grid, cfg).run()
+    for r in range(world):
+        d = np.load(tmp_path / f"s{r}.npz")
+        assert np.array_equal(d["mu"], np.asarray(ref.mu))
+        assert list(d["res"]) == rref.residuals
+        assert d["need"].max() < grid.shape[0]
