@@ -379,17 +379,31 @@ def test_batch_plan():
 # ---------------------------------------------------------------------------
 # slab decomposition (slab.SlabSartRun)
 # ---------------------------------------------------------------------------
-def _slab_problem():
-    """Taller grid than _problem so G ranks own slabs of several layers."""
+def _slab_problem(variant="base"):
+    """Taller grid than _problem so G ranks own slabs of several layers;
+    variant "thin": 5 layers over 4 ranks (slabs of one or two layers, some
+    ranks' windows the whole volume), a weight map with zeros, a fixed
+    permutation and no nonnegativity clamp."""
     import paper_2005_11976_b200 as P
     rng = np.random.default_rng(7)
     geom = P.ScanGeometry(400.0, 200.0, 40, 24, 0.4, (11.5, 19.5), P.full_turn_angles(9))
-    grid = P.CylGrid(24, 12, 6, 4.0, 12.0, P.Pose.tilt(0.3, 0.08, [0.2, 0.1, 0.3]))
+    n_h = 5 if variant == "thin" else 24
+    grid = P.CylGrid(n_h, 12, 6, 4.0, 12.0, P.Pose.tilt(0.3, 0.08, [0.2, 0.1, 0.3]))
     truth = rng.random(grid.shape) * 0.05
     return P, geom, grid, truth
 
 
-def _slab_worker(rank, world, port, outdir):
+def _slab_cfg(P, grid, variant):
+    if variant != "thin":
+        return P.SartConfig(relaxation=0.4, n_iterations=2, n_subsets=3)
+    w = np.random.default_rng(8).uniform(0.0, 1.0, grid.shape)
+    w[w < 0.25] = 0.0
+    return P.SartConfig(relaxation=0.6, n_iterations=2, n_subsets=2, weights=w,
+                        projection_order="fixed_permutation", order_seed=3,
+                        nonnegativity=False)
+
+
+def _slab_worker(rank, world, port, outdir, variant="base"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                       WORLD_SIZE=str(world))
     sys.path.insert(0, str(ROOT))
@@ -398,10 +412,10 @@ def _slab_worker(rank, world, port, outdir):
     import oracle as orc
     from paper_2005_11976_b200 import distributed as PD
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    P, geom, grid, truth = _slab_problem()
+    P, geom, grid, truth = _slab_problem(variant)
     images = np.stack([orc.forward(truth, grid, geom, i)[0] for i in range(geom.n_proj)])
     ps = P.ProjectionSet(geom, images)
-    cfg = P.SartConfig(relaxation=0.4, n_iterations=2, n_subsets=3)
+    cfg = _slab_cfg(P, grid, variant)
     eng = OracleEngine(orc, ps, grid, cfg)
     run = PD.SlabSartRun(ps, grid, cfg, engine=eng, poison=True)
     vol, rep = run.run()
@@ -413,28 +427,32 @@ def _slab_worker(rank, world, port, outdir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_slab_decomposed_os_sart_matches_single_process(oracle, tmp_path, world):
+@pytest.mark.parametrize("world,variant", [(2, "base"), (3, "base"), (4, "thin")])
+def test_slab_decomposed_os_sart_matches_single_process(oracle, tmp_path, world, variant):
     """Slab decomposition with every unowned value poisoned to NaN: each rank
     marches its row bands from its window of mu, back-projects into its slab
     from the correction rows it computed or received, and the gathered volume
     and the residuals equal the single-process OS-SART oracle; every detector
     row is corrected once per pass and every voxel updated once per subset."""
     import torch.multiprocessing as mp
-    mp.start_processes(_slab_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
-                       start_method="spawn", join=True)
-    P, geom, grid, truth = _slab_problem()
+    mp.start_processes(_slab_worker, args=(world, _free_port(), str(tmp_path), variant),
+                       nprocs=world, start_method="spawn", join=True)
+    P, geom, grid, truth = _slab_problem(variant)
     images = np.stack([oracle.forward(truth, grid, geom, i)[0] for i in range(geom.n_proj)])
     images = images.astype(np.float32)
-    mu_ref, res_ref = oracle.sart(images, grid, geom, relaxation=0.4, n_iterations=2,
-                                  n_subsets=3)
+    cfg = _slab_cfg(P, grid, variant)
+    order = (np.random.default_rng(cfg.order_seed).permutation(geom.n_proj)
+             if cfg.projection_order == "fixed_permutation" else None)
+    mu_ref, res_ref = oracle.sart(images, grid, geom, relaxation=cfg.relaxation,
+                                  n_iterations=2, n_subsets=cfg.n_subsets, order=order,
+                                  weights=cfg.weights, nonneg=cfg.nonnegativity)
     rs = [np.load(tmp_path / f"slab{r}.npz") for r in range(world)]
     for r in rs:
         assert np.array_equal(rs[0]["mu"], r["mu"])
         assert np.abs(r["mu"] - mu_ref).max() <= 1e-12 * np.abs(mu_ref).max()
         assert np.allclose(r["res"], res_ref, rtol=1e-12)
-        # locality: no rank needs the whole volume's layers
-        assert r["need"].max() < grid.n_h
+        if variant == "base":     # locality: no rank needs the whole volume's layers
+            assert r["need"].max() < grid.n_h
     rows = np.concatenate([r["marched"] for r in rs])
     keys = rows[:, 0] * geom.det_rows + rows[:, 1]
     counts = np.bincount(keys, minlength=geom.n_proj * geom.det_rows)
