@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define CT_ABI_VERSION 8
+#define CT_ABI_VERSION 9
 
 #define CT_OK 0
 #define CT_ERR_ARG (-1)   /* invalid argument (null pointer, bad size) */
@@ -99,6 +99,10 @@ typedef struct ct_update {
     float *const *mu_peers;
     int32_t n_peers;
     int32_t _pad;
+    /* (ABI v9) NULL, or a device int64 array [n_peers][2]: voxel m goes to
+     * replica p only when peer_ranges[2p] <= m < peer_ranges[2p+1] (the
+     * slab decomposition's halo layers, slab.SlabSartRun fused mode). */
+    const int64_t *peer_ranges;
 } ct_update;
 
 /* Detector / batch description shared by the batched calls:
@@ -219,18 +223,28 @@ int ct_residual_sum(const double *scratch, int64_t n, double *accum, ct_stream_t
  * col) at corr[(b * det_rows + row) * det_cols + col] (rows outside the band
  * untouched); residual partials at the n_slots-view slots of the full launch
  * (see above), so disjoint bands of one view on different ranks fill
- * disjoint slots.  _correction_bands with a scratch: both epilogues. */
+ * disjoint slots.  _correction_bands with a scratch: both epilogues.
+ * (ABI v9) corr_peers / n_peers: the corrections are stored into every
+ * corr_peers[p] at the same full-stack position instead of into corr, and,
+ * with peer_rows (device int32 [n_batch][n_peers][2]) set, into replica p
+ * only for rows peer_rows[2 (b n_peers + p)] <= row < peer_rows[... + 1]:
+ * the exchange of the slab decomposition fused into the FP (NVLink peer
+ * stores into symmetric memory). */
 int ct_fp_cyl_correction_bands(const float *mu, const float *gather, const ct_cyl_grid *grid,
                                const ct_ray_view *views, const ct_batch *batch,
                                const ct_sampling *sampling, const float *p_meas,
                                const double *row_thr, float *corr, const int32_t *bands,
                                int band_rows, int n_slots, double *scratch,
+                               float *const *corr_peers, int n_peers,
+                               const int32_t *peer_rows,
                                ct_stream_t stream);
 int ct_fp_cart_correction_bands(const float *mu, const float *gather, const ct_cart_grid *grid,
                                 const ct_ray_view *views, const ct_batch *batch,
                                 const ct_sampling *sampling, const float *p_meas,
                                 const double *row_thr, float *corr, const int32_t *bands,
                                 int band_rows, int n_slots, double *scratch,
+                               float *const *corr_peers, int n_peers,
+                               const int32_t *peer_rows,
                                 ct_stream_t stream);
 int ct_fp_cyl_residual_bands(const float *mu, const float *gather, const ct_cyl_grid *grid,
                              const ct_ray_view *views, const ct_batch *batch,

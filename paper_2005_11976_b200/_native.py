@@ -20,7 +20,7 @@ LIB_NAME = "libcyltomo_b200.so"
 LIB_PATH = Path(os.environ.get("CT_LIBRARY") or Path(__file__).resolve().parent / LIB_NAME)
 
 CT_OK = 0
-CT_ABI_VERSION = 8
+CT_ABI_VERSION = 9
 
 
 class CylGridC(C.Structure):
@@ -52,7 +52,8 @@ class SamplingC(C.Structure):
 class UpdateC(C.Structure):
     _fields_ = [("relaxation", C.c_float), ("nonneg", C.c_int32),
                 ("weights", C.c_void_p), ("mu", C.c_void_p),
-                ("mu_peers", C.c_void_p), ("n_peers", C.c_int32), ("_pad", C.c_int32)]
+                ("mu_peers", C.c_void_p), ("n_peers", C.c_int32), ("_pad", C.c_int32),
+                ("peer_ranges", C.c_void_p)]
 
 
 class BatchC(C.Structure):
@@ -94,10 +95,10 @@ _SIGNATURES = {
     "ct_residual_sum": (C.c_int, [P, C.c_int64, P, P]),
     "ct_fp_cyl_correction_bands": (C.c_int, [P, P, C.POINTER(CylGridC), P, C.POINTER(BatchC),
                                              C.POINTER(SamplingC), P, P, P, P, C.c_int,
-                                             C.c_int, P, P]),
+                                             C.c_int, P, P, C.c_int, P, P]),
     "ct_fp_cart_correction_bands": (C.c_int, [P, P, C.POINTER(CartGridC), P, C.POINTER(BatchC),
                                               C.POINTER(SamplingC), P, P, P, P, C.c_int,
-                                              C.c_int, P, P]),
+                                              C.c_int, P, P, C.c_int, P, P]),
     "ct_fp_cyl_residual_bands": (C.c_int, [P, P, C.POINTER(CylGridC), P, C.POINTER(BatchC),
                                            C.POINTER(SamplingC), P, P, C.c_int, C.c_int, P,
                                            P]),

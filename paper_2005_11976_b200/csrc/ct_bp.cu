@@ -510,8 +510,14 @@ __global__ void __launch_bounds__(BP_THREADS, TMA ? 4 : BP_MIN_BLOCKS) bp_kernel
       if (a.upd.nonneg) mu = fmaxf(mu, 0.0f);
       if (a.upd.n_peers > 0) {
         // all-gather of the updated shard fused into the update: every
-        // rank's replica gets the voxel (NVLink peer stores)
-        for (int p = 0; p < a.upd.n_peers; ++p) a.upd.mu_peers[p][m] = mu;
+        // rank's replica gets the voxel (NVLink peer stores); with
+        // peer_ranges only the replicas whose range holds it (slab halos)
+        for (int p = 0; p < a.upd.n_peers; ++p) {
+          if (a.upd.peer_ranges && ((int64_t)m < __ldg(a.upd.peer_ranges + 2 * p) ||
+                                    (int64_t)m >= __ldg(a.upd.peer_ranges + 2 * p + 1)))
+            continue;
+          a.upd.mu_peers[p][m] = mu;
+        }
       } else {
         a.upd.mu[m] = mu;
       }

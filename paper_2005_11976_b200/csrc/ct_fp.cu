@@ -107,14 +107,25 @@ struct FpArgs {
   // residual partial slots stay those of the full launch); outputs land at
   // their full-stack positions (frow_lo = 0)
   const int32_t* __restrict__ bands;
+  // per-peer row ranges of the peer stores (slab decomposition, fused): with
+  // peer_rows set, view slot b's row `row` goes to peer p only when
+  // peer_rows[2 (b n_peers + p)] <= row < peer_rows[2 (b n_peers + p) + 1]
+  const int32_t* __restrict__ peer_rows;
 };
 
 // A correction value: local output, or (fused all-gather) every rank's copy
 // of the gathered stack over NVLink peer stores.
 template <class Geo>
-__device__ __forceinline__ void store_corr(const FpArgs<Geo>& a, size_t oidx, float c) {
+__device__ __forceinline__ void store_corr(const FpArgs<Geo>& a, size_t oidx, float c, int b,
+                                           int row) {
   if (a.n_peers > 0) {
-    for (int p = 0; p < a.n_peers; ++p) a.peers[p][a.peer_off + (int64_t)oidx] = c;
+    for (int p = 0; p < a.n_peers; ++p) {
+      if (a.peer_rows) {
+        const int* r = a.peer_rows + 2 * ((size_t)b * a.n_peers + p);
+        if (row < __ldg(r) || row >= __ldg(r + 1)) continue;
+      }
+      a.peers[p][a.peer_off + (int64_t)oidx] = c;
+    }
   } else {
     a.out0[oidx] = c;
   }
@@ -597,7 +608,7 @@ __device__ __forceinline__ void fp_body(const FpArgs<Geo>& a) {
         const float pm = a.p_meas[(size_t)vid * npix + pix];
         c = (pm - (float)p64) / (float)w64;
       }
-      store_corr(a, oidx, c);
+      store_corr(a, oidx, c, b, row);
     }
   } else {
     double x = 0.0;
@@ -608,7 +619,7 @@ __device__ __forceinline__ void fp_body(const FpArgs<Geo>& a) {
         const float pm = a.p_meas[(size_t)vid * npix + pix];
         float c = 0.0f;
         if (w64 > a.row_thr[vid]) c = (pm - (float)p64) / (float)w64;
-        store_corr(a, oidx, c);
+        store_corr(a, oidx, c, b, row);
         const double r = (double)pm - (double)(float)p64;
         x = r * r;
       } else if (EPI == EPI_RESID) {
@@ -706,9 +717,11 @@ int launch_fp(const Geo& geo, const ct_ray_view* views, const ct_batch& b, const
               const float* p_meas, const double* thr, float* o0, float* o1, double* red,
               cudaStream_t st, int red_rows = 0, int64_t frow_lo = 0,
               int64_t frow_hi = INT64_MAX, float* const* peers = nullptr, int n_peers = 0,
-              int64_t peer_off = 0, const int32_t* bands = nullptr, int band_rows = 0) {
+              int64_t peer_off = 0, const int32_t* bands = nullptr, int band_rows = 0,
+              const int32_t* peer_rows = nullptr) {
   FpArgs<Geo> a;
   a.bands = bands;
+  a.peer_rows = peer_rows;
   dim3 grid = fp_grid(b);
   if (bands) grid.z = (band_rows + fp_tile_rows(b) - 1) / fp_tile_rows(b);
   a.peers = peers;
@@ -967,20 +980,22 @@ template <class Geo>
 int fp_bands(const Geo& geo, const ct_ray_view* views, const ct_batch* batch,
              const ct_sampling* s, const float* p_meas, const double* row_thr, float* corr,
              const int32_t* bands, int band_rows, int n_slots, double* scratch,
-             ct_stream_t stream) {
+             ct_stream_t stream, float* const* peers = nullptr, int n_peers = 0,
+             const int32_t* peer_rows = nullptr) {
   if (!bands) return set_err(CT_ERR_ARG, "null bands");
   if (band_rows < 1 || band_rows > batch->det_rows) return set_err(CT_ERR_ARG, "bad band_rows");
+  if (n_peers < 0 || (n_peers > 0 && !peers)) return set_err(CT_ERR_ARG, "bad peer list");
   const cudaStream_t st = CT_STREAM(stream);
   if (corr && !scratch)
     return launch_fp<Geo, EPI_CORR>(geo, views, *batch, *s, p_meas, row_thr, corr, nullptr,
-                                    nullptr, st, 0, 0, INT64_MAX, nullptr, 0, 0, bands,
-                                    band_rows);
+                                    nullptr, st, 0, 0, INT64_MAX, peers, n_peers, 0, bands,
+                                    band_rows, peer_rows);
   int rc = check_slots(batch, n_slots, scratch);
   if (rc) return rc;
   if (corr)
     return launch_fp<Geo, EPI_CORR_RESID>(geo, views, *batch, *s, p_meas, row_thr, corr,
-                                          nullptr, scratch, st, n_slots, 0, INT64_MAX, nullptr,
-                                          0, 0, bands, band_rows);
+                                          nullptr, scratch, st, n_slots, 0, INT64_MAX, peers,
+                                          n_peers, 0, bands, band_rows, peer_rows);
   return launch_fp<Geo, EPI_RESID>(geo, views, *batch, *s, p_meas, nullptr, nullptr, nullptr,
                                    scratch, st, n_slots, 0, INT64_MAX, nullptr, 0, 0, bands,
                                    band_rows);
@@ -1234,28 +1249,30 @@ int ct_fp_cyl_correction_bands(const float* mu, const float* gather, const ct_cy
                                const ct_ray_view* views, const ct_batch* batch,
                                const ct_sampling* s, const float* p_meas, const double* row_thr,
                                float* corr, const int32_t* bands, int band_rows, int n_slots,
-                               double* scratch, ct_stream_t stream) {
+                               double* scratch, float* const* corr_peers,
+    int n_peers, const int32_t* peer_rows, ct_stream_t stream) {
   int rc = check_batch(batch, views, s);
   if (rc || (rc = check_cyl(grid))) return rc;
   if (!mu || !p_meas || !row_thr || !corr) return set_err(CT_ERR_ARG, "null pointer");
   CylGeo geo;
   geo.init(mu, gather, *grid);
   return fp_bands(geo, views, batch, s, p_meas, row_thr, corr, bands, band_rows, n_slots,
-                  scratch, stream);
+                  scratch, stream, corr_peers, n_peers, peer_rows);
 }
 
 int ct_fp_cart_correction_bands(const float* mu, const float* gather, const ct_cart_grid* grid,
                                 const ct_ray_view* views, const ct_batch* batch,
                                 const ct_sampling* s, const float* p_meas, const double* row_thr,
                                 float* corr, const int32_t* bands, int band_rows, int n_slots,
-                                double* scratch, ct_stream_t stream) {
+                                double* scratch, float* const* corr_peers,
+    int n_peers, const int32_t* peer_rows, ct_stream_t stream) {
   int rc = check_batch(batch, views, s);
   if (rc || (rc = check_cart(grid))) return rc;
   if (!mu || !p_meas || !row_thr || !corr) return set_err(CT_ERR_ARG, "null pointer");
   CartGeo geo;
   geo.init(mu, gather, *grid);
   return fp_bands(geo, views, batch, s, p_meas, row_thr, corr, bands, band_rows, n_slots,
-                  scratch, stream);
+                  scratch, stream, corr_peers, n_peers, peer_rows);
 }
 
 int ct_fp_cyl_residual_bands(const float* mu, const float* gather, const ct_cyl_grid* grid,

@@ -198,6 +198,9 @@ class GpuEngine:
             self._upd = make_update(mu, self.weights, self.cfg)
             if peers:
                 self._upd.mu_peers, self._upd.n_peers = int(peers[0]), int(peers[1])
+                if len(peers) > 2 and peers[2] is not None:      # per-replica voxel ranges
+                    self._upd_ranges = peers[2]
+                    self._upd.peer_ranges = peers[2].data_ptr()
         self.eng.pack_quads(corr, n, self.quads)
         self.eng.bp_update_range(corr, slots, n, self._upd, offset, count, self.quads)
 
@@ -214,9 +217,11 @@ class GpuEngine:
     def upload_bands(self, bands):
         return self.D.upload_i32(np.ascontiguousarray(bands).reshape(-1))
 
-    def correction_bands(self, mu, slots, n, corr, bands, band_rows, n_slots, scratch):
+    def correction_bands(self, mu, slots, n, corr, bands, band_rows, n_slots, scratch,
+                         peers=None):
+        pp, npeer, rows = peers if peers else (None, 0, None)
         self.eng.correction_bands(mu, self.p_meas, slots, n, corr, bands, band_rows, n_slots,
-                                  scratch, self.gather)
+                                  scratch, self.gather, pp, npeer, rows)
 
     def residual_bands(self, mu, slots, n, bands, band_rows, n_slots, scratch):
         self.eng.residual_bands(mu, self.p_meas, slots, n, bands, band_rows, n_slots, scratch,

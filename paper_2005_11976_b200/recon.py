@@ -349,15 +349,20 @@ class SartEngine:
                D.stream_handle())
 
     def correction_bands(self, mu, p_meas, slots, n: int, corr, bands, band_rows: int,
-                         n_slots: int = 0, scratch=None, gather=None) -> None:
+                         n_slots: int = 0, scratch=None, gather=None, peers=None,
+                         n_peers: int = 0, peer_rows=None) -> None:
         """Corrections of each view slot's row band (bands: device int32
         [n][2]) into the full [n][H][W] stack; with a scratch also the
-        residual partials at the n_slots-view slots."""
+        residual partials at the n_slots-view slots.  peers (device pointer
+        array) / n_peers / peer_rows (device int32 [n][n_peers][2]): stored
+        into the peers' stacks instead, each for its row range."""
         b = D.batch_c(n, self.rows, self.cols, slots)
         fn = "ct_fp_cyl_correction_bands" if self.cyl else "ct_fp_cart_correction_bands"
         N.call(fn, D.ptr(mu), D.ptr(gather), C.byref(self.gc), D.ptr(self.fp_views),
                C.byref(b), C.byref(self.samp), D.ptr(p_meas), D.ptr(self.row_thr), D.ptr(corr),
-               D.ptr(bands), int(band_rows), int(n_slots), D.ptr(scratch), D.stream_handle())
+               D.ptr(bands), int(band_rows), int(n_slots), D.ptr(scratch),
+               C.c_void_p(int(peers) if peers else 0), int(n_peers), D.ptr(peer_rows),
+               D.stream_handle())
 
     def residual_bands(self, mu, p_meas, slots, n: int, bands, band_rows: int, n_slots: int,
                        scratch, gather=None) -> None:

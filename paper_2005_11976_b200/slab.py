@@ -243,7 +243,18 @@ class SlabSartRun:
         shape = tuple(grid.shape)
         self.n_layers = shape[0]
         self.layer = int(shape[1] * shape[2])
-        self.mu = self.e.tensor(shape)
+        # fused exchanges (opt-in, CT_FUSED_COMM=1, NCCL groups): mu and the
+        # correction stack live in symmetric memory; the FP epilogue stores
+        # each correction into every rank whose BP needs its row and the BP
+        # update each voxel into every rank whose FP window holds its layer
+        # (NVLink peer stores), and device barriers replace the P2P exchanges
+        self.fused = (os.environ.get("CT_FUSED_COMM", "0") == "1" and engine is None
+                      and dist.get_backend(group) == "nccl")
+        if self.fused:
+            self.poison = False
+            self.mu = self._symm_tensor(int(np.prod(shape))).view(shape)
+        else:
+            self.mu = self.e.tensor(shape)
         if cfg.initial is not None:
             self.mu.copy_(_initial_mu(grid, cfg, self.mu.device).to(self.mu.device))
         self.order = projection_order(cfg, ps.geom.n_proj)
@@ -270,7 +281,9 @@ class SlabSartRun:
             pieces += self.rest.rows_marched
         if hasattr(self.e, "upload_rows"):
             self.e.upload_rows(None if not multi else sorted(set(pieces)))
-        self.corr = self.e.tensor((max(len(s) for s in self.subsets), rows, cols))
+        nmax = max(len(s) for s in self.subsets)
+        self.corr = (self._symm_tensor(nmax * rows * cols).view(nmax, rows, cols) if self.fused
+                     else self.e.tensor((nmax, rows, cols)))
         self.scratch = self.e.scratch(n_proj)
         self.red = self.e.scratch(n_proj)
         self.resid = self.e.tensor(cfg.n_iterations, "float64")
@@ -284,10 +297,57 @@ class SlabSartRun:
             # its communicator there; P2P batches need it to exist)
             dist.all_reduce(self.acc, group=group)
             self.acc.zero_()
+        if self.fused:
+            self._setup_fused()
         if self.poison:
             self._poison_mu()
             if hasattr(self.e, "poison_gather"):
                 self.e.poison_gather()
+
+    # -- fused exchanges (symmetric memory) -----------------------------------
+    def _symm_tensor(self, n):
+        import torch
+        import torch.distributed._symmetric_memory as symm_mem
+        t = symm_mem.empty(n, dtype=torch.float32, device=self.e.device)
+        t.zero_()
+        return t
+
+    def _setup_fused(self):
+        """Rendezvous, the per-peer store tables, and a barrier so that no
+        rank's first peer store lands before every replica is initialised."""
+        import torch
+        import torch.distributed._symmetric_memory as symm_mem
+        g = self.group if self.group is not None else _dist().group.WORLD
+        self._h_corr = symm_mem.rendezvous(self.corr.view(-1), g)
+        self._h_mu = symm_mem.rendezvous(self.mu.view(-1), g)
+        me, world = self.rank, self.world
+        dev = self.mu.device
+        for sb in self.sub:
+            t = np.zeros((sb.n, world, 2), dtype=np.int32)
+            for b, v in enumerate(sb.views):
+                a0, a1 = self.plan.band(int(v), me)
+                for p in range(world):
+                    if p == me:
+                        t[b, p] = (a0, a1)
+                    else:
+                        q0, q1 = (int(x) for x in self.plan.need[p, int(v)])
+                        lo, hi = max(a0, q0), min(a1, q1)
+                        t[b, p] = (lo, hi) if hi > lo else (0, 0)
+            sb.peer_rows = torch.as_tensor(t.reshape(-1), device=dev)
+        r = np.zeros((world, 2), dtype=np.int64)
+        for p in range(world):
+            if p == me:
+                r[p] = (0, self.n_layers * self.layer)
+            else:
+                lo = max(self.k0, int(self.plan.mu_need[p, 0]))
+                hi = min(self.k1, int(self.plan.mu_need[p, 1]))
+                r[p] = (lo * self.layer, hi * self.layer) if hi > lo else (0, 0)
+        self._mu_ranges = torch.as_tensor(r.reshape(-1), device=dev)
+        self._h_corr.barrier()
+        self._h_mu.barrier()
+
+    def _corr_peers(self, sb):
+        return ((self._h_corr.buffer_ptrs_dev, self.world, sb.peer_rows),) if self.fused else ()
 
     # -- accounting (bench.py) ------------------------------------------------
     @property
@@ -367,22 +427,30 @@ class SlabSartRun:
         if self.poison:
             self.corr[:sb.n].fill_(float("nan"))
         fused = s == 0 and self._pending is not None
+        peers = self._corr_peers(sb)
         if sb.band_rows > 0:
             if fused:
                 self._timed("fp_correction_resid", s, self.e.correction_bands, self.mu,
                             sb.slots, sb.n, self.corr, sb.bands, sb.band_rows, n_proj,
-                            self.scratch)
+                            self.scratch, *peers)
             else:
                 self._timed("fp_correction", s, self.e.correction_bands, self.mu, sb.slots,
-                            sb.n, self.corr, sb.bands, sb.band_rows, 0, None)
+                            sb.n, self.corr, sb.bands, sb.band_rows, 0, None, *peers)
         if fused:
             self._finish_residual()
-        if self.world > 1:
+        if self.fused:           # every rank's peer stores of the corrections are done
+            self._timed("barrier_corr", s, self._h_corr.barrier)
+        elif self.world > 1:
             self._timed("exchange_corr", s, self._exchange_corr, sb)
+        mu_peers = ((self._h_mu.buffer_ptrs_dev, self.world, self._mu_ranges),) \
+            if self.fused else ()
         if self.k1 > self.k0:
             self._timed("bp_update", s, self.e.bp_update_range, self.corr[:sb.n], sb.slots,
-                        sb.n, self.k0 * self.layer, (self.k1 - self.k0) * self.layer, self.mu)
-        if self.world > 1:
+                        sb.n, self.k0 * self.layer, (self.k1 - self.k0) * self.layer, self.mu,
+                        *mu_peers)
+        if self.fused:           # every slab's halo layers are in the replicas needing them
+            self._timed("barrier_mu", s, self._h_mu.barrier)
+        elif self.world > 1:
             self._timed("exchange_mu", s, self._exchange_mu)
         if self.poison:
             self._poison_mu()

@@ -53,10 +53,10 @@ def test_struct_layouts_match_header(tmp_path):
           printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(ct_cyl_grid), sizeof(ct_cart_grid),
                  sizeof(ct_ray_view), sizeof(ct_det_view), sizeof(ct_sampling),
                  sizeof(ct_update), sizeof(ct_batch));
-          printf("%zu %zu %zu %zu %zu %zu\\n", offsetof(ct_cyl_grid, rot),
+          printf("%zu %zu %zu %zu %zu %zu %zu\\n", offsetof(ct_cyl_grid, rot),
                  offsetof(ct_cyl_grid, t), offsetof(ct_update, weights),
                  offsetof(ct_batch, view_ids), offsetof(ct_update, mu_peers),
-                 offsetof(ct_update, n_peers));
+                 offsetof(ct_update, n_peers), offsetof(ct_update, peer_ranges));
           return 0;
         }"""))
     exe = tmp_path / "probe"
@@ -70,7 +70,8 @@ def test_struct_layouts_match_header(tmp_path):
     assert [int(x) for x in offs.split()] == [N.CylGridC.rot.offset, N.CylGridC.t.offset,
                                              N.UpdateC.weights.offset, N.BatchC.view_ids.offset,
                                              N.UpdateC.mu_peers.offset,
-                                             N.UpdateC.n_peers.offset]
+                                             N.UpdateC.n_peers.offset,
+                                             N.UpdateC.peer_ranges.offset]
 
 
 def test_argument_errors_return_status_not_crash():

@@ -170,3 +170,107 @@ def test_slab_gpu_engine_ranks_bit_identical(tmp_path, world, cart):
         assert np.array_equal(d["mu"], np.asarray(ref.mu))
         assert list(d["res"]) == rref.residuals
         assert d["need"].max() < grid.shape[0]
+
+
+def test_peer_stores_follow_their_ranges():
+    """The fused exchange's kernel side with three local buffers standing in
+    for the ranks' symmetric-memory replicas: the band FP stores each
+    correction into exactly the replicas whose row range holds its row, the
+    BP update each voxel into exactly the replicas whose voxel range holds
+    it, with the plain launches' values."""
+    from paper_2005_11976_b200.recon import SartEngine, make_update
+    from paper_2005_11976_b200 import _device as D
+    geom, grid, images = _problem()
+    cfg = P.SartConfig(relaxation=0.4)
+    eng = SartEngine(grid, geom, cfg.sampling)
+    eng.prepare_thresholds()
+    n, H, W = geom.n_proj, geom.det_rows, geom.det_cols
+    rng = np.random.default_rng(5)
+    mu = torch.as_tensor(rng.random(grid.shape).astype(np.float32) * 0.05, device="cuda")
+    gather = eng.alloc_gather()
+    eng.pack(mu, gather)
+    p = torch.as_tensor(images, device="cuda")
+    slots = D.upload_i32(np.arange(n))
+    tile = eng.row_tile()
+    bands = np.tile(np.array([tile, H - tile], np.int32), (n, 1))
+    bdev = D.upload_i32(bands.reshape(-1))
+    ref = torch.full((n, H, W), float("nan"), device="cuda")
+    eng.correction_bands(mu, p, slots, n, ref, bdev, H - 2 * tile, gather=gather)
+    k = 3
+    reps = [torch.full((n, H, W), float("nan"), device="cuda") for _ in range(k)]
+    ptrs = torch.tensor([t.data_ptr() for t in reps], dtype=torch.int64, device="cuda")
+    rows = np.sort(rng.integers(0, H + 1, size=(n, k, 2)), axis=2).astype(np.int32)
+    local = torch.full((n, H, W), float("nan"), device="cuda")
+    eng.correction_bands(mu, p, slots, n, local, bdev, H - 2 * tile, gather=gather,
+                         peers=ptrs.data_ptr(), n_peers=k,
+                         peer_rows=D.upload_i32(rows.reshape(-1)))
+    assert torch.isnan(local).all()      # with peers the stores go to the replicas only
+    for q in range(k):
+        got = reps[q].cpu().numpy()
+        want = ref.cpu().numpy()
+        for b in range(n):
+            lo, hi = max(rows[b, q, 0], tile), min(rows[b, q, 1], H - tile)
+            inside = np.zeros(H, bool)
+            inside[lo:hi] = True
+            assert np.array_equal(got[b, inside], want[b, inside])
+            assert np.isnan(got[b, ~inside]).all()
+    # BP update: voxel ranges per replica
+    corr = torch.nan_to_num(ref, nan=0.0)
+    quads = eng.alloc_quads(n)
+    eng.pack_quads(corr, n, quads)
+    mu_ref = mu.clone()
+    upd = make_update(mu_ref, None, cfg)
+    eng.bp_update(corr, slots, n, upd, quads)
+    nvox = mu.numel()
+    mreps = [torch.full_like(mu, -1.0) for _ in range(k)]
+    mptrs = torch.tensor([t.data_ptr() for t in mreps], dtype=torch.int64, device="cuda")
+    ranges = np.sort(rng.integers(0, nvox + 1, size=(k, 2)), axis=1).astype(np.int64)
+    ranges[0] = (0, nvox)
+    rdev = torch.as_tensor(ranges.reshape(-1), device="cuda")
+    src = mu.clone()
+    upd2 = make_update(src, None, cfg)
+    upd2.mu_peers, upd2.n_peers, upd2.peer_ranges = mptrs.data_ptr(), k, rdev.data_ptr()
+    eng.bp_update(corr, slots, n, upd2, quads)
+    changed = (mu_ref != mu).cpu().numpy().ravel()
+    assert changed.any()
+    want = mu_ref.cpu().numpy().ravel()
+    for q in range(k):
+        got = mreps[q].cpu().numpy().ravel()
+        sel = np.zeros(nvox, bool)
+        sel[ranges[q, 0]:ranges[q, 1]] = True
+        # stored: the updated value wherever the update touched the voxel
+        assert np.array_equal(got[sel & changed], want[sel & changed])
+        assert (got[~sel] == -1.0).all()
+    assert torch.equal(src, mu)          # the source replica is read, never written
+
+
+@pytest.mark.parametrize("fused", ["0", "1"])
+def test_slab_run_on_one_rank_group_matches_single_gpu(monkeypatch, fused):
+    """The slab driver on a 1-rank NCCL group gives the single-GPU result;
+    fused="1": corrections and voxels stored into the symmetric-memory
+    replicas by the kernels, device barriers instead of the P2P exchanges."""
+    monkeypatch.setenv("CT_FUSED_COMM", fused)
+    import os
+    import torch.distributed as dist
+    from paper_2005_11976_b200 import distributed as PD
+    from paper_2005_11976_b200.recon import SartRun
+    if dist.is_initialized():
+        pytest.skip("process group already initialised")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        geom, grid, images = _problem()
+        ps = P.ProjectionSet(geom, images)
+        cfg = P.SartConfig(relaxation=0.4, n_iterations=2, n_subsets=3)
+        run = PD.SlabSartRun(ps, grid, cfg)
+        assert run.fused == (fused == "1")
+        a, ra = run.run()
+        b, rb = SartRun(ps, grid, cfg).run()
+        assert np.array_equal(np.asarray(a.mu), np.asarray(b.mu))
+        assert ra.residuals == rb.residuals
+    finally:
+        dist.destroy_process_group()
