@@ -212,10 +212,11 @@ def c5_object(obj: int, n_views: int = 120) -> Workload:
         spheres.append(_rand_sphere(rng, 2.0, 10.0, float(rng.uniform(0.5, 1.5)), 0.0, 2.0))
     pose = random_tilt_pose(rng, 10.0, 5.0)
     grid = CylGrid(512, 1024, 384, RADIUS, HEIGHT, pose)
+    phantom = Phantom(base.shells, spheres)
     return Workload(f"c5_obj{obj}", grid, geometry(n_views, 1024, 0.08, 300.0, 600.0),
-                    rasterize_cyl(Phantom(base.shells, spheres), grid), n_iterations=15,
+                    rasterize_cyl(phantom, grid), n_iterations=15,
                     relaxation=0.3, n_subsets=6, seed=5000 + obj,
-                    extra={"template_phantom": base})
+                    extra={"template_phantom": base, "phantom": phantom})
 
 
 def c5_template() -> np.ndarray:
