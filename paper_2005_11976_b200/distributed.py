@@ -5,7 +5,13 @@ reference is single-process; the sharding follows the
 north_star and SURVEY.md §8e, with the exchange chosen to move the fewest
 bytes:
 
-* **angle sharding** -- within OS-SART subset s (n views of H x W pixels)
+* **angle sharding, slab decomposition** (the default, :mod:`slab`): each
+  rank owns a slab of mu's layers and a detector-row band of every view,
+  packs only its FP window and exchanges by NCCL P2P only the correction
+  rows and mu layers other ranks need (or stores them into their replicas
+  from the kernels, CT_FUSED_COMM=1);
+* **angle sharding, flattened-row split** (:class:`ShardedSartRun`) --
+  within OS-SART subset s (n views of H x W pixels)
   the subset's rays are split by flattened detector row f = b*H + row into G
   contiguous ranges at FP block tiles (ct_fp_row_tile), balanced by the
   rows' in-support sample counts (ct_row_samples_*), so each rank marches
