@@ -15,6 +15,11 @@ results are committed (tests/test_gpu_iterations.py reads them):
 * golden_c3_iter.npz -- BASELINE configs[2] (C3): 30 views, per-view SART,
   weight map (1.0 ROI / 0.2), template initial volume, lambda 0.5, TWO
   passes (SURVEY.md §8c's plan); the same kinds of samples.
+* golden_c5_iter.npz -- BASELINE configs[4] (C5), object 0: (512,1024,384)
+  grid, 120 views on 1024^2, ONE full OS-SART iteration (6 subsets, lambda
+  0.3) from the shared template (~40 min on 8 cores); 20,000 voxel samples
+  (half seeded, half where the update from the template is largest), the
+  h layer with the largest update, the pass residual.
 
 The phantoms, poses and weight maps are pure functions of committed seeded
 code (paper_2005_11976_b200.workloads); their sha256 is stored so a drift in
@@ -92,6 +97,29 @@ def c3():
                         mu_sha=sha(mu, np.float64), phantom_sha=sha(wl.mu),
                         weights_sha=sha(wl.weights), template_sha=sha(wl.template),
                         images_sha=sha(imgs), norm=np.linalg.norm(mu))
+
+
+def c5():
+    wl = W.c5_object(0)
+    template = W.c5_template()
+    imgs = oracle_projections(wl)
+    t = time.time()
+    mu, res = orc.sart(imgs, wl.grid, wl.geom, relaxation=wl.relaxation, n_iterations=1,
+                       n_subsets=wl.n_subsets, initial=template)
+    print(f"  C5 OS-SART iteration {time.time() - t:.0f} s, residual {res}", flush=True)
+    upd = np.abs(mu - template).reshape(-1)
+    rng = np.random.default_rng(5)
+    top = np.argpartition(upd, -N_SAMPLES // 2)[-N_SAMPLES // 2:]
+    rest = np.setdiff1d(np.arange(mu.size), top)
+    idx = np.sort(np.concatenate([top, rng.choice(rest, N_SAMPLES // 2, replace=False)]))
+    # the h layer the update from the template is largest in (the changed inclusion)
+    layer = int(np.argmax(np.abs(mu - template).sum(axis=(1, 2))))
+    np.savez_compressed(OUT / "golden_c5_iter.npz", residuals=np.array(res), idx=idx,
+                        val=mu.reshape(-1)[idx], layers=np.array([layer]),
+                        layer_mu=mu[[layer]].astype(np.float32),
+                        mu_sha=sha(mu, np.float64), phantom_sha=sha(wl.mu),
+                        template_sha=sha(template), images_sha=sha(imgs),
+                        norm=np.linalg.norm(mu))
 
 
 if __name__ == "__main__":

@@ -93,3 +93,31 @@ def test_c3_two_weighted_template_passes_vs_oracle_golden():
     assert rel_l2(d_layers, g["layer_mu"].astype(np.float64) - wl.template[g["layers"]]) \
         < RECON_TOL
     assert np.allclose(rep.residuals, g["residuals"], rtol=RECON_TOL)
+
+
+def test_c5_full_os_sart_iteration_vs_oracle_golden():
+    """BASELINE configs[4] (the headline workload), object 0: ONE complete
+    OS-SART iteration (6 subsets of 20 views on 1024^2, lambda 0.3, from the
+    shared template, residual FP) through the production path (bricked
+    GL_QUAD layout, quad BP) vs the oracle: the update from the template at
+    20,000 voxels (half of them where it is largest), over the whole h layer
+    where it is largest, and the pass residual."""
+    g = load("golden_c5_iter.npz")
+    wl = W.c5_object(0)
+    template = W.c5_template()
+    assert sha(wl.mu) == str(g["phantom_sha"])
+    assert sha(template) == str(g["template_sha"])
+    vol = P.CylVolume(wl.grid, dev(wl.mu))
+    ps = P.forward_project_all(vol, wl.geom)
+    del vol
+    t = dev(template)
+    cfg = P.SartConfig(relaxation=wl.relaxation, n_iterations=1, n_subsets=wl.n_subsets,
+                       initial=P.CylVolume(wl.grid, t))
+    out, rep = P.sart_run(ps, wl.grid, cfg)
+    mu = out.mu
+    start = _samples(t, g)
+    assert rel_l2(_samples(mu, g) - start, g["val"] - start) < RECON_TOL
+    li = torch.as_tensor(g["layers"], device="cuda")
+    d_layer = (mu[li] - t[li]).cpu().numpy()
+    assert rel_l2(d_layer, g["layer_mu"].astype(np.float64) - template[g["layers"]]) < RECON_TOL
+    assert rep.residuals[0] == pytest.approx(float(g["residuals"][0]), rel=RECON_TOL)
