@@ -345,6 +345,11 @@ class SlabSartRun:
         self._mu_ranges = torch.as_tensor(r.reshape(-1), device=dev)
         self._h_corr.barrier()
         self._h_mu.barrier()
+        if world > 1:
+            import warnings
+            warnings.warn("CT_FUSED_COMM=1 with more than one rank: the slab peer stores are "
+                          "verified with local replicas and on 1-rank groups only",
+                          RuntimeWarning, stacklevel=3)
 
     def _corr_peers(self, sb):
         return ((self._h_corr.buffer_ptrs_dev, self.world, sb.peer_rows),) if self.fused else ()
