@@ -95,9 +95,7 @@ def configure_threads(n: int | None) -> None:
     cyltomo/cli.py:45-53): here the cap applies to the host worker pool that
     stages pageable projections (recon._stage_pool) and to torch's intra-op
     threads; the GPU kernels are unaffected."""
-    if n is None:
-        env = os.environ.get("CYLTOMO_THREADS")
-        n = int(env) if env else None
+    n = n if n is not None else (os.environ.get("CYLTOMO_THREADS") or None)
     if n is None:
         return
     n = max(1, int(n))
@@ -126,13 +124,11 @@ GEOMETRY_SCHEMA = {
 
 def geometry_from_config(d: dict) -> ScanGeometry:
     """(cyltomo/cli.py:83-101)"""
-    if "stage_angles_rad" in d:
+    if "stage_angles_rad" in d:                 # an explicit geometry document
         return ScanGeometry.from_dict(d)
     n_views = int(d.get("n_views", 21))
-    if d.get("full_turn", False):
-        angles = full_turn_angles(n_views)
-    else:
-        angles = make_circular_trajectory(n_views, math.radians(d.get("last_angle_deg", 200.0)))
+    angles = (full_turn_angles(n_views) if d.get("full_turn", False) else
+              make_circular_trajectory(n_views, math.radians(d.get("last_angle_deg", 200.0))))
     cols, rows = int(d.get("det_cols", 96)), int(d.get("det_rows", 192))
     pp = d.get("principal_point_px")
     return ScanGeometry(float(d.get("sdd_mm", 791.0)), float(d.get("sod_mm", 679.0)), cols, rows,
@@ -201,22 +197,24 @@ RECON_SCHEMA = {
 }
 
 
+# pose-parameter keys of a config document: (key, converter, default); the
+# reference's names and defaults (cyltomo/cli.py:143-158)
+_POSE_KEYS = (("threshold_level", None, "auto"), ("threshold_levels", int, 1),
+              ("threshold_span", float, 0.0), ("dilation_radius", int, 0), ("band", int, 1),
+              ("nuisance_level", None, None), ("nuisance_dilation", int, 2),
+              ("exclude_rects", lambda v: tuple(tuple(r) for r in v), ()),
+              ("estimate_gamma", bool, False), ("strip_offset", float, 0.0),
+              ("strip_width", float, 1.0))
+
+
 def pose_params_from_config(d: dict) -> PoseFitParams:
-    """(cyltomo/cli.py:143-158)"""
-    lm = LmConfig(**d.get("lm", {})) if d.get("lm") else LmConfig()
-    return PoseFitParams(
-        threshold_level=d.get("threshold_level", "auto"),
-        threshold_levels=int(d.get("threshold_levels", 1)),
-        threshold_span=float(d.get("threshold_span", 0.0)),
-        dilation_radius=int(d.get("dilation_radius", 0)),
-        band=int(d.get("band", 1)),
-        nuisance_level=d.get("nuisance_level"),
-        nuisance_dilation=int(d.get("nuisance_dilation", 2)),
-        exclude_rects=tuple(tuple(r) for r in d.get("exclude_rects", [])),
-        estimate_gamma=bool(d.get("estimate_gamma", False)),
-        strip_offset=float(d.get("strip_offset", 0.0)),
-        strip_width=float(d.get("strip_width", 1.0)),
-        lm=lm)
+    """PoseFitParams from a config document (cyltomo/cli.py:143-158)."""
+    kw = {}
+    for key, conv, default in _POSE_KEYS:
+        v = d.get(key, default)
+        kw[key] = conv(v) if (conv is not None and key in d) else v
+    kw["lm"] = LmConfig(**d["lm"]) if d.get("lm") else LmConfig()
+    return PoseFitParams(**kw)
 
 
 # the reference DeviceSpec's pose parameters (cyltomo/experiments.py:219-223):
